@@ -1,0 +1,167 @@
+/*
+ * packedconv.h -- C ABI of the B200 (sm_100a) packed approximate overlap-save convolution.
+ *
+ * Implements the hot path of Anam & Andreopoulos, "Throughput Scaling Of Convolution For
+ * Error-Tolerant Multimedia Applications" (arXiv 1201.3018; PAPER.md cited P:<line>):
+ * per overlap-save block, uniform companding to integers (Eq. (2)), tight packing of
+ * several integers into one binary64 word (symmetric Eqs. (4)-(5), or asymmetric
+ * Eq. (7)), a direct FP64 convolution of the packed words (Eqs. (8)-(9)),
+ * unpacking (Eqs. (11)-(15)), inverse companding (Eq. (16)) and output
+ * placement (Eq. (17)).  Readings of the paper where it is ambiguous are listed in
+ * DESIGN.md §3 (codes C1..C17).
+ *
+ * Conventions for every entry point
+ *  - Pointers named *_dev are CUDA device pointers; *_host are host pointers (pinned
+ *    memory recommended).  The caller owns every buffer passed in; the plan owns its own
+ *    device memory (packed kernels, scratch) and frees it in conv_plan_destroy.
+ *  - Device buffers of samples must be 16-byte aligned for the TMA bulk-copy path;
+ *    misaligned buffers take a slower plain-load path with identical results.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  All
+ *    execution entry points are stream-ordered and asynchronous unless stated.
+ *  - One plan may be used by one stream at a time (it owns scratch state).
+ *  - No exception or C++ type crosses this boundary.  Every int-returning call returns a
+ *    PC_* status code; conv_status_string() names it.
+ *  - There is no CPU fallback: without a CUDA device every call that would launch work
+ *    returns PC_E_CUDA.
+ */
+#ifndef PACKEDCONV_H
+#define PACKEDCONV_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (SPEC.md S:522 exit codes 0/2/3/4, plus CUDA and margin) ---------- */
+enum {
+  PC_OK = 0,
+  PC_E_CONFIG = 2,          /* invalid geometry / arguments ("config error")        */
+  PC_E_BOUND = 3,           /* R_max exceeds the packing's bound under STRICT      */
+  PC_E_BACKEND = 4,         /* backend validation failure                          */
+  PC_E_CUDA = 5,            /* a CUDA runtime call failed / no device                     */
+  PC_W_UNPACK_MARGIN = 6,   /* warning: digit residual exceeded 0.25 LSB (FFT core)        */
+  PC_E_STATE = 7            /* call order violated (e.g. execute before set_kernel)        */
+};
+
+/* ---- enumerations -------------------------------------------------------------------- */
+enum { PC_MODE_CONV = 0, PC_MODE_XCORR = 1 };              /* P:31 Eq.(1); P:189 xcorr   */
+enum { PC_PACK_FULL = 0, PC_PACK_SYM = 1, PC_PACK_ASYM2 = 2, PC_PACK_ASYM3 = 3,
+       PC_PACK_ADAPTIVE = 4 };                             /* P:59 options (i)-(iii)      */
+enum { PC_EPS_PAPER = 0, PC_EPS_RADIX = 1, PC_EPS_POW2 = 2 };   /* Eq.(6); C2; C4         */
+enum { PC_RMAX_PAPER = 0, PC_RMAX_L1 = 1 };                /* Eq.(3); C3                  */
+enum { PC_BOUND_STRICT = 0, PC_BOUND_WARN = 1 };
+enum { PC_CORE_DIRECT = 0, PC_CORE_FFT = 1 };              /* Tier-2 core          */
+enum { PC_EXEC_FUSED = 0, PC_EXEC_STAGED = 1 };            /* one kernel vs G1->G2->G4    */
+
+/* Plan options.  conv_opts_default() fills: eps_rule POW2, rmax_rule PAPER, bound_policy
+ * STRICT, core DIRECT, exec FUSED, K_q 0 (= Q), device -1 (current), u_sys 3.1193e-11. */
+typedef struct conv_opts {
+  int32_t eps_rule;
+  int32_t rmax_rule;
+  int32_t bound_policy;
+  int32_t core;
+  int32_t exec;
+  int32_t K_q;              /* kernel companding range; 0 means K_q = S_q = Q       */
+  int32_t device;           /* CUDA device ordinal, -1 = current device                    */
+  int32_t reserved[9];
+  double u_sys;             /* P:153; used only by the literal paper unpack form          */
+} conv_opts;
+
+/* Read-only plan description (conv_plan_query). */
+typedef struct conv_plan_info {
+  int64_t L;                /* input samples                                               */
+  int64_t L_out;            /* output samples: L+N-1 (conv) or L-N+1 valid lags (xcorr)   */
+  int64_t P;                /* overlap-save blocks, ceil(L/W)                        */
+  int32_t N, Np;            /* kernel taps; N' = N or N+1 (odd)                       */
+  int32_t W_block, W;       /* block samples; outputs per block W = W_block - N' - 1 */
+  int32_t mode, packing;
+  int32_t Q, K_q;           /* S_q and K_q                                           */
+  int32_t taps;             /* taps of the convolution core: ceil(N'/2) (sym) or N'        */
+  int32_t kernel_set;       /* 1 after conv_plan_set_kernel succeeded                      */
+  int64_t R_max;            /* Eq. (3) or the L1 rule (C3)                                  */
+  int64_t bound;            /* Table 1 bound (PAPER/RADIX eps) or dyadic bound (POW2)      */
+  int32_t bound_ok;         /* R_max <= bound                                               */
+  int32_t eps_b;            /* eps = 2^-eps_b under POW2, else 0                            */
+  double eps, eps_inv;      /* packing coefficient (Eq. (6) / C2 / C4) and its inverse     */
+  double c_k, k_peak;       /* kernel companding factor and ||k||_inf                */
+  int64_t packed_stride;    /* per-block stride (words) of the debug packed-word dump      */
+  int64_t rbar_stride;      /* per-block stride (words) of the debug packed-output dump    */
+  int64_t rint_stride;      /* per-block stride of the debug integer dump (= W + N' - 1)   */
+  int32_t q_mode[4];        /* ADAPTIVE: max Q per packing under its bound          */
+} conv_plan_info;
+
+/* Per-block decision of conv_adapt_block. */
+typedef struct conv_block_decision {
+  int32_t packing;          /* PC_PACK_SYM / ASYM2 / ASYM3 / FULL                           */
+  int32_t Q;                /* S_q = K_q used for the block (0 for FULL)                    */
+  double snr_lin;           /* Eq. (19) linear prediction (inf for FULL)                    */
+} conv_block_decision;
+
+typedef struct conv_plan conv_plan;
+
+void conv_opts_default(conv_opts* opts);
+
+/* Create a plan for an L-sample input and an N-tap kernel in W_block-sample overlap-save
+ * blocks.  mode: PC_MODE_*; packing: PC_PACK_*; Q = S_q >= 1 (ignored for
+ * FULL).  Geometry: N' = N | 1; W = W_block - N' - 1 must be even and >= 2N'.
+ * Returns PC_E_CONFIG on invalid arguments, PC_E_CUDA if no device. *out is NULL on error. */
+int conv_plan_create(conv_plan** out, int64_t L, int32_t N, int32_t W_block, int32_t mode,
+                     int32_t packing, int32_t Q, const conv_opts* opts);
+
+/* Install the N-tap kernel (device pointer, N doubles).  Performs the paper's
+ * Initialization on the device: pad to N' (C13), reverse for xcorr,
+ * ||k||_inf, c_k = K_q/||k||_inf, k~ = [[c_k k]] (Eq. (2)), R_max (Eq. (3) / C3), eps
+ * (Eq. (6) / C2 / C4), bound check (Table 1), packed kernel (Eq. (5) under C1, or
+ * k~ for asymmetric, Eq. (8)).  Synchronizes `stream` (one-time plan cost).
+ * Returns PC_E_BOUND under STRICT when R_max exceeds the bound (kernel not installed). */
+int conv_plan_set_kernel(conv_plan* plan, const double* k_dev, void* stream);
+
+/* Run the whole hot path on an L-sample device input, writing L_out device outputs:
+ * r_out (Eq. (17)) for conv, or the valid cross-correlation lags c[j] = sum_n s[j+n] q[n],
+ * 0 <= j <= L-N, for xcorr (C17). */
+int conv_execute(conv_plan* plan, const double* s_dev, double* r_dev, void* stream);
+
+/* Same as conv_execute restricted to blocks [block_begin, block_end) -- the unit of
+ * multi-GPU sharding.  s_dev holds global samples [s_offset, ...) (the
+ * block range plus its N'+1-sample halo); r_dev receives global outputs [r_offset, ...). */
+int conv_execute_blocks(conv_plan* plan, const double* s_dev, int64_t s_offset, double* r_dev,
+                        int64_t r_offset, int64_t block_begin, int64_t block_end, void* stream);
+
+/* n_signals independent signals of L samples (row stride s_stride doubles) through the
+ * same plan; outputs row stride r_stride doubles.  One launch over all blocks. */
+int conv_execute_batch(conv_plan* plan, const double* s_dev, int64_t n_signals, int64_t s_stride,
+                       double* r_dev, int64_t r_stride, void* stream);
+
+/* End-to-end through host memory: copies s_host (L doubles) to the device, runs
+ * conv_execute, copies L_out doubles back to r_host, and synchronizes `stream`. */
+int conv_execute_host(conv_plan* plan, const double* s_host, double* r_host, void* stream);
+
+/* xcorr plans only: per signal, the maximum of c[j] over valid lags and its argmax
+ * (lowest j on ties; C17) -- the music-matching score. */
+int conv_xcorr_max(conv_plan* plan, const double* db_dev, int64_t n_signals, int64_t s_stride,
+                   double* score_dev, int64_t* lag_dev, void* stream);
+
+/* Parity/debug run of the whole path that also dumps, per block w (row w of each array,
+ * strides from conv_plan_info; any pointer may be NULL): packed words as the core sees
+ * them (Eq. (4)/(7)), packed outputs (Eq. (9)/(8)), unpacked integers of the kept range
+ * (Eqs. (12)-(15)), and c_s (Eq. (2)).  r_dev as in conv_execute (may be NULL). */
+int conv_execute_debug(conv_plan* plan, const double* s_dev, double* r_dev, double* packed_dev,
+                       double* rbar_dev, int64_t* rint_dev, double* c_s_dev, void* stream);
+
+/* SNR-constrained adaptation for ADAPTIVE plans: per block, the first
+ * packing of {SYM, ASYM2} whose Eq. (19) prediction at its maximum Q under its bound
+ * meets snr_floor_db - calib_offset_db, else FULL.  Decisions are installed for the next
+ * conv_execute on the same input and copied to out_host (P entries) if non-NULL.
+ * Synchronizes `stream`. */
+int conv_adapt_block(conv_plan* plan, const double* s_dev, double snr_floor_db,
+                     double calib_offset_db, conv_block_decision* out_host, void* stream);
+
+int conv_plan_query(const conv_plan* plan, conv_plan_info* info);
+void conv_plan_destroy(conv_plan* plan);
+const char* conv_status_string(int status);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PACKEDCONV_H */

@@ -553,3 +553,25 @@ def flop_count(packing, domain, N):
             SYM: (22.5 * N + 7.5) * lg(3 * N + 1) + 5 * N + 1,
             ASYM2: (30 * N + 15) * lg(2 * N + 1) + 19.5 * N + 6.5,
             ASYM3: (25 * N + 15) * lg(5.0 / 3.0 * N + 1) + 62.0 / 3.0 * N + 7}[packing]
+
+
+def adaptive_pipeline(s, k, W_block, floor_db, calib_offset_db=0.0, candidates=(SYM, ASYM2),
+                      eps_rule=EPS_POW2, rmax_rule=RMAX_L1):
+    """§IV.D end to end: per-block decisions (adapt_decisions), then each
+    block runs the per-block loop with its chosen packing at that packing's Q (kernel
+    companded once per packing).  Returns (output, decisions, qmode)."""
+    s = np.asarray(s, dtype=np.float64)
+    dec, qmode = adapt_decisions(s, k, W_block, floor_db, calib_offset_db, candidates, eps_rule, rmax_rule)
+    geom = Geometry(s.shape[0], len(k), W_block)
+    states = {m: prepare_kernel(k, geom, m, qmode[m], None, CONV, eps_rule, rmax_rule)
+              for m in candidates if qmode[m] >= 1}
+    states[FULL] = prepare_kernel(k, geom, FULL, 0)
+    y = np.zeros(geom.L_out)
+    for w, (m, Q, _) in enumerate(dec):
+        br = process_block(s, w, geom, states[m], Q)
+        g0 = geom.block_start(w)
+        o0, n_out = geom.kept(w)
+        n = min(n_out, geom.L_out - (g0 + o0))
+        if n > 0:
+            y[g0 + o0:g0 + o0 + n] = br.out[:n]
+    return y, dec, qmode

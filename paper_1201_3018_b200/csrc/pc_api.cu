@@ -1,0 +1,665 @@
+// pc_api.cu -- the C ABI of include/packedconv.h: plan geometry, kernel initialization,
+// bound policy and launch orchestration.  All numeric work runs in pc_kernels.cu.
+#include <cmath>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+
+#include <cuda_runtime.h>
+
+#include "../../include/packedconv.h"
+#include "pc_kernels.h"
+
+using pc::Exec;
+using pc::Geo;
+using pc::ModeP;
+
+namespace {
+
+constexpr size_t kMaxSmem = 232448;      // 227 KB dynamic shared memory per CTA (sm_100)
+constexpr size_t kStageSmemCap = 116224; // stage raw blocks only while 2 CTAs/SM still fit
+
+struct ModeState {
+  int valid = 0;
+  int Q = 0, K_q = 0;
+  long long R = 0, bound = 0;
+  int bound_ok = 0;
+  double eps = 0, eps_inv = 0;
+  int b = 0;
+  double c_k = 1.0;
+  double* kr = nullptr;
+  int K = 0, K_pad = 0, rows = 0;
+};
+
+}  // namespace
+
+struct conv_plan {
+  long long L = 0, P = 0;
+  int N = 0, Np = 0, W_block = 0, W = 0;
+  int mode = 0, packing = 0, Q = 0, K_q = 0;
+  conv_opts opts;
+  int device = 0;
+  int kernel_set = 0;
+  double k_peak = 0, k_sigma = 0;
+  ModeState ms[4];
+  int qmode[4] = {0, 0, 0, 0};
+  double* d_k_pad = nullptr;
+  double* d_k_int = nullptr;
+  double* d_scal = nullptr;
+  // adaptive decisions (per block)
+  int* d_dec_pack = nullptr;
+  int* d_dec_q = nullptr;
+  double* d_dec_snr = nullptr;
+  double* d_sigma = nullptr;
+  double* d_peak = nullptr;
+  int* d_cand = nullptr;
+  int adapt_ready = 0;
+  // host end-to-end staging
+  double* d_in = nullptr;
+  double* d_out = nullptr;
+  // xcorr scratch
+  double* d_xc = nullptr;
+  size_t d_xc_bytes = 0;
+};
+
+namespace {
+
+int n_digits(int p) { return p == PC_PACK_ASYM2 ? 2 : 3; }
+
+// Reading C4: eps = 2^-b exact iff R(2^{2b}+2^b+1) < 2^53 (3 digits) / R(2^b+1) < 2^53.
+bool pow2_exact(long long R, int digits) {
+  if (R < 1) return true;
+  const int b = 64 - __builtin_clzll((unsigned long long)(2 * R));
+  if (b > 40) return false;
+  unsigned __int128 span = digits == 3 ? (((unsigned __int128)1 << (2 * b)) + ((unsigned __int128)1 << b) + 1)
+                                       : (((unsigned __int128)1 << b) + 1);
+  return (unsigned __int128)R * span < ((unsigned __int128)1 << 53);
+}
+long long pow2_bound(int digits) {
+  long long lo = 1, hi = 1LL << 40;
+  while (lo < hi) {
+    const long long mid = lo + (hi - lo + 1) / 2;
+    if (pow2_exact(mid, digits)) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+// Table 1 for the paper's eps; the dyadic exactness bound for POW2.
+long long bound_for(int packing, int eps_rule) {
+  if (eps_rule == PC_EPS_POW2) return pow2_bound(n_digits(packing));
+  return packing == PC_PACK_ASYM2 ? 43165096LL : 97667LL;
+}
+
+int core_taps(const conv_plan* p, int packing) { return packing == PC_PACK_SYM ? (p->Np + 1) / 2 : p->Np; }
+
+Geo make_geo(const conv_plan* p) {
+  Geo g;
+  g.L = p->L;
+  g.P = p->P;
+  g.N = p->N;
+  g.Np = p->Np;
+  g.W_block = p->W_block;
+  g.W = p->W;
+  g.mode = p->mode;
+  return g;
+}
+
+template <int PACK>
+void max_core_sizes(const Geo& g, int K, int* m_out_max, int* m_out_typ) {
+  const pc::Blk b0 = pc::block_info<PACK>(g, K, 0);
+  const pc::Blk b1 = pc::block_info<PACK>(g, K, 1);
+  *m_out_max = b0.M_out > b1.M_out ? b0.M_out : b1.M_out;
+  *m_out_typ = g.P > 1 ? b1.M_out : b0.M_out;
+}
+void core_sizes(const conv_plan* p, int packing, int* mmax, int* mtyp) {
+  const Geo g = make_geo(p);
+  const int K = core_taps(p, packing);
+  switch (packing) {
+    case PC_PACK_SYM: max_core_sizes<pc::PACK_SYM>(g, K, mmax, mtyp); break;
+    case PC_PACK_ASYM2: max_core_sizes<pc::PACK_ASYM2>(g, K, mmax, mtyp); break;
+    case PC_PACK_ASYM3: max_core_sizes<pc::PACK_ASYM3>(g, K, mmax, mtyp); break;
+    default: max_core_sizes<pc::PACK_FULL>(g, K, mmax, mtyp); break;
+  }
+}
+
+void set_core_layout(const conv_plan* p, int packing, ModeState* m) {
+  int mmax, mtyp;
+  core_sizes(p, packing, &mmax, &mtyp);
+  m->K = core_taps(p, packing);
+  m->K_pad = (m->K + pc::kT - 1) / pc::kT * pc::kT;
+  const int ngroups = (mmax + pc::kT - 1) / pc::kT;
+  m->rows = ngroups + m->K_pad / pc::kT + 1;
+  m->rows = (m->rows + 1) & ~1;   // keep each column 16-byte aligned
+}
+
+// Launch shape of the fused kernel for the packings that may run in this plan.
+struct Shape {
+  int threads;
+  int stage_raw;
+  size_t smem;
+};
+bool launch_shape(const conv_plan* p, const int* packs, int npacks, Shape* sh) {
+  size_t core = 0;
+  int mmax_all = 0, groups_typ = 0;
+  for (int i = 0; i < npacks; ++i) {
+    const ModeState& m = p->ms[packs[i]];
+    int mmax, mtyp;
+    core_sizes(p, packs[i], &mmax, &mtyp);
+    const size_t c = (size_t)pc::kT * m.rows * 8 + (size_t)m.K_pad * 8;
+    if (c > core) core = c;
+    if (mmax > mmax_all) mmax_all = mmax;
+    const int gt = (mtyp + pc::kT - 1) / pc::kT;
+    if (gt > groups_typ) groups_typ = gt;
+  }
+  const size_t staged = pc::kSmemHeader + (size_t)p->W_block * 8 + core;
+  const size_t unstaged = pc::kSmemHeader + core + (size_t)mmax_all * 8 + 16;
+  if (staged <= kStageSmemCap) {
+    sh->stage_raw = 1;
+    sh->smem = staged;
+  } else if (unstaged <= kMaxSmem) {
+    sh->stage_raw = 0;
+    sh->smem = unstaged;
+  } else {
+    return false;
+  }
+  const int iters = (groups_typ + pc::kMaxThreads - 1) / pc::kMaxThreads;
+  int t = (groups_typ + iters - 1) / iters;
+  t = (t + 31) / 32 * 32;
+  if (t < 64) t = 64;
+  if (t > pc::kMaxThreads) t = pc::kMaxThreads;
+  sh->threads = t;
+  return true;
+}
+
+int cuda_status(cudaError_t e) { return e == cudaSuccess ? PC_OK : PC_E_CUDA; }
+
+void fill_modep(const ModeState& m, ModeP* mp) {
+  mp->kr = m.kr;
+  mp->Q = (double)m.Q;
+  mp->c_k = m.c_k;
+  mp->eps = m.eps;
+  mp->eps_inv = m.eps_inv;
+  mp->pow2 = m.b > 0;
+  mp->K = m.K;
+  mp->K_pad = m.K_pad;
+  mp->rows = m.rows;
+}
+
+// The packings a plan's launches may use.
+int plan_packs(const conv_plan* p, int* packs) {
+  if (p->packing == PC_PACK_ADAPTIVE) {
+    packs[0] = PC_PACK_SYM;
+    packs[1] = PC_PACK_ASYM2;
+    packs[2] = PC_PACK_FULL;
+    return 3;
+  }
+  packs[0] = p->packing;
+  return 1;
+}
+
+int run_fused(conv_plan* p, const double* s, long long s_off, long long s_stride, double* r, long long r_off,
+              long long r_stride, long long b0, long long nblk, long long n_sig, Exec* dbg, cudaStream_t st) {
+  if (!p->kernel_set) return PC_E_STATE;
+  if (p->packing == PC_PACK_ADAPTIVE && !p->adapt_ready) return PC_E_STATE;
+  if (nblk <= 0 || n_sig <= 0) return PC_OK;
+  int packs[4];
+  const int np = plan_packs(p, packs);
+  Shape sh;
+  if (!launch_shape(p, packs, np, &sh)) return PC_E_CONFIG;
+  Exec e;
+  std::memset(&e, 0, sizeof(e));
+  if (dbg) e = *dbg;
+  e.s = s;
+  e.s_off = s_off;
+  e.s_stride = s_stride;
+  e.r = r;
+  e.r_off = r_off;
+  e.r_stride = r_stride;
+  e.b0 = b0;
+  e.nblk = nblk;
+  e.stage_raw = sh.stage_raw;
+  for (int i = 0; i < np; ++i) fill_modep(p->ms[packs[i]], &e.mp[packs[i]]);
+  e.dec_pack = p->packing == PC_PACK_ADAPTIVE ? p->d_dec_pack : nullptr;
+  const int launch_pack = p->packing == PC_PACK_ADAPTIVE ? -1 : p->packing;
+  return cuda_status(pc::launch_fused(launch_pack, make_geo(p), e, nblk * n_sig, sh.threads, sh.smem, st));
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+void conv_opts_default(conv_opts* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->eps_rule = PC_EPS_POW2;
+  o->rmax_rule = PC_RMAX_PAPER;
+  o->bound_policy = PC_BOUND_STRICT;
+  o->core = PC_CORE_DIRECT;
+  o->exec = PC_EXEC_FUSED;
+  o->K_q = 0;
+  o->device = -1;
+  o->u_sys = 3.1193e-11;
+}
+
+const char* conv_status_string(int s) {
+  switch (s) {
+    case PC_OK: return "ok";
+    case PC_E_CONFIG: return "config error";
+    case PC_E_BOUND: return "companding range exceeds the packing bound";
+    case PC_E_BACKEND: return "backend validation failure";
+    case PC_E_CUDA: return "CUDA error";
+    case PC_W_UNPACK_MARGIN: return "unpack margin warning";
+    case PC_E_STATE: return "invalid call order";
+  }
+  return "unknown status";
+}
+
+int conv_plan_create(conv_plan** out, int64_t L, int32_t N, int32_t W_block, int32_t mode, int32_t packing,
+                     int32_t Q, const conv_opts* opts) {
+  if (!out) return PC_E_CONFIG;
+  *out = nullptr;
+  if (L < 1 || N < 1 || W_block < 4) return PC_E_CONFIG;
+  if (mode != PC_MODE_CONV && mode != PC_MODE_XCORR) return PC_E_CONFIG;
+  if (packing < PC_PACK_FULL || packing > PC_PACK_ADAPTIVE) return PC_E_CONFIG;
+  if (packing != PC_PACK_FULL && packing != PC_PACK_ADAPTIVE && Q < 1) return PC_E_CONFIG;
+  if (mode == PC_MODE_XCORR && L < N) return PC_E_CONFIG;
+  conv_opts o;
+  conv_opts_default(&o);
+  if (opts) o = *opts;
+  if (o.core != PC_CORE_DIRECT) return PC_E_CONFIG;   // FFT core: not in this build
+  const int Np = (N % 2) ? N : N + 1;                 // P:45, C13
+  const long long W = (long long)W_block - Np - 1;
+  if (W < 2 || (W % 2) || W < 2LL * Np) return PC_E_CONFIG;
+  int dev = o.device;
+  if (dev < 0) {
+    if (cudaGetDevice(&dev) != cudaSuccess) return PC_E_CUDA;
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1 || dev >= ndev) return PC_E_CUDA;
+  if (cudaSetDevice(dev) != cudaSuccess) return PC_E_CUDA;
+  conv_plan* p = new (std::nothrow) conv_plan();
+  if (!p) return PC_E_CUDA;
+  p->L = L;
+  p->N = N;
+  p->Np = Np;
+  p->W_block = W_block;
+  p->W = (int)W;
+  p->P = (L + W - 1) / W;                             // P = ceil(L / W)
+  p->mode = mode;
+  p->packing = packing;
+  p->Q = Q;
+  p->K_q = o.K_q > 0 ? o.K_q : Q;
+  p->opts = o;
+  p->device = dev;
+  cudaError_t e = cudaSuccess;
+  e = cudaMalloc(&p->d_k_pad, sizeof(double) * Np);
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_k_int, sizeof(double) * Np);
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_scal, sizeof(double) * 4);
+  if (e != cudaSuccess) {
+    conv_plan_destroy(p);
+    return PC_E_CUDA;
+  }
+  // shared-memory feasibility of the fused kernel for every packing the plan may use
+  int packs[4];
+  const int np = plan_packs(p, packs);
+  for (int i = 0; i < np; ++i) set_core_layout(p, packs[i], &p->ms[packs[i]]);
+  Shape sh;
+  if (!launch_shape(p, packs, np, &sh)) {
+    conv_plan_destroy(p);
+    return PC_E_CONFIG;
+  }
+  *out = p;
+  return PC_OK;
+}
+
+void conv_plan_destroy(conv_plan* p) {
+  if (!p) return;
+  cudaSetDevice(p->device);
+  for (auto& m : p->ms) cudaFree(m.kr);
+  cudaFree(p->d_k_pad);
+  cudaFree(p->d_k_int);
+  cudaFree(p->d_scal);
+  cudaFree(p->d_dec_pack);
+  cudaFree(p->d_dec_q);
+  cudaFree(p->d_dec_snr);
+  cudaFree(p->d_sigma);
+  cudaFree(p->d_peak);
+  cudaFree(p->d_cand);
+  cudaFree(p->d_in);
+  cudaFree(p->d_out);
+  cudaFree(p->d_xc);
+  delete p;
+}
+
+}  // extern "C"
+
+namespace {
+
+// Initialization of one packing at S_q = Q, K_q: k~, R_max, eps, bound, core taps.
+int init_mode(conv_plan* p, int packing, int Q, int K_q, const double* k_dev, cudaStream_t st) {
+  ModeState& m = p->ms[packing];
+  set_core_layout(p, packing, &m);
+  double scal[4] = {0, 0, 0, 0};
+  cudaError_t e = pc::launch_kernel_prep(k_dev, p->N, p->Np, p->mode == PC_MODE_XCORR, (double)K_q, p->d_k_pad,
+                                         p->d_k_int, p->d_scal, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(scal, p->d_scal, sizeof(double) * 3, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return PC_E_CUDA;
+  p->k_peak = scal[0];
+  m.Q = Q;
+  m.K_q = K_q;
+  if (packing == PC_PACK_FULL) {
+    m.c_k = 1.0;
+    m.R = 0;
+    m.bound = 0;
+    m.bound_ok = 1;
+    m.eps = m.eps_inv = 0.0;
+    m.b = 0;
+  } else {
+    m.c_k = scal[1];
+    const long long l1 = (long long)scal[2];
+    long long R = (p->opts.rmax_rule == PC_RMAX_L1) ? (long long)Q * l1 : (long long)p->Np * Q * (long long)K_q;
+    if (R < 1) R = 1;
+    m.R = R;
+    if (p->opts.eps_rule == PC_EPS_PAPER) {
+      m.eps_inv = 2.0 * (double)R;            // Eq. (6)
+      m.eps = 1.0 / m.eps_inv;
+      m.b = 0;
+    } else if (p->opts.eps_rule == PC_EPS_RADIX) {
+      m.eps_inv = 2.0 * (double)R + 1.0;      // reading C2
+      m.eps = 1.0 / m.eps_inv;
+      m.b = 0;
+    } else {
+      m.b = 64 - __builtin_clzll((unsigned long long)(2 * R));   // reading C4
+      m.eps_inv = std::ldexp(1.0, m.b);
+      m.eps = std::ldexp(1.0, -m.b);
+    }
+    m.bound = bound_for(packing, p->opts.eps_rule);
+    m.bound_ok = R <= m.bound;
+    if (!m.bound_ok && p->opts.bound_policy == PC_BOUND_STRICT) return PC_E_BOUND;
+  }
+  if (!m.kr && cudaMalloc(&m.kr, sizeof(double) * m.K_pad) != cudaSuccess) return PC_E_CUDA;
+  e = pc::launch_build_taps(p->d_k_pad, p->d_k_int, p->Np, packing, m.eps_inv, m.K, m.K_pad, m.kr, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return PC_E_CUDA;
+  m.valid = 1;
+  return PC_OK;
+}
+
+// R_max(Q) for the L1 rule needs k~ at each Q: evaluated with the prep kernel.
+int l1_at(conv_plan* p, int Q, const double* k_dev, cudaStream_t st, long long* l1) {
+  double scal[4];
+  cudaError_t e = pc::launch_kernel_prep(k_dev, p->N, p->Np, p->mode == PC_MODE_XCORR, (double)Q, p->d_k_pad,
+                                         p->d_k_int, p->d_scal, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(scal, p->d_scal, sizeof(double) * 3, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return PC_E_CUDA;
+  *l1 = (long long)scal[2];
+  return PC_OK;
+}
+
+// Largest tied Q = S_q = K_q whose R_max meets the packing's bound.
+int max_q(conv_plan* p, int packing, const double* k_dev, cudaStream_t st, int* q_out) {
+  const long long bound = bound_for(packing, p->opts.eps_rule);
+  int lo = 0, hi = 1 << 15;
+  while (lo < hi) {
+    const int mid = lo + (hi - lo + 1) / 2;
+    long long R;
+    if (p->opts.rmax_rule == PC_RMAX_L1) {
+      long long l1;
+      int rc = l1_at(p, mid, k_dev, st, &l1);
+      if (rc) return rc;
+      R = (long long)mid * l1;
+    } else {
+      R = (long long)p->Np * mid * (long long)mid;
+    }
+    if (R <= bound) lo = mid; else hi = mid - 1;
+  }
+  *q_out = lo;
+  return PC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int conv_plan_set_kernel(conv_plan* p, const double* k_dev, void* stream) {
+  if (!p || !k_dev) return PC_E_CONFIG;
+  if (cudaSetDevice(p->device) != cudaSuccess) return PC_E_CUDA;
+  cudaStream_t st = (cudaStream_t)stream;
+  p->kernel_set = 0;
+  p->adapt_ready = 0;
+  int rc;
+  if (p->packing == PC_PACK_ADAPTIVE) {
+    const int cands[2] = {PC_PACK_SYM, PC_PACK_ASYM2};
+    for (int c : cands) {
+      int q;
+      if ((rc = max_q(p, c, k_dev, st, &q))) return rc;
+      p->qmode[c] = q;
+      if (q >= 1) {
+        if ((rc = init_mode(p, c, q, q, k_dev, st))) return rc;
+      } else {
+        p->ms[c].valid = 0;
+      }
+    }
+    if ((rc = init_mode(p, PC_PACK_FULL, 0, 1, k_dev, st))) return rc;
+    // sigma_k, ||k||_inf (reading C12), on the padded kernel
+    Geo g;
+    std::memset(&g, 0, sizeof(g));
+    g.L = p->Np;
+    g.P = 1;
+    g.W_block = p->Np;
+    g.W = p->Np;
+    double* d_sk = nullptr;
+    if (cudaMalloc(&d_sk, 2 * sizeof(double)) != cudaSuccess) return PC_E_CUDA;
+    cudaError_t e = pc::launch_block_stats(g, p->d_k_pad, d_sk, d_sk + 1, st);
+    double hk[2] = {0, 0};
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hk, d_sk, sizeof(hk), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(d_sk);
+    if (e != cudaSuccess) return PC_E_CUDA;
+    p->k_sigma = hk[0];
+    p->k_peak = hk[1];
+  } else {
+    if ((rc = init_mode(p, p->packing, p->Q, p->K_q, k_dev, st))) return rc;
+  }
+  p->kernel_set = 1;
+  return PC_OK;
+}
+
+int conv_execute(conv_plan* p, const double* s, double* r, void* stream) {
+  if (!p || !s || !r) return PC_E_CONFIG;
+  if (cudaSetDevice(p->device) != cudaSuccess) return PC_E_CUDA;
+  return run_fused(p, s, 0, 0, r, 0, 0, 0, p->P, 1, nullptr, (cudaStream_t)stream);
+}
+
+int conv_execute_blocks(conv_plan* p, const double* s, int64_t s_offset, double* r, int64_t r_offset,
+                        int64_t block_begin, int64_t block_end, void* stream) {
+  if (!p || !s || !r) return PC_E_CONFIG;
+  if (block_begin < 0 || block_end > p->P || block_begin > block_end) return PC_E_CONFIG;
+  if (cudaSetDevice(p->device) != cudaSuccess) return PC_E_CUDA;
+  return run_fused(p, s, s_offset, 0, r, r_offset, 0, block_begin, block_end - block_begin, 1, nullptr,
+                   (cudaStream_t)stream);
+}
+
+int conv_execute_batch(conv_plan* p, const double* s, int64_t n_signals, int64_t s_stride, double* r,
+                       int64_t r_stride, void* stream) {
+  if (!p || !s || !r || n_signals < 0) return PC_E_CONFIG;
+  if (p->packing == PC_PACK_ADAPTIVE && n_signals > 1) return PC_E_CONFIG;
+  if (cudaSetDevice(p->device) != cudaSuccess) return PC_E_CUDA;
+  return run_fused(p, s, 0, s_stride, r, 0, r_stride, 0, p->P, n_signals, nullptr, (cudaStream_t)stream);
+}
+
+int conv_execute_host(conv_plan* p, const double* s_host, double* r_host, void* stream) {
+  if (!p || !s_host || !r_host) return PC_E_CONFIG;
+  if (cudaSetDevice(p->device) != cudaSuccess) return PC_E_CUDA;
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long L_out = p->mode == PC_MODE_XCORR ? p->L - p->N + 1 : p->L + p->N - 1;
+  if (!p->d_in && cudaMalloc(&p->d_in, sizeof(double) * p->L) != cudaSuccess) return PC_E_CUDA;
+  if (!p->d_out && cudaMalloc(&p->d_out, sizeof(double) * L_out) != cudaSuccess) return PC_E_CUDA;
+  if (cudaMemcpyAsync(p->d_in, s_host, sizeof(double) * p->L, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return PC_E_CUDA;
+  int rc = run_fused(p, p->d_in, 0, 0, p->d_out, 0, 0, 0, p->P, 1, nullptr, st);
+  if (rc) return rc;
+  if (cudaMemcpyAsync(r_host, p->d_out, sizeof(double) * L_out, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    return PC_E_CUDA;
+  return cuda_status(cudaStreamSynchronize(st));
+}
+
+int conv_execute_debug(conv_plan* p, const double* s, double* r, double* packed, double* rbar, int64_t* rint,
+                       double* c_s, void* stream) {
+  if (!p || !s) return PC_E_CONFIG;
+  if (cudaSetDevice(p->device) != cudaSuccess) return PC_E_CUDA;
+  conv_plan_info info;
+  conv_plan_query(p, &info);
+  Exec d;
+  std::memset(&d, 0, sizeof(d));
+  d.dbg_packed = packed;
+  d.dbg_packed_stride = info.packed_stride;
+  d.dbg_rbar = rbar;
+  d.dbg_rbar_stride = info.rbar_stride;
+  d.dbg_rint = reinterpret_cast<long long*>(rint);
+  d.dbg_rint_stride = info.rint_stride;
+  d.dbg_cs = c_s;
+  return run_fused(p, s, 0, 0, r, 0, 0, 0, p->P, 1, &d, (cudaStream_t)stream);
+}
+
+int conv_xcorr_max(conv_plan* p, const double* db, int64_t n_signals, int64_t s_stride, double* score,
+                   int64_t* lag, void* stream) {
+  if (!p || !db || !score || !lag || n_signals < 0) return PC_E_CONFIG;
+  if (p->mode != PC_MODE_XCORR || p->packing == PC_PACK_ADAPTIVE) return PC_E_CONFIG;
+  if (cudaSetDevice(p->device) != cudaSuccess) return PC_E_CUDA;
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long n_lags = p->L - p->N + 1;
+  long long chunk = (1LL << 28) / n_lags;    // <= 2 GiB of lag scratch
+  if (chunk < 1) chunk = 1;
+  if (chunk > n_signals) chunk = n_signals;
+  const size_t need = sizeof(double) * (size_t)chunk * (size_t)n_lags;
+  if (need > p->d_xc_bytes) {
+    cudaFree(p->d_xc);
+    p->d_xc = nullptr;
+    p->d_xc_bytes = 0;
+    if (cudaMalloc(&p->d_xc, need) != cudaSuccess) return PC_E_CUDA;
+    p->d_xc_bytes = need;
+  }
+  for (long long s0 = 0; s0 < n_signals; s0 += chunk) {
+    const long long n = (n_signals - s0 < chunk) ? n_signals - s0 : chunk;
+    int rc = run_fused(p, db + s0 * s_stride, 0, s_stride, p->d_xc, 0, n_lags, 0, p->P, n, nullptr, st);
+    if (rc) return rc;
+    cudaError_t e = pc::launch_xcorr_max(p->d_xc, n, n_lags, n_lags, score + s0,
+                                         reinterpret_cast<long long*>(lag) + s0, st);
+    if (e != cudaSuccess) return PC_E_CUDA;
+  }
+  return PC_OK;
+}
+
+int conv_adapt_block(conv_plan* p, const double* s, double snr_floor_db, double calib_offset_db,
+                     conv_block_decision* out, void* stream) {
+  if (!p || !s) return PC_E_CONFIG;
+  if (p->packing != PC_PACK_ADAPTIVE) return PC_E_CONFIG;
+  if (!p->kernel_set) return PC_E_STATE;
+  if (cudaSetDevice(p->device) != cudaSuccess) return PC_E_CUDA;
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long P = p->P;
+  cudaError_t e = cudaSuccess;
+  if (!p->d_dec_pack) {
+    e = cudaMalloc(&p->d_dec_pack, sizeof(int) * P);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_dec_q, sizeof(int) * P);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_dec_snr, sizeof(double) * P);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_sigma, sizeof(double) * P);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_peak, sizeof(double) * P);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_cand, sizeof(int) * 8);
+    if (e != cudaSuccess) return PC_E_CUDA;
+  }
+  int hc[8] = {0};
+  int nc = 0;
+  const int cands[2] = {PC_PACK_SYM, PC_PACK_ASYM2};
+  for (int c : cands) {
+    hc[nc] = c;
+    hc[4 + nc] = p->ms[c].valid ? p->qmode[c] : 0;
+    ++nc;
+  }
+  // predicted_db >= floor  <=>  snr_lin >= 10^((floor - offset)/10)
+  const double thr = std::pow(10.0, (snr_floor_db - calib_offset_db) / 10.0);
+  e = cudaMemcpyAsync(p->d_cand, hc, sizeof(hc), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = pc::launch_block_stats(make_geo(p), s, p->d_sigma, p->d_peak, st);
+  if (e == cudaSuccess)
+    e = pc::launch_adapt_decide(P, p->d_sigma, p->d_peak, p->k_sigma, p->k_peak, p->d_cand, p->d_cand + 4, nc, thr,
+                                p->d_dec_pack, p->d_dec_q, p->d_dec_snr, st);
+  if (e != cudaSuccess) return PC_E_CUDA;
+  if (out) {
+    int* hp = (int*)std::malloc(sizeof(int) * P * 2);
+    double* hs = (double*)std::malloc(sizeof(double) * P);
+    if (!hp || !hs) {
+      std::free(hp);
+      std::free(hs);
+      return PC_E_CUDA;
+    }
+    e = cudaMemcpyAsync(hp, p->d_dec_pack, sizeof(int) * P, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hp + P, p->d_dec_q, sizeof(int) * P, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hs, p->d_dec_snr, sizeof(double) * P, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) {
+      for (long long w = 0; w < P; ++w) {
+        out[w].packing = hp[w];
+        out[w].Q = hp[P + w];
+        out[w].snr_lin = hs[w];
+      }
+    }
+    std::free(hp);
+    std::free(hs);
+    if (e != cudaSuccess) return PC_E_CUDA;
+  } else if (cudaStreamSynchronize(st) != cudaSuccess) {
+    return PC_E_CUDA;
+  }
+  p->adapt_ready = 1;
+  return PC_OK;
+}
+
+int conv_plan_query(const conv_plan* p, conv_plan_info* info) {
+  if (!p || !info) return PC_E_CONFIG;
+  std::memset(info, 0, sizeof(*info));
+  info->L = p->L;
+  info->L_out = p->mode == PC_MODE_XCORR ? p->L - p->N + 1 : p->L + p->N - 1;
+  info->P = p->P;
+  info->N = p->N;
+  info->Np = p->Np;
+  info->W_block = p->W_block;
+  info->W = p->W;
+  info->mode = p->mode;
+  info->packing = p->packing;
+  info->Q = p->Q;
+  info->K_q = p->K_q;
+  const int pk = p->packing == PC_PACK_ADAPTIVE ? PC_PACK_ASYM2 : p->packing;
+  const ModeState& m = p->ms[pk];
+  info->taps = core_taps(p, pk);
+  info->kernel_set = p->kernel_set;
+  info->R_max = m.R;
+  info->bound = m.bound;
+  info->bound_ok = m.bound_ok;
+  info->eps_b = m.b;
+  info->eps = m.eps;
+  info->eps_inv = m.eps_inv;
+  info->c_k = m.c_k;
+  info->k_peak = p->k_peak;
+  int mmax = 0, mtyp = 0, best = 0;
+  for (int pkk = 0; pkk < 4; ++pkk) {
+    core_sizes(p, pkk, &mmax, &mtyp);
+    const int xl = mmax + core_taps(p, pkk) - 1;
+    if (xl > best) best = xl;
+  }
+  info->packed_stride = best > p->W_block / 2 ? best : p->W_block / 2;
+  core_sizes(p, pk, &mmax, &mtyp);
+  int mm = 0;
+  for (int pkk = 0; pkk < 4; ++pkk) {
+    core_sizes(p, pkk, &mmax, &mtyp);
+    if (mmax > mm) mm = mmax;
+  }
+  info->rbar_stride = mm;
+  info->rint_stride = p->W + p->Np - 1;
+  for (int i = 0; i < 4; ++i) info->q_mode[i] = p->qmode[i];
+  return PC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,423 @@
+// pc_kernels.cu -- sm_100a kernels of the packed overlap-save path (arXiv 1201.3018).
+//
+//   pc_kernel_prep      a1: kernel companding once: pad/reverse, ||k||_inf,
+//                       c_k, k~ = [[c_k k]], ||k~||_1 (for the L1 R_max rule, C3)
+//   pc_build_taps       a1: core taps, reversed: packed kernel Eq. (5) under C1 (sym),
+//                       k~ (asym, Eq. (8)) or k (full precision)
+//   pc_fused_kernel     a2-a7 (+a9 store mapping) in ONE kernel, one CTA per overlap-save
+//                       block: TMA bulk copy of the block and the taps into shared memory,
+//                       block peak (warp shuffles), companding (Eq. (2)), packing (Eq. (4)
+//                       or (7)) into a conflict-free column layout, the direct FP64 core
+//                       on packed words, unpacking (Eqs. (11)-(15), balanced form),
+//                       inverse companding (Eq. (16)), overlap discard and placement
+//                       (Eq. (17)).  FULL = the same kernel without the Tier-1.5 layer
+//                       (the full-precision reference path on identical tiling).
+//   pc_block_stats      a8: per-block peak and order-independent sigma (reading C12)
+//   pc_adapt_decide     a8: per-block mode choice from Eq. (19)
+//   pc_xcorr_max        a9: per-signal max and argmax of the valid lags (C17)
+#include "pc_device.cuh"
+#include "pc_kernels.h"
+
+namespace pc {
+
+// ------------------------------------------------------------------ a1: kernel preparation
+__global__ void pc_kernel_prep(const double* __restrict__ k_in, int N, int Np, int reverse, double K_q,
+                               double* __restrict__ k_pad, double* __restrict__ k_int,
+                               double* __restrict__ scal /* [peak, c_k, l1] */) {
+  __shared__ double red[32];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  double m = 0.0;
+  for (int i = tid; i < Np; i += nt) {
+    double v = 0.0;
+    if (i < N) v = k_in[reverse ? (N - 1 - i) : i];   // xcorr: reverse then pad (a9)
+    k_pad[i] = v;
+    m = fmax(m, fabs(v));
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((tid & 31) == 0) red[tid >> 5] = m;
+  __syncthreads();
+  if (tid < 32) {
+    m = (tid < (nt + 31) / 32) ? red[tid] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (tid == 0) red[0] = m;
+  }
+  __syncthreads();
+  const double peak = red[0];
+  const double c_k = (peak == 0.0) ? 1.0 : K_q / peak;   // P:53; all-zero -> c = 1
+  __syncthreads();
+  double l1 = 0.0;                                        // sum of integers < 2^53: exact
+  for (int i = tid; i < Np; i += nt) {
+    const double q = compand1(c_k, k_pad[i]);
+    k_int[i] = q;
+    l1 += fabs(q);
+  }
+  for (int o = 16; o > 0; o >>= 1) l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+  if ((tid & 31) == 0) red[tid >> 5] = l1;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (nt + 31) / 32; ++w) t += red[w];
+    scal[0] = peak;
+    scal[1] = c_k;
+    scal[2] = t;
+  }
+}
+
+__global__ void pc_build_taps(const double* __restrict__ k_pad, const double* __restrict__ k_int, int Np,
+                              int packing, double eps_inv, int K, int K_pad, double* __restrict__ kr) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < K_pad; j += gridDim.x * blockDim.x) {
+    double v = 0.0;
+    if (j < K) {
+      const int n = K - 1 - j;   // reversed: kr[j] = core tap K-1-j
+      if (packing == PACK_SYM) {
+        // Eq. (5) under reading C1: k_bar[n] = k~[2n+1] + eps^-1 k~[2n], k~[N'] = 0
+        const double kev = k_int[2 * n];
+        const double kod = (2 * n + 1 < Np) ? k_int[2 * n + 1] : 0.0;
+        v = __dadd_rn(kod, __dmul_rn(eps_inv, kev));
+      } else if (packing == PACK_FULL) {
+        v = k_pad[n];
+      } else {
+        v = k_int[n];             // Eq. (8): asymmetric packing convolves with k~
+      }
+    }
+    kr[j] = v;
+  }
+}
+
+// ------------------------------------------------------------------ fused per-block kernel
+__device__ __forceinline__ double block_max_abs(const double* raw, int n, const double* __restrict__ gsrc,
+                                                long long g_avail, bool staged, double* red) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  double m = 0.0;
+  if (staged) {
+    for (int i = tid; i < n; i += nt) m = fmax(m, fabs(raw[i]));
+  } else {
+    for (int i = tid; i < n; i += nt) m = fmax(m, (i < g_avail) ? fabs(gsrc[i]) : 0.0);
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __syncthreads();   // red may still be read by a previous use
+  if ((tid & 31) == 0) red[tid >> 5] = m;
+  __syncthreads();
+  double r = 0.0;
+  for (int w = 0; w < (nt + 31) / 32; ++w) r = fmax(r, red[w]);
+  return r;
+}
+
+template <int PACK, int T>
+__device__ __forceinline__ void fused_block(const Geo& g, const Exec& e, const ModeP& mp, long long sig,
+                                            long long w, unsigned char* smem) {
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+  double* red = reinterpret_cast<double*>(smem + 16);
+  double* raw = reinterpret_cast<double*>(smem + kSmemHeader);          // W_block (if staged)
+  double* xs = raw + (e.stage_raw ? g.W_block : 0);                      // T x rows
+  double* kr = xs + (size_t)T * mp.rows;                                 // K_pad
+  double* Rs = e.stage_raw ? raw : (kr + mp.K_pad);                      // M_out core outputs
+
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const double* __restrict__ s = e.s + sig * e.s_stride;   // s[i - s_off] = sample i
+  double* __restrict__ r = e.r ? e.r + sig * e.r_stride : nullptr;
+  const Blk b = block_info<PACK>(g, mp.K, w);
+  const long long dbg_row = sig * g.P + w;
+
+  // ---- stage the block (W_block samples; zeros past L) and the taps: TMA bulk copies
+  const long long avail = g.L - b.g0;                       // samples of this block inside L
+  const int n_valid = (int)(avail < 0 ? 0 : (avail > g.W_block ? g.W_block : avail));
+  const double* gsrc = s + (b.g0 - e.s_off);
+  const bool aligned = ((reinterpret_cast<uintptr_t>(gsrc) & 15u) == 0);
+  const int n_bulk = (e.stage_raw && aligned) ? (n_valid & ~1) : 0;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    const uint32_t bytes = (uint32_t)n_bulk * 8u + (uint32_t)mp.K_pad * 8u;
+    mbar_arrive_expect_tx(bar, bytes);
+    if (n_bulk) bulk_g2s(raw, gsrc, (uint32_t)n_bulk * 8u, bar);
+    bulk_g2s(kr, mp.kr, (uint32_t)mp.K_pad * 8u, bar);
+  }
+  if (e.stage_raw) {
+    for (int i = n_bulk + tid; i < g.W_block; i += nt) raw[i] = (i < n_valid) ? gsrc[i] : 0.0;
+  }
+  __syncthreads();            // barrier init visible before anyone waits on it
+  mbar_wait(bar, 0);
+
+  // ---- a2/a3: block peak and companding factor (Eq. (2))
+  double c_s = 1.0;
+  if (PACK != PACK_FULL) {
+    const double peak = block_max_abs(raw, g.W_block, gsrc, n_valid, e.stage_raw, red);
+    c_s = (peak == 0.0) ? 1.0 : mp.Q / peak;
+  }
+  auto sample = [&](int i) -> double {      // local sample i of the block (0 outside)
+    if (i < 0 || i >= g.W_block) return 0.0;
+    if (e.stage_raw) return raw[i];
+    return (i < n_valid) ? gsrc[i] : 0.0;
+  };
+
+  // ---- a4: packing into the core's column layout  xs[(i % T) * rows + i / T]
+  const int xlen_pad = T * mp.rows;
+  for (int i = tid; i < xlen_pad; i += nt) {
+    double v = 0.0;
+    if (i < b.xlen) {
+      if (PACK == PACK_SYM) {
+        const int j = i - b.pre;              // s_bar[j], j < W_block/2 (Eq. (4))
+        if (j >= 0) v = pack_sym(compand1(c_s, sample(2 * j)), compand1(c_s, sample(2 * j + 1)), mp.eps);
+      } else if (PACK == PACK_ASYM2 || PACK == PACK_ASYM3) {
+        constexpr int M = (PACK == PACK_ASYM2) ? 2 : 3;
+        const int base = b.o0 - (g.Np - 1) + i;   // Eq. (7) under C8, Horner (oracle order)
+        v = compand1(c_s, sample(base + (M - 1) * b.S));
+#pragma unroll
+        for (int q = M - 2; q >= 0; --q)
+          v = __dadd_rn(compand1(c_s, sample(base + q * b.S)), __dmul_rn(mp.eps, v));
+      } else {
+        v = sample(b.o0 - (g.Np - 1) + i);
+      }
+    }
+    xs[(i % T) * mp.rows + i / T] = v;
+  }
+  if (e.dbg_packed && PACK != PACK_FULL) {
+    double* dp = e.dbg_packed + dbg_row * e.dbg_packed_stride;
+    if (PACK == PACK_SYM) {
+      for (int j = tid; j < g.W_block / 2; j += nt)
+        dp[j] = pack_sym(compand1(c_s, sample(2 * j)), compand1(c_s, sample(2 * j + 1)), mp.eps);
+    } else {
+      for (int i = tid; i < b.xlen; i += nt) dp[i] = xs[(i % T) * mp.rows + i / T];
+    }
+  }
+  if (e.dbg_cs && tid == 0) e.dbg_cs[dbg_row] = c_s;
+  __syncthreads();
+
+  // ---- a5: the Tier-2 core on packed words (hot loop)
+  const int ngroups = (b.M_out + T - 1) / T;
+  for (int gi = tid; gi < ngroups; gi += nt) {
+    double acc[T];
+    conv_group<T>(xs, mp.rows, kr, mp.K_pad, gi, acc);
+#pragma unroll
+    for (int i = 0; i < T; ++i) {
+      const int m = gi * T + i;
+      if (m < b.M_out) Rs[m] = acc[i];
+    }
+  }
+  __syncthreads();
+  if (e.dbg_rbar) {
+    double* dr = e.dbg_rbar + dbg_row * e.dbg_rbar_stride;
+    for (int m = tid; m < b.M_out; m += nt) dr[m] = Rs[m];
+  }
+
+  // ---- a6/a7: unpack, inverse-compand, discard and place (Eqs. (11)-(17))
+  const double cc = __dmul_rn(c_s, mp.c_k);
+  const long long gbase = b.g0 + b.o0;        // global index of kept output 0
+  long long* dri = e.dbg_rint ? e.dbg_rint + dbg_row * e.dbg_rint_stride : nullptr;
+  auto store = [&](int k, double rint_v, double val) {
+    if (dri) dri[k] = (long long)rint_v;
+    if (!r) return;
+    const long long gi = gbase + k;
+    if (g.mode == 0) {
+      if (gi < g.L + g.N - 1) r[gi - e.r_off] = val;
+    } else {
+      const long long j = gi - (g.N - 1);      // valid lag j = 0 .. L-N (C17)
+      if (j >= 0 && j <= g.L - g.N) r[j - e.r_off] = val;
+    }
+  };
+  if (PACK == PACK_SYM) {
+    // kept output k: w=0 -> packed m = k/2; w>0 -> m = k/2 + 1 (the seeded m = W_start
+    // word only supplies B).  r~[2m+1] = A[m]; r~[2m] = C[m] + B[m-1], B[-1] = 0 (w=0).
+    const int moff = (w == 0) ? 0 : 1;
+    const int npairs = b.n_out / 2;
+    for (int p = tid; p < npairs; p += nt) {
+      const int m = p + moff;
+      const Digits3 d = decode_sym(Rs[m], mp.eps, mp.eps_inv, mp.pow2);
+      const double Bp = (m >= 1) ? decode_sym_B(Rs[m - 1], mp.eps, mp.eps_inv, mp.pow2) : 0.0;
+      const double ev = d.C + Bp, od = d.A;
+      store(2 * p, ev, __ddiv_rn(ev, cc));
+      store(2 * p + 1, od, __ddiv_rn(od, cc));
+    }
+  } else if (PACK == PACK_ASYM2 || PACK == PACK_ASYM3) {
+    constexpr int M = (PACK == PACK_ASYM2) ? 2 : 3;
+    for (int m = tid; m < b.S; m += nt) {
+      double v = Rs[m];
+#pragma unroll
+      for (int q = 0; q < M; ++q) {          // balanced digits, most significant first (C9)
+        const double t = rint(v);
+        if (q < M - 1) v = __dmul_rn(__dsub_rn(v, t), mp.eps_inv);
+        const int k = q * b.S + m;
+        if (k < b.n_out) store(k, t, __ddiv_rn(t, cc));
+      }
+    }
+  } else {
+    for (int m = tid; m < b.n_out; m += nt) store(m, 0.0, Rs[m]);
+  }
+}
+
+// PACK >= 0: one packing for every block.  PACK < 0: per-block packing from e.dec_pack
+// (conv_adapt_block; "switch between asymmetric, symmetric and no packing").
+template <int PACK>
+__global__ void __launch_bounds__(kMaxThreads) pc_fused_kernel(Geo g, Exec e) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const long long job = blockIdx.x;
+  const long long sig = job / e.nblk;
+  const long long w = e.b0 + job % e.nblk;
+  if (PACK >= 0) {
+    fused_block<(PACK < 0 ? 0 : PACK), kT>(g, e, e.mp[PACK < 0 ? 0 : PACK], sig, w, smem);
+  } else {
+    switch (e.dec_pack[sig * g.P + w]) {
+      case PACK_SYM: fused_block<PACK_SYM, kT>(g, e, e.mp[PACK_SYM], sig, w, smem); break;
+      case PACK_ASYM2: fused_block<PACK_ASYM2, kT>(g, e, e.mp[PACK_ASYM2], sig, w, smem); break;
+      case PACK_ASYM3: fused_block<PACK_ASYM3, kT>(g, e, e.mp[PACK_ASYM3], sig, w, smem); break;
+      default: fused_block<PACK_FULL, kT>(g, e, e.mp[PACK_FULL], sig, w, smem); break;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ a8: block statistics
+// Per block: peak p and sigma from the second moment on the fixed grid z = [[x 2^20/p]]
+// with an exact int64 sum (reading C12).
+__global__ void pc_block_stats(Geo g, const double* __restrict__ s, double* __restrict__ sigma,
+                               double* __restrict__ peak_out) {
+  __shared__ double red[32];
+  __shared__ unsigned long long ired[32];
+  const long long w = blockIdx.x;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const long long g0 = (w == 0) ? 0 : w * (long long)g.W - 2;
+  const long long avail = g.L - g0;
+  const int n_valid = (int)(avail < 0 ? 0 : (avail > g.W_block ? g.W_block : avail));
+  const double* src = s + g0;
+  const double p = block_max_abs(nullptr, n_valid, src, n_valid, false, red);
+  unsigned long long acc = 0;
+  if (p != 0.0) {
+    const double sc = 1048576.0 / p;
+    for (int i = tid; i < n_valid; i += nt) {
+      const long long z = (long long)round(__dmul_rn(src[i], sc));
+      acc += (unsigned long long)(z * z);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((tid & 31) == 0) ired[tid >> 5] = acc;
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long t = 0;
+    for (int i = 0; i < (nt + 31) / 32; ++i) t += ired[i];
+    const double m2 = __ddiv_rn((double)t, (double)g.W_block);
+    sigma[w] = (p == 0.0) ? 0.0 : __ddiv_rn(__dmul_rn(p, __dsqrt_rn(m2)), 1048576.0);
+    peak_out[w] = p;
+  }
+}
+
+// Eqs. (18)-(19) linear form in the oracle's evaluation order (oracle.snr_linear).
+__device__ __forceinline__ double snr_linear(double ss, double sk, double ps, double pk, double Sq, double Kq) {
+  const double sq12 = 3.4641016151377544;   // sqrt(12) correctly rounded
+  const double vs = __ddiv_rn(ps, __dmul_rn(Sq, sq12));
+  const double vk = __ddiv_rn(pk, __dmul_rn(Kq, sq12));
+  const double a = __dmul_rn(ss, vk), b = __dmul_rn(sk, vs), c = __dmul_rn(vk, vs);
+  const double D = __dadd_rn(__dadd_rn(__dmul_rn(a, a), __dmul_rn(b, b)), __dmul_rn(c, c));
+  const double n = __dmul_rn(ss, sk);
+  return __ddiv_rn(__dmul_rn(n, n), D);
+}
+
+__global__ void pc_adapt_decide(long long P, const double* __restrict__ sigma, const double* __restrict__ peak,
+                                double sig_k, double peak_k, const int* __restrict__ cand, const int* __restrict__ qmode,
+                                int ncand, double thr_lin, int* __restrict__ dec_pack, int* __restrict__ dec_q,
+                                double* __restrict__ dec_snr) {
+  const long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (w >= P) return;
+  int mode = PACK_FULL, q = 0;
+  double lin = __longlong_as_double(0x7ff0000000000000LL);   // +inf
+  const double ss = sigma[w];
+  if (ss > 0.0) {
+    for (int c = 0; c < ncand; ++c) {
+      const int Qm = qmode[c];
+      if (Qm < 1) continue;
+      const double l = snr_linear(ss, sig_k, peak[w], peak_k, (double)Qm, (double)Qm);
+      if (l >= thr_lin) { mode = cand[c]; q = Qm; lin = l; break; }
+    }
+  } else {
+    mode = cand[0];
+    q = qmode[0];
+  }
+  dec_pack[w] = mode;
+  dec_q[w] = q;
+  dec_snr[w] = lin;
+}
+
+// ------------------------------------------------------------------ a9: xcorr score
+// One CTA per signal: max over valid lags, lowest lag on ties (C17).
+__global__ void pc_xcorr_max(const double* __restrict__ c, long long n_lags, long long stride,
+                             double* __restrict__ score, long long* __restrict__ lag) {
+  __shared__ double sv[32];
+  __shared__ long long sj[32];
+  const long long sig = blockIdx.x;
+  const double* row = c + sig * stride;
+  double best = -__longlong_as_double(0x7ff0000000000000LL);
+  long long bj = 0x7fffffffffffffffLL;
+  for (long long j = threadIdx.x; j < n_lags; j += blockDim.x) {
+    const double v = row[j];
+    if (v > best) { best = v; bj = j; }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const long long oj = __shfl_xor_sync(0xffffffffu, bj, o);
+    if (ov > best || (ov == best && oj < bj)) { best = ov; bj = oj; }
+  }
+  if ((threadIdx.x & 31) == 0) { sv[threadIdx.x >> 5] = best; sj[threadIdx.x >> 5] = bj; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int wi = 1; wi < (int)((blockDim.x + 31) / 32); ++wi)
+      if (sv[wi] > best || (sv[wi] == best && sj[wi] < bj)) { best = sv[wi]; bj = sj[wi]; }
+    score[sig] = best;
+    lag[sig] = bj;
+  }
+}
+
+// ------------------------------------------------------------------ host-side launchers
+template <int PACK>
+static cudaError_t launch_fused_t(const Geo& g, const Exec& e, long long n_jobs, int threads, size_t smem,
+                                  cudaStream_t st) {
+  auto kfn = pc_fused_kernel<PACK>;
+  cudaError_t err = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (err != cudaSuccess) return err;
+  kfn<<<(unsigned)n_jobs, threads, smem, st>>>(g, e);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fused(int packing, const Geo& g, const Exec& e, long long n_jobs, int threads, size_t smem,
+                         cudaStream_t st) {
+  if (n_jobs <= 0) return cudaSuccess;
+  switch (packing) {
+    case PACK_FULL: return launch_fused_t<PACK_FULL>(g, e, n_jobs, threads, smem, st);
+    case PACK_SYM: return launch_fused_t<PACK_SYM>(g, e, n_jobs, threads, smem, st);
+    case PACK_ASYM2: return launch_fused_t<PACK_ASYM2>(g, e, n_jobs, threads, smem, st);
+    case PACK_ASYM3: return launch_fused_t<PACK_ASYM3>(g, e, n_jobs, threads, smem, st);
+    case -1: return launch_fused_t<-1>(g, e, n_jobs, threads, smem, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_kernel_prep(const double* k_in, int N, int Np, int reverse, double K_q, double* k_pad,
+                               double* k_int, double* scal, cudaStream_t st) {
+  pc_kernel_prep<<<1, 1024, 0, st>>>(k_in, N, Np, reverse, K_q, k_pad, k_int, scal);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_build_taps(const double* k_pad, const double* k_int, int Np, int packing, double eps_inv, int K,
+                              int K_pad, double* kr, cudaStream_t st) {
+  const int blocks = (K_pad + 255) / 256;
+  pc_build_taps<<<blocks, 256, 0, st>>>(k_pad, k_int, Np, packing, eps_inv, K, K_pad, kr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_block_stats(const Geo& g, const double* s, double* sigma, double* peak, cudaStream_t st) {
+  pc_block_stats<<<(unsigned)g.P, 256, 0, st>>>(g, s, sigma, peak);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_adapt_decide(long long P, const double* sigma, const double* peak, double sig_k, double peak_k,
+                                const int* cand, const int* qmode, int ncand, double thr, int* dp, int* dq, double* ds,
+                                cudaStream_t st) {
+  pc_adapt_decide<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(P, sigma, peak, sig_k, peak_k, cand, qmode, ncand,
+                                                                 thr, dp, dq, ds);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_xcorr_max(const double* c, long long n_signals, long long n_lags, long long stride,
+                             double* score, long long* lag, cudaStream_t st) {
+  pc_xcorr_max<<<(unsigned)n_signals, 1024, 0, st>>>(c, n_lags, stride, score, lag);
+  return cudaGetLastError();
+}
+
+}  // namespace pc

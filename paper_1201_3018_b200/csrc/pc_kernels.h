@@ -1,0 +1,56 @@
+// pc_kernels.h -- launch interface between the C ABI (pc_api.cu) and the kernels.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "pc_device.cuh"
+
+namespace pc {
+
+constexpr int kT = 8;              // outputs per thread of the direct core (register tile)
+constexpr int kMaxThreads = 256;   // threads per CTA (one CTA per overlap-save block)
+constexpr int kSmemHeader = 512;   // mbarrier + reduction scratch, keeps the rest 128B-aligned
+
+// Per-packing parameters of one launch (adaptive plans fill several).
+struct ModeP {
+  const double* kr;     // core taps, reversed, K_pad doubles (device)
+  double Q;             // S_q
+  double c_k;           // kernel companding factor
+  double eps, eps_inv;  // packing coefficient and its inverse
+  int pow2;             // eps = 2^-b (reading C4)
+  int K, K_pad;         // core taps and taps padded to a multiple of kT
+  int rows;             // rows of the column layout of the core's input words
+};
+
+struct Exec {
+  const double* s;      // s[i - s_off] is global sample i (row `sig` at s + sig*s_stride)
+  long long s_off, s_stride;
+  double* r;            // r[g - r_off] is global output g (or lag g for xcorr)
+  long long r_off, r_stride;
+  long long b0, nblk;   // block range [b0, b0 + nblk) of every signal; grid = n_sig * nblk
+  int stage_raw;        // stage the W_block raw samples in shared memory (TMA bulk copy)
+  ModeP mp[4];          // indexed by packing (PACK_FULL .. PACK_ASYM3)
+  const int* dec_pack;  // adaptive: per (signal, block) packing, else nullptr
+  // parity/debug dumps (row = sig * P + w), nullptr in production
+  double* dbg_packed;
+  long long dbg_packed_stride;
+  double* dbg_rbar;
+  long long dbg_rbar_stride;
+  long long* dbg_rint;
+  long long dbg_rint_stride;
+  double* dbg_cs;
+};
+
+cudaError_t launch_fused(int packing, const Geo& g, const Exec& e, long long n_jobs, int threads, size_t smem,
+                         cudaStream_t st);
+cudaError_t launch_kernel_prep(const double* k_in, int N, int Np, int reverse, double K_q, double* k_pad,
+                               double* k_int, double* scal, cudaStream_t st);
+cudaError_t launch_build_taps(const double* k_pad, const double* k_int, int Np, int packing, double eps_inv, int K,
+                              int K_pad, double* kr, cudaStream_t st);
+cudaError_t launch_block_stats(const Geo& g, const double* s, double* sigma, double* peak, cudaStream_t st);
+cudaError_t launch_adapt_decide(long long P, const double* sigma, const double* peak, double sig_k, double peak_k,
+                                const int* cand, const int* qmode, int ncand, double thr, int* dp, int* dq, double* ds,
+                                cudaStream_t st);
+cudaError_t launch_xcorr_max(const double* c, long long n_signals, long long n_lags, long long stride,
+                             double* score, long long* lag, cudaStream_t st);
+
+}  // namespace pc

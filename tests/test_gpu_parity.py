@@ -1,0 +1,305 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Bar (task rule ③): companding factors, packed words, packed convolution
+outputs (dyadic eps: exact arithmetic), unpacked integers and dequantized outputs are
+BIT-EXACT; full-precision outputs are within 1e-12 normalized L-inf (north_star,
+reading C16).  Sizes span several tiles and ragged tails; full BASELINE sizes are
+checked on sampled blocks the oracle computes one by one.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_1201_3018_b200 import workloads as WL
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_1201_3018_b200 import binding as pcb
+    DEV = torch.device("cuda:0")
+
+PK = {O.FULL: 0, O.SYM: 1, O.ASYM2: 2, O.ASYM3: 3}
+EPS = {O.EPS_PAPER: 0, O.EPS_RADIX: 1, O.EPS_POW2: 2}
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).to(DEV)
+
+
+def gpu_run(s, k, W_block, packing, Q, mode=O.CONV, eps_rule=O.EPS_POW2, rmax_rule=O.RMAX_PAPER, debug=True):
+    with pcb.Plan(len(s), len(k), W_block, mode, PK[packing], Q, eps_rule=EPS[eps_rule],
+                  rmax_rule=rmax_rule, bound_policy=pcb.BOUND_WARN) as p:
+        p.set_kernel(dev(k))
+        info = p.info()
+        s_d = dev(s)
+        r = torch.full((info["L_out"],), float("nan"), dtype=torch.float64, device=DEV)
+        out = {"info": info}
+        if debug:
+            P = info["P"]
+            packed = torch.zeros((P, info["packed_stride"]), dtype=torch.float64, device=DEV)
+            rbar = torch.zeros((P, info["rbar_stride"]), dtype=torch.float64, device=DEV)
+            rint = torch.zeros((P, info["rint_stride"]), dtype=torch.int64, device=DEV)
+            cs = torch.zeros(P, dtype=torch.float64, device=DEV)
+            p.execute_debug(s_d, r, packed, rbar, rint, cs)
+            torch.cuda.synchronize()
+            out.update(packed=packed.cpu().numpy(), rbar=rbar.cpu().numpy(), rint=rint.cpu().numpy(),
+                       cs=cs.cpu().numpy(), r_dbg=r.cpu().numpy())
+            r.fill_(float("nan"))
+        p.execute(s_d, r)
+        torch.cuda.synchronize()
+        out["r"] = r.cpu().numpy()
+    return out
+
+
+def check_blocks(g, ref, packing):
+    """Per-step bit-exact comparison against the oracle's per-block record."""
+    geom = ref.geom
+    for br in ref.blocks:
+        w = br.w
+        o0, n_out = geom.kept(w)
+        if packing != O.FULL:
+            assert g["cs"][w] == br.c_s, ("c_s", w)
+            assert np.array_equal(g["packed"][w, :br.packed.shape[0]], br.packed), ("packed words", w)
+            assert np.array_equal(g["rbar"][w, :br.rbar.shape[0]], br.rbar), ("packed conv outputs", w)
+            assert np.array_equal(g["rint"][w, :n_out], br.r_int.astype(np.int64)), ("unpacked integers", w)
+            assert np.array_equal(g["rint"][w, :n_out], br.r_exact), ("exact integer conv", w)
+
+
+SMALL_CASES = [  # (L, N, W_block, Q): several tiles, ragged tails, P = 1, N = 1, N > L
+    (1000, 9, 40, 7), (777, 10, 34, 7), (5, 1, 4, 3), (4097, 64, 1024, 127), (20000, 513, 4096, 31),
+    (3, 2, 10, 5), (5, 9, 30, 3), (70000, 65, 1024, 60), (12345, 255, 2048, 15),
+]
+
+
+@pytest.mark.parametrize("packing", [O.SYM, O.ASYM2, O.ASYM3])
+@pytest.mark.parametrize("case", SMALL_CASES)
+def test_packed_bit_exact_pow2(packing, case):
+    L, N, W_block, Q = case
+    rng = np.random.default_rng(L * 7 + N)
+    s, k = rng.laplace(0, 0.3, L), rng.uniform(-1, 1, N)
+    ref = O.conv_pipeline(s, k, W_block, packing, Q, keep_blocks=True)
+    assert ref.kernel.bound_ok and ref.mismatches == 0
+    g = gpu_run(s, k, W_block, packing, Q)
+    assert g["info"]["c_k"] == ref.kernel.c_k and g["info"]["R_max"] == ref.kernel.R
+    assert g["info"]["eps_inv"] == ref.kernel.eps.eps_inv
+    check_blocks(g, ref, packing)
+    assert np.array_equal(g["r_dbg"], ref.out)
+    assert np.array_equal(g["r"], ref.out)
+
+
+@pytest.mark.parametrize("packing", [O.SYM, O.ASYM2, O.ASYM3])
+@pytest.mark.parametrize("eps_rule", [O.EPS_PAPER, O.EPS_RADIX])
+def test_packed_integers_exact_nondyadic_eps(packing, eps_rule):
+    """Non-dyadic eps: packed words are deterministic (bit-exact); the core's FMA order may
+    change the last bits of r_bar, but the unpacked integers are exact (within bound)."""
+    L, N, W_block, Q = 20000, 65, 1024, 5
+    rng = np.random.default_rng(11)
+    s, k = rng.laplace(0, 0.3, L), rng.uniform(-1, 1, N)
+    ref = O.conv_pipeline(s, k, W_block, packing, Q, eps_rule=eps_rule, keep_blocks=True)
+    assert ref.kernel.bound_ok and ref.mismatches == 0
+    g = gpu_run(s, k, W_block, packing, Q, eps_rule=eps_rule)
+    for br in ref.blocks:
+        o0, n_out = ref.geom.kept(br.w)
+        assert np.array_equal(g["packed"][br.w, :br.packed.shape[0]], br.packed)
+        assert np.array_equal(g["rint"][br.w, :n_out], br.r_exact)
+    assert np.array_equal(g["r"], ref.out)
+
+
+@pytest.mark.parametrize("case", SMALL_CASES)
+def test_full_precision_within_1e12(case):
+    L, N, W_block, _ = case
+    rng = np.random.default_rng(L + 3 * N)
+    s, k = rng.normal(size=L), rng.normal(size=N)
+    want = O.full_precision(s, k)
+    g = gpu_run(s, k, W_block, O.FULL, 0, debug=False)
+    err = np.max(np.abs(g["r"] - want)) / np.max(np.abs(want))
+    assert err < 1e-12, err
+
+
+@pytest.mark.parametrize("packing", [O.FULL, O.SYM, O.ASYM2])
+def test_xcorr_mode(packing):
+    rng = np.random.default_rng(5)
+    s, q = rng.laplace(0, 0.3, 9000), rng.uniform(-1, 1, 100)
+    ref = O.conv_pipeline(s, q, 512, packing, 63, mode=O.XCORR, keep_blocks=True)
+    g = gpu_run(s, q, 512, packing, 63, mode=O.XCORR, debug=packing != O.FULL)
+    assert g["r"].shape == (9000 - 100 + 1,)
+    if packing == O.FULL:
+        want = O.full_precision(s, q, O.XCORR)
+        assert np.max(np.abs(g["r"] - want)) / np.max(np.abs(want)) < 1e-12
+    else:
+        assert ref.mismatches == 0
+        check_blocks(g, ref, packing)
+        assert np.array_equal(g["r"], ref.out)
+
+
+def test_edge_cases_zero_delta_saturating():
+    rng = np.random.default_rng(8)
+    s = rng.uniform(-1, 1, 3000)
+    s[500:1500] = 0.0                                            # all-zero blocks: c_s = 1
+    for packing in (O.SYM, O.ASYM2, O.ASYM3):
+        for k in ([1.0], [0.0, 0.0, 0.0], rng.uniform(-1, 1, 9)):   # delta, zero kernel, random
+            ref = O.conv_pipeline(s, k, 40, packing, 15, keep_blocks=True)
+            g = gpu_run(s, k, 40, packing, 15)
+            check_blocks(g, ref, packing)
+            assert np.array_equal(g["r"], ref.out)
+    # square wave matched to the kernel signs: outputs reach +R_max (L1 rule, reading C3)
+    k = rng.uniform(-1, 1, 9)
+    k_int, _, _ = O.compand(k, 5)
+    sq = np.tile(np.sign(k_int[::-1]) + (k_int[::-1] == 0), 40)
+    ref = O.conv_pipeline(sq, k, 40, O.SYM, 5, rmax_rule=O.RMAX_L1, keep_blocks=True)
+    assert max(int(np.max(b.r_exact)) for b in ref.blocks) == ref.kernel.R
+    g = gpu_run(sq, k, 40, O.SYM, 5, rmax_rule=O.RMAX_L1)
+    check_blocks(g, ref, O.SYM)
+    assert np.array_equal(g["r"], ref.out)
+
+
+def test_bound_policy_strict():
+    k = np.ones(513)
+    with pcb.Plan(10000, 513, 4096, pcb.MODE_CONV, pcb.PACK_SYM, 127) as p:   # 513*127^2 > 131071
+        with pytest.raises(pcb.PcError) as ei:
+            p.set_kernel(dev(k))
+        assert ei.value.code == pcb.PC_E_BOUND
+
+
+def test_execute_blocks_sharding_bit_identical():
+    """Block-range sharding: each 'rank' holds only its input slice plus the
+    N'+1 halo; the union of outputs is bit-identical to the single run, for G = 1,2,3,4,8."""
+    rng = np.random.default_rng(2)
+    L, N, W_block, Q = 200000, 64, 1024, 255
+    s, k = rng.laplace(0, 0.2, L), rng.uniform(-1, 1, N)
+    ref = O.conv_pipeline(s, k, W_block, O.ASYM2, Q)
+    with pcb.Plan(L, N, W_block, pcb.MODE_CONV, pcb.PACK_ASYM2, Q) as p:
+        p.set_kernel(dev(k))
+        info = p.info()
+        P, W = info["P"], info["W"]
+        for G in (1, 2, 3, 4, 8):
+            out = np.full(info["L_out"], np.nan)
+            for rank in range(G):
+                b0, b1 = P * rank // G, P * (rank + 1) // G
+                in0 = 0 if b0 == 0 else b0 * W - 2
+                in1 = min(L, (b1 - 1) * W - 2 + W_block) if b1 > 1 else min(L, W_block)
+                o0 = 0 if b0 == 0 else info["Np"] - 1 + b0 * W
+                o1 = min(info["L_out"], info["Np"] - 1 + b1 * W)
+                s_slice = dev(s[in0:in1])
+                r_slice = torch.full((o1 - o0,), float("nan"), dtype=torch.float64, device=DEV)
+                p.execute_blocks(s_slice, in0, r_slice, o0, b0, b1)
+                torch.cuda.synchronize()
+                out[o0:o1] = r_slice.cpu().numpy()
+            assert np.array_equal(out, ref.out), G
+
+
+def test_execute_batch_and_host_and_misaligned():
+    rng = np.random.default_rng(3)
+    L, N, W_block, Q = 50000, 100, 1024, 127
+    k = rng.uniform(-1, 1, N)
+    S = rng.laplace(0, 0.2, (3, L))
+    refs = [O.conv_pipeline(S[i], k, W_block, O.ASYM2, Q).out for i in range(3)]
+    with pcb.Plan(L, N, W_block, pcb.MODE_CONV, pcb.PACK_ASYM2, Q) as p:
+        p.set_kernel(dev(k))
+        Lo = L + N - 1
+        R = torch.full((3, Lo + 5), float("nan"), dtype=torch.float64, device=DEV)
+        Sd = torch.zeros((3, L + 3), dtype=torch.float64, device=DEV)
+        Sd[:, :L] = dev(S)
+        p.execute_batch(Sd, 3, L + 3, R, Lo + 5)
+        torch.cuda.synchronize()
+        for i in range(3):
+            assert np.array_equal(R[i, :Lo].cpu().numpy(), refs[i])
+        # host buffers (pinned) through conv_execute_host
+        sh = torch.from_numpy(S[1].copy()).pin_memory()
+        rh = torch.empty(Lo, dtype=torch.float64).pin_memory()
+        p.execute_host(sh, rh)
+        assert np.array_equal(rh.numpy(), refs[1])
+        # misaligned input pointer (8-byte offset): plain-load staging path, same bits
+        buf = torch.zeros(L + 1, dtype=torch.float64, device=DEV)
+        buf[1:] = dev(S[2])
+        r = torch.empty(Lo, dtype=torch.float64, device=DEV)
+        p.execute(buf[1:], r)
+        torch.cuda.synchronize()
+        assert np.array_equal(r.cpu().numpy(), refs[2])
+
+
+@pytest.mark.parametrize("floor", [20.0, 30.0, 40.0, 50.0, 60.0, math.inf])
+def test_adaptive_decisions_and_output(floor):
+    s, k = WL.cfg5(seed=1, L=1 << 17, N=1024)
+    W_block = 4096
+    y_ref, dec_ref, qmode = O.adaptive_pipeline(s, k, W_block, floor)
+    with pcb.Plan(len(s), len(k), W_block, pcb.MODE_CONV, pcb.PACK_ADAPTIVE, 0, rmax_rule=pcb.RMAX_L1) as p:
+        p.set_kernel(dev(k))
+        info = p.info()
+        assert info["q_mode"][1] == qmode[O.SYM] and info["q_mode"][2] == qmode[O.ASYM2]
+        s_d = dev(s)
+        dec = p.adapt_block(s_d, floor)
+        assert [(d[0], d[1]) for d in dec] == [(PK[m], q) for m, q, _ in dec_ref]
+        assert [d[2] for d in dec] == [x[2] for x in dec_ref]
+        r = torch.empty(info["L_out"], dtype=torch.float64, device=DEV)
+        p.execute(s_d, r)
+        torch.cuda.synchronize()
+        assert np.array_equal(r.cpu().numpy(), y_ref)
+
+
+def test_xcorr_max_scores():
+    rng = np.random.default_rng(4)
+    n_sig, L, N = 6, 1 << 14, 256
+    db = np.stack([WL.cfg4_signal(i, L) for i in range(n_sig)])
+    q = db[3, 5000:5000 + N] + rng.normal(0, 0.01, N)
+    for packing, Q in ((O.FULL, 0), (O.SYM, 7), (O.ASYM2, 127)):
+        with pcb.Plan(L, N, 2048, pcb.MODE_XCORR, PK[packing], Q, rmax_rule=pcb.RMAX_L1) as p:
+            p.set_kernel(dev(q))
+            sc = torch.empty(n_sig, dtype=torch.float64, device=DEV)
+            lag = torch.empty(n_sig, dtype=torch.int64, device=DEV)
+            p.xcorr_max(dev(db), n_sig, L, sc, lag)
+            torch.cuda.synchronize()
+            sc, lag = sc.cpu().numpy(), lag.cpu().numpy()
+        for i in range(n_sig):
+            if packing == O.FULL:
+                c = O.full_precision(db[i], q, O.XCORR)
+                best, j = O.xcorr_score(c)
+                assert abs(sc[i] - best) <= 1e-12 * np.max(np.abs(c))
+                assert c[lag[i]] >= best - 1e-12 * np.max(np.abs(c))
+            else:
+                c = O.conv_pipeline(db[i], q, 2048, packing, Q, mode=O.XCORR, rmax_rule=O.RMAX_L1).out
+                assert (sc[i], lag[i]) == O.xcorr_score(c)
+        assert int(np.argmax(sc)) == 3 and lag[3] == 5000
+
+
+# --------------------------------------------------------------------- full BASELINE sizes
+def _sampled_full_size(s, k, W_block, packing, Q, rmax_rule, min_snr):
+    geom = O.Geometry(len(s), len(k), W_block)
+    blocks = sorted({0, 1, 2, geom.P // 3, geom.P // 2, geom.P - 2, geom.P - 1})
+    ref = O.conv_pipeline(s, k, W_block, packing, Q, rmax_rule=rmax_rule, blocks=blocks)
+    g = gpu_run(s, k, W_block, packing, Q, rmax_rule=rmax_rule, debug=False)
+    sel = ~np.isnan(ref.out)
+    assert np.array_equal(g["r"][sel], ref.out[sel])
+    assert ref.mismatches == 0
+    assert not np.any(np.isnan(g["r"]))
+    return g
+
+
+@pytest.mark.parametrize("packing,Q,rmax,min_snr", [(O.ASYM2, 511, O.RMAX_L1, 40.0), (O.SYM, 127, O.RMAX_L1, 30.0),
+                                                    (O.ASYM3, 127, O.RMAX_L1, 30.0), (O.ASYM2, 31, O.RMAX_PAPER, 20.0)])
+def test_cfg2_full_size_sampled(packing, Q, rmax, min_snr):
+    s, k = WL.cfg2(seed=0)
+    g = _sampled_full_size(s, k, 4096, packing, Q, rmax, min_snr)
+    full = O.full_precision(s[:1 << 18], k)
+    snr = O.measured_snr_db(full[:(1 << 18)], g["r"][:1 << 18])
+    assert snr >= min_snr, snr
+
+
+def test_cfg2_full_precision_full_size():
+    s, k = WL.cfg2(seed=0)
+    g = gpu_run(s, k, 4096, O.FULL, 0, debug=False)
+    want = O.full_precision(s, k)
+    assert np.max(np.abs(g["r"] - want)) / np.max(np.abs(want)) < 1e-12
+
+
+def test_cfg1_full_size_all_packings():
+    s, k = WL.cfg1(seed=0)
+    for packing, Q in ((O.ASYM2, 127), (O.ASYM2, 255), (O.SYM, 44), (O.ASYM3, 15)):
+        ref = O.conv_pipeline(s, k, 1024, packing, Q, keep_blocks=True)
+        assert ref.kernel.bound_ok and ref.mismatches == 0
+        g = gpu_run(s, k, 1024, packing, Q)
+        check_blocks(g, ref, packing)
+        assert np.array_equal(g["r"], ref.out)
