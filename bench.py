@@ -260,7 +260,7 @@ def run_ours(args, ws, rank, local):
         results[name] = {"ms_per_step": ms / args.steps, "kernel_ms": kern_ms,
                          "value": ws * L_out * args.steps / (ms / 1e3),
                          "fp64_tflops": 2.0 * fma / (kern_ms / 1e3) / 1e12, "fma_per_output": fma / L_out,
-                         "R_max": info["R_max"], "Q": Q, "bound_ok": info["bound_ok"]}
+                         "R_max": info["R_max"], "Q": Q, "bound_ok": info["bound_ok"], "tile": info["core_tile"]}
         outputs[name] = R[(args.steps - 1) % n_buf].clone()
         if name == HEADLINE:
             # end to end through the C ABI with HOST buffers (pinned): H2D + run + D2H per step

@@ -52,7 +52,10 @@ enum { PC_EPS_PAPER = 0, PC_EPS_RADIX = 1, PC_EPS_POW2 = 2 };   /* Eq.(6); C2; C
 enum { PC_RMAX_PAPER = 0, PC_RMAX_L1 = 1 };                /* Eq.(3); C3                  */
 enum { PC_BOUND_STRICT = 0, PC_BOUND_WARN = 1 };
 enum { PC_CORE_DIRECT = 0, PC_CORE_FFT = 1 };              /* Tier-2 core          */
-enum { PC_EXEC_FUSED = 0, PC_EXEC_STAGED = 1 };            /* one kernel vs G1->G2->G4    */
+/* Execution form: FUSED = persistent warp-specialized kernel (producer warps compand and
+ * pack block n+1 while consumer warps run the core on block n); PERBLOCK = one CTA per
+ * block, phases separated by barriers (also the form that serves conv_execute_debug). */
+enum { PC_EXEC_FUSED = 0, PC_EXEC_PERBLOCK = 1 };
 
 /* Plan options.  conv_opts_default() fills: eps_rule POW2, rmax_rule PAPER, bound_policy
  * STRICT, core DIRECT, exec FUSED, K_q 0 (= Q), device -1 (current), u_sys 3.1193e-11. */
@@ -64,7 +67,8 @@ typedef struct conv_opts {
   int32_t exec;
   int32_t K_q;              /* kernel companding range; 0 means K_q = S_q = Q       */
   int32_t device;           /* CUDA device ordinal, -1 = current device                    */
-  int32_t reserved[9];
+  int32_t reserved[9];      /* [0]: raw-block staging 0 auto/1 on/2 off (per-block kernel);
+                               [1]: force the persistent core tile (12/14/16; tests); rest 0 */
   double u_sys;             /* P:153; used only by the literal paper unpack form          */
 } conv_opts;
 
@@ -89,6 +93,8 @@ typedef struct conv_plan_info {
   int64_t rbar_stride;      /* per-block stride (words) of the debug packed-output dump    */
   int64_t rint_stride;      /* per-block stride of the debug integer dump (= W + N' - 1)   */
   int32_t q_mode[4];        /* ADAPTIVE: max Q per packing under its bound          */
+  int32_t core_tile;        /* outputs per thread of the persistent core (12, 14 or 16)      */
+  int32_t reserved_i;
 } conv_plan_info;
 
 /* Per-block decision of conv_adapt_block. */

@@ -84,8 +84,10 @@ def compand(x, Q):
 
 
 def inverse_compand(r_int, c_s, c_k):
-    """Eq. (16): r = (c_s c_k)^-1 r~, evaluated as r~ / (c_s * c_k) (C11)."""
-    return np.asarray(r_int, dtype=np.float64) / (c_s * c_k)
+    """Eq. (16): r = (c_s c_k)^-1 r~ -- the inverse (c_s c_k)^-1 is formed once
+    per block (one product, one IEEE division) and multiplies every r~ (reading C11)."""
+    inv = 1.0 / (c_s * c_k)
+    return np.asarray(r_int, dtype=np.float64) * inv
 
 
 # ----------------------------------------------------------------------------- geometry

@@ -21,7 +21,7 @@ EPS_PAPER, EPS_RADIX, EPS_POW2 = 0, 1, 2
 RMAX_PAPER, RMAX_L1 = 0, 1
 BOUND_STRICT, BOUND_WARN = 0, 1
 CORE_DIRECT, CORE_FFT = 0, 1
-EXEC_FUSED, EXEC_STAGED = 0, 1
+EXEC_FUSED, EXEC_PERBLOCK = 0, 1
 
 PACK_NAMES = {PACK_FULL: "full", PACK_SYM: "sym", PACK_ASYM2: "asym2", PACK_ASYM3: "asym3",
               PACK_ADAPTIVE: "adaptive"}
@@ -41,7 +41,7 @@ class conv_plan_info(C.Structure):
                 ("R_max", C.c_int64), ("bound", C.c_int64), ("bound_ok", C.c_int32), ("eps_b", C.c_int32),
                 ("eps", C.c_double), ("eps_inv", C.c_double), ("c_k", C.c_double), ("k_peak", C.c_double),
                 ("packed_stride", C.c_int64), ("rbar_stride", C.c_int64), ("rint_stride", C.c_int64),
-                ("q_mode", C.c_int32 * 4)]
+                ("q_mode", C.c_int32 * 4), ("core_tile", C.c_int32), ("reserved_i", C.c_int32)]
 
 
 class conv_block_decision(C.Structure):

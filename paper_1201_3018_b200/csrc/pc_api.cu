@@ -18,7 +18,7 @@ using pc::ModeP;
 namespace {
 
 constexpr size_t kMaxSmem = 232448;      // 227 KB dynamic shared memory per CTA (sm_100)
-constexpr size_t kStageSmemCap = 116224; // stage raw blocks only while 2 CTAs/SM still fit
+constexpr size_t kSmemPerSM = 233472;    // 228 KB shared memory per SM
 
 struct ModeState {
   int valid = 0;
@@ -29,7 +29,8 @@ struct ModeState {
   int b = 0;
   double c_k = 1.0;
   double* kr = nullptr;
-  int K = 0, K_pad = 0, rows = 0;
+  int K = 0, K_pad = 0, rows = 0;      // per-block kernel layout (tile kT)
+  int K_padP = 0, rowsP = 0, TP = 16;  // persistent kernel layout (tile TP, chosen per plan)
 };
 
 }  // namespace
@@ -61,6 +62,9 @@ struct conv_plan {
   // xcorr scratch
   double* d_xc = nullptr;
   size_t d_xc_bytes = 0;
+  // persistent kernel job counter (monotonic; base tracked on the host)
+  unsigned long long* d_counter = nullptr;
+  unsigned long long counter_base = 0;
 };
 
 namespace {
@@ -122,25 +126,51 @@ void core_sizes(const conv_plan* p, int packing, int* mmax, int* mtyp) {
   }
 }
 
+// Column layout of the core's input words for a tile of T outputs per thread: K padded to a
+// multiple of T; rows >= groups + K_pad/T, rounded to 4 mod 16 so that lane-consecutive
+// word stores (packing) hit every bank pair exactly twice.
+void layout_for(int K, int mmax, int T, int* K_pad, int* rows) {
+  *K_pad = (K + T - 1) / T * T;
+  const int ngroups = (mmax + T - 1) / T;
+  int r = ngroups + *K_pad / T + 1;
+  r = (r + 11) / 16 * 16 + 4;
+  *rows = r;
+}
 void set_core_layout(const conv_plan* p, int packing, ModeState* m) {
   int mmax, mtyp;
   core_sizes(p, packing, &mmax, &mtyp);
   m->K = core_taps(p, packing);
-  m->K_pad = (m->K + pc::kT - 1) / pc::kT * pc::kT;
-  const int ngroups = (mmax + pc::kT - 1) / pc::kT;
-  m->rows = ngroups + m->K_pad / pc::kT + 1;
-  m->rows = (m->rows + 1) & ~1;   // keep each column 16-byte aligned
+  layout_for(m->K, mmax, pc::kT, &m->K_pad, &m->rows);
+  // persistent tile: the T in {16,14,12} whose groups best fill whole consumer warps for a
+  // typical block (ties within 2% go to the larger T: fewer x-loads per FMA)
+  double best = -1.0;
+  for (int T : pc::kTPChoices) {
+    const double groups = (double)mtyp / T;
+    const double util = groups / (32.0 * std::ceil(groups / 32.0));
+    if (util > best + 0.02) {
+      best = util;
+      m->TP = T;
+    }
+  }
+  const int force = p->opts.reserved[1];   // test hook: force the persistent tile
+  if (force == 12 || force == 14 || force == 16) m->TP = force;
+  layout_for(m->K, mmax, m->TP, &m->K_padP, &m->rowsP);
 }
 
 // Launch shape of the fused kernel for the packings that may run in this plan.
+// Threads: one T-output group per thread when the largest block has <= 1024 groups (the
+// register path); otherwise 256 threads looping over groups with a separate result region.
+// The raw block is TMA-staged in shared memory only when that does not lower the number
+// of resident CTAs per SM (64 registers/thread cap from __launch_bounds__).
 struct Shape {
   int threads;
   int stage_raw;
+  int reg_path;
   size_t smem;
 };
 bool launch_shape(const conv_plan* p, const int* packs, int npacks, Shape* sh) {
   size_t core = 0;
-  int mmax_all = 0, groups_typ = 0;
+  int mmax_all = 0, groups_max = 0;
   for (int i = 0; i < npacks; ++i) {
     const ModeState& m = p->ms[packs[i]];
     int mmax, mtyp;
@@ -148,27 +178,52 @@ bool launch_shape(const conv_plan* p, const int* packs, int npacks, Shape* sh) {
     const size_t c = (size_t)pc::kT * m.rows * 8 + (size_t)m.K_pad * 8;
     if (c > core) core = c;
     if (mmax > mmax_all) mmax_all = mmax;
-    const int gt = (mtyp + pc::kT - 1) / pc::kT;
-    if (gt > groups_typ) groups_typ = gt;
+    const int gm = (mmax + pc::kT - 1) / pc::kT;
+    if (gm > groups_max) groups_max = gm;
   }
-  const size_t staged = pc::kSmemHeader + (size_t)p->W_block * 8 + core;
-  const size_t unstaged = pc::kSmemHeader + core + (size_t)mmax_all * 8 + 16;
-  if (staged <= kStageSmemCap) {
+  sh->reg_path = groups_max <= pc::kMaxThreads;
+  int t = sh->reg_path ? (groups_max + 31) / 32 * 32 : 256;
+  if (t < 64) t = 64;
+  sh->threads = t;
+  const size_t base = pc::kSmemHeader + core + (sh->reg_path ? 0 : (size_t)mmax_all * 8 + 16);
+  const size_t staged = base + (size_t)p->W_block * 8;
+  const int by_regs = 65536 / (t * 64);
+  auto ctas = [&](size_t sm) { return (int)(kSmemPerSM / (sm + 1024)); };
+  int mode = p->opts.reserved[0];   // 0 auto, 1 force staging, 2 never stage
+  bool stage = staged <= kMaxSmem && (mode == 1 || (mode == 0 && ctas(staged) >= (by_regs < ctas(base) ? by_regs : ctas(base))));
+  if (stage) {
     sh->stage_raw = 1;
     sh->smem = staged;
-  } else if (unstaged <= kMaxSmem) {
+  } else if (base <= kMaxSmem) {
     sh->stage_raw = 0;
-    sh->smem = unstaged;
+    sh->smem = base;
   } else {
     return false;
   }
-  const int iters = (groups_typ + pc::kMaxThreads - 1) / pc::kMaxThreads;
-  int t = (groups_typ + iters - 1) / iters;
-  t = (t + 31) / 32 * 32;
-  if (t < 64) t = 64;
-  if (t > pc::kMaxThreads) t = pc::kMaxThreads;
-  sh->threads = t;
   return true;
+}
+
+// Persistent warp-specialized kernel: producer warps (4 for short kernels, else 2) and one
+// consumer thread per T-group of a typical block; two packed stages in shared memory.
+struct PShape {
+  int threads, np_warps, nc_warps, gmax;
+  size_t smem;
+};
+bool persist_shape(const conv_plan* p, int packing, PShape* sh) {
+  const ModeState& m = p->ms[packing];
+  int mmax, mtyp;
+  core_sizes(p, packing, &mmax, &mtyp);
+  const int T = m.TP;
+  sh->gmax = (mmax + T - 1) / T;
+  const int gtyp = (mtyp + T - 1) / T;
+  sh->np_warps = m.K < 256 ? 2 : 1;
+  int nc = (gtyp + 31) / 32;
+  if (nc < 2) nc = 2;
+  if (nc > pc::kMaxThreadsP / 32 - sh->np_warps) nc = pc::kMaxThreadsP / 32 - sh->np_warps;
+  sh->nc_warps = nc;
+  sh->threads = 32 * (sh->np_warps + nc);
+  sh->smem = pc::kSmemHeader + (size_t)m.K_padP * 8 + 2 * (size_t)T * m.rowsP * 8 + 4 * (size_t)sh->gmax * 8;
+  return sh->smem <= kMaxSmem;
 }
 
 int cuda_status(cudaError_t e) { return e == cudaSuccess ? PC_OK : PC_E_CUDA; }
@@ -197,7 +252,7 @@ int plan_packs(const conv_plan* p, int* packs) {
   return 1;
 }
 
-int run_fused(conv_plan* p, const double* s, long long s_off, long long s_stride, double* r, long long r_off,
+int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride, double* r, long long r_off,
               long long r_stride, long long b0, long long nblk, long long n_sig, Exec* dbg, cudaStream_t st) {
   if (!p->kernel_set) return PC_E_STATE;
   if (p->packing == PC_PACK_ADAPTIVE && !p->adapt_ready) return PC_E_STATE;
@@ -218,9 +273,27 @@ int run_fused(conv_plan* p, const double* s, long long s_off, long long s_stride
   e.b0 = b0;
   e.nblk = nblk;
   e.stage_raw = sh.stage_raw;
+  e.reg_path = sh.reg_path;
   for (int i = 0; i < np; ++i) fill_modep(p->ms[packs[i]], &e.mp[packs[i]]);
   e.dec_pack = p->packing == PC_PACK_ADAPTIVE ? p->d_dec_pack : nullptr;
+  e.nsig = n_sig;
   const int launch_pack = p->packing == PC_PACK_ADAPTIVE ? -1 : p->packing;
+  PShape ps;
+  if (!dbg && p->packing != PC_PACK_ADAPTIVE && p->opts.exec == PC_EXEC_FUSED && persist_shape(p, p->packing, &ps)) {
+    e.counter = p->d_counter;
+    e.base = p->counter_base;
+    e.np_warps = ps.np_warps;
+    e.nc_warps = ps.nc_warps;
+    e.gmax = ps.gmax;
+    e.mp[p->packing].K_pad = p->ms[p->packing].K_padP;
+    e.mp[p->packing].rows = p->ms[p->packing].rowsP;
+    int grid = 0;
+    cudaError_t err = pc::launch_persist(p->packing, p->ms[p->packing].TP, make_geo(p), e, nblk * n_sig, ps.threads,
+                                         ps.smem, st, &grid);
+    if (err != cudaSuccess) return PC_E_CUDA;
+    p->counter_base += (unsigned long long)(nblk * n_sig) + (unsigned long long)grid;
+    return PC_OK;
+  }
   return cuda_status(pc::launch_fused(launch_pack, make_geo(p), e, nblk * n_sig, sh.threads, sh.smem, st));
 }
 
@@ -296,6 +369,8 @@ int conv_plan_create(conv_plan** out, int64_t L, int32_t N, int32_t W_block, int
   e = cudaMalloc(&p->d_k_pad, sizeof(double) * Np);
   if (e == cudaSuccess) e = cudaMalloc(&p->d_k_int, sizeof(double) * Np);
   if (e == cudaSuccess) e = cudaMalloc(&p->d_scal, sizeof(double) * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_counter, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(p->d_counter, 0, sizeof(unsigned long long));
   if (e != cudaSuccess) {
     conv_plan_destroy(p);
     return PC_E_CUDA;
@@ -329,6 +404,7 @@ void conv_plan_destroy(conv_plan* p) {
   cudaFree(p->d_in);
   cudaFree(p->d_out);
   cudaFree(p->d_xc);
+  cudaFree(p->d_counter);
   delete p;
 }
 
@@ -379,8 +455,9 @@ int init_mode(conv_plan* p, int packing, int Q, int K_q, const double* k_dev, cu
     m.bound_ok = R <= m.bound;
     if (!m.bound_ok && p->opts.bound_policy == PC_BOUND_STRICT) return PC_E_BOUND;
   }
-  if (!m.kr && cudaMalloc(&m.kr, sizeof(double) * m.K_pad) != cudaSuccess) return PC_E_CUDA;
-  e = pc::launch_build_taps(p->d_k_pad, p->d_k_int, p->Np, packing, m.eps_inv, m.K, m.K_pad, m.kr, st);
+  const int kr_len = m.K_padP > m.K_pad ? m.K_padP : m.K_pad;   // zero taps past K serve both tiles
+  if (!m.kr && cudaMalloc(&m.kr, sizeof(double) * kr_len) != cudaSuccess) return PC_E_CUDA;
+  e = pc::launch_build_taps(p->d_k_pad, p->d_k_int, p->Np, packing, m.eps_inv, m.K, kr_len, m.kr, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return PC_E_CUDA;
   m.valid = 1;
@@ -471,7 +548,7 @@ int conv_plan_set_kernel(conv_plan* p, const double* k_dev, void* stream) {
 int conv_execute(conv_plan* p, const double* s, double* r, void* stream) {
   if (!p || !s || !r) return PC_E_CONFIG;
   if (cudaSetDevice(p->device) != cudaSuccess) return PC_E_CUDA;
-  return run_fused(p, s, 0, 0, r, 0, 0, 0, p->P, 1, nullptr, (cudaStream_t)stream);
+  return run_exec(p, s, 0, 0, r, 0, 0, 0, p->P, 1, nullptr, (cudaStream_t)stream);
 }
 
 int conv_execute_blocks(conv_plan* p, const double* s, int64_t s_offset, double* r, int64_t r_offset,
@@ -479,7 +556,7 @@ int conv_execute_blocks(conv_plan* p, const double* s, int64_t s_offset, double*
   if (!p || !s || !r) return PC_E_CONFIG;
   if (block_begin < 0 || block_end > p->P || block_begin > block_end) return PC_E_CONFIG;
   if (cudaSetDevice(p->device) != cudaSuccess) return PC_E_CUDA;
-  return run_fused(p, s, s_offset, 0, r, r_offset, 0, block_begin, block_end - block_begin, 1, nullptr,
+  return run_exec(p, s, s_offset, 0, r, r_offset, 0, block_begin, block_end - block_begin, 1, nullptr,
                    (cudaStream_t)stream);
 }
 
@@ -488,7 +565,7 @@ int conv_execute_batch(conv_plan* p, const double* s, int64_t n_signals, int64_t
   if (!p || !s || !r || n_signals < 0) return PC_E_CONFIG;
   if (p->packing == PC_PACK_ADAPTIVE && n_signals > 1) return PC_E_CONFIG;
   if (cudaSetDevice(p->device) != cudaSuccess) return PC_E_CUDA;
-  return run_fused(p, s, 0, s_stride, r, 0, r_stride, 0, p->P, n_signals, nullptr, (cudaStream_t)stream);
+  return run_exec(p, s, 0, s_stride, r, 0, r_stride, 0, p->P, n_signals, nullptr, (cudaStream_t)stream);
 }
 
 int conv_execute_host(conv_plan* p, const double* s_host, double* r_host, void* stream) {
@@ -500,7 +577,7 @@ int conv_execute_host(conv_plan* p, const double* s_host, double* r_host, void* 
   if (!p->d_out && cudaMalloc(&p->d_out, sizeof(double) * L_out) != cudaSuccess) return PC_E_CUDA;
   if (cudaMemcpyAsync(p->d_in, s_host, sizeof(double) * p->L, cudaMemcpyHostToDevice, st) != cudaSuccess)
     return PC_E_CUDA;
-  int rc = run_fused(p, p->d_in, 0, 0, p->d_out, 0, 0, 0, p->P, 1, nullptr, st);
+  int rc = run_exec(p, p->d_in, 0, 0, p->d_out, 0, 0, 0, p->P, 1, nullptr, st);
   if (rc) return rc;
   if (cudaMemcpyAsync(r_host, p->d_out, sizeof(double) * L_out, cudaMemcpyDeviceToHost, st) != cudaSuccess)
     return PC_E_CUDA;
@@ -522,7 +599,7 @@ int conv_execute_debug(conv_plan* p, const double* s, double* r, double* packed,
   d.dbg_rint = reinterpret_cast<long long*>(rint);
   d.dbg_rint_stride = info.rint_stride;
   d.dbg_cs = c_s;
-  return run_fused(p, s, 0, 0, r, 0, 0, 0, p->P, 1, &d, (cudaStream_t)stream);
+  return run_exec(p, s, 0, 0, r, 0, 0, 0, p->P, 1, &d, (cudaStream_t)stream);
 }
 
 int conv_xcorr_max(conv_plan* p, const double* db, int64_t n_signals, int64_t s_stride, double* score,
@@ -545,7 +622,7 @@ int conv_xcorr_max(conv_plan* p, const double* db, int64_t n_signals, int64_t s_
   }
   for (long long s0 = 0; s0 < n_signals; s0 += chunk) {
     const long long n = (n_signals - s0 < chunk) ? n_signals - s0 : chunk;
-    int rc = run_fused(p, db + s0 * s_stride, 0, s_stride, p->d_xc, 0, n_lags, 0, p->P, n, nullptr, st);
+    int rc = run_exec(p, db + s0 * s_stride, 0, s_stride, p->d_xc, 0, n_lags, 0, p->P, n, nullptr, st);
     if (rc) return rc;
     cudaError_t e = pc::launch_xcorr_max(p->d_xc, n, n_lags, n_lags, score + s0,
                                          reinterpret_cast<long long*>(lag) + s0, st);
@@ -659,6 +736,7 @@ int conv_plan_query(const conv_plan* p, conv_plan_info* info) {
   info->rbar_stride = mm;
   info->rint_stride = p->W + p->Np - 1;
   for (int i = 0; i < 4; ++i) info->q_mode[i] = p->qmode[i];
+  info->core_tile = m.TP;
   return PC_OK;
 }
 

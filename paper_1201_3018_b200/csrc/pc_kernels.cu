@@ -106,12 +106,15 @@ __device__ __forceinline__ double block_max_abs(const double* raw, int n, const 
 template <int PACK, int T>
 __device__ __forceinline__ void fused_block(const Geo& g, const Exec& e, const ModeP& mp, long long sig,
                                             long long w, unsigned char* smem) {
+  // shared memory: [header][raw W_block (stage_raw only)][xs T x rows][kr K_pad][Rs (loop path only)]
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
   double* red = reinterpret_cast<double*>(smem + 16);
-  double* raw = reinterpret_cast<double*>(smem + kSmemHeader);          // W_block (if staged)
-  double* xs = raw + (e.stage_raw ? g.W_block : 0);                      // T x rows
-  double* kr = xs + (size_t)T * mp.rows;                                 // K_pad
-  double* Rs = e.stage_raw ? raw : (kr + mp.K_pad);                      // M_out core outputs
+  double* raw = reinterpret_cast<double*>(smem + kSmemHeader);
+  double* xs = raw + (e.stage_raw ? g.W_block : 0);
+  double* kr = xs + (size_t)T * mp.rows;
+  // register path: one T-output group per thread, results re-staged in the xs region after
+  // the core finished; loop path: groups > threads, results in a separate region.
+  double* Rs = e.reg_path ? xs : (kr + mp.K_pad);
 
   const int tid = threadIdx.x, nt = blockDim.x;
   const double* __restrict__ s = e.s + sig * e.s_stride;   // s[i - s_off] = sample i
@@ -119,7 +122,7 @@ __device__ __forceinline__ void fused_block(const Geo& g, const Exec& e, const M
   const Blk b = block_info<PACK>(g, mp.K, w);
   const long long dbg_row = sig * g.P + w;
 
-  // ---- stage the block (W_block samples; zeros past L) and the taps: TMA bulk copies
+  // ---- TMA bulk copies: the core taps (always) and the raw block (stage_raw)
   const long long avail = g.L - b.g0;                       // samples of this block inside L
   const int n_valid = (int)(avail < 0 ? 0 : (avail > g.W_block ? g.W_block : avail));
   const double* gsrc = s + (b.g0 - e.s_off);
@@ -127,71 +130,107 @@ __device__ __forceinline__ void fused_block(const Geo& g, const Exec& e, const M
   const int n_bulk = (e.stage_raw && aligned) ? (n_valid & ~1) : 0;
   if (tid == 0) {
     mbar_init(bar, 1);
-    const uint32_t bytes = (uint32_t)n_bulk * 8u + (uint32_t)mp.K_pad * 8u;
-    mbar_arrive_expect_tx(bar, bytes);
+    mbar_arrive_expect_tx(bar, (uint32_t)n_bulk * 8u + (uint32_t)mp.K_pad * 8u);
     if (n_bulk) bulk_g2s(raw, gsrc, (uint32_t)n_bulk * 8u, bar);
     bulk_g2s(kr, mp.kr, (uint32_t)mp.K_pad * 8u, bar);
   }
   if (e.stage_raw) {
     for (int i = n_bulk + tid; i < g.W_block; i += nt) raw[i] = (i < n_valid) ? gsrc[i] : 0.0;
-  }
-  __syncthreads();            // barrier init visible before anyone waits on it
-  mbar_wait(bar, 0);
-
-  // ---- a2/a3: block peak and companding factor (Eq. (2))
-  double c_s = 1.0;
-  if (PACK != PACK_FULL) {
-    const double peak = block_max_abs(raw, g.W_block, gsrc, n_valid, e.stage_raw, red);
-    c_s = (peak == 0.0) ? 1.0 : mp.Q / peak;
+    __syncthreads();          // barrier init visible before anyone waits on it
+    mbar_wait(bar, 0);
   }
   auto sample = [&](int i) -> double {      // local sample i of the block (0 outside)
-    if (i < 0 || i >= g.W_block) return 0.0;
-    if (e.stage_raw) return raw[i];
-    return (i < n_valid) ? gsrc[i] : 0.0;
+    if (i < 0 || i >= n_valid) return 0.0;
+    return e.stage_raw ? raw[i] : __ldg(gsrc + i);
   };
 
-  // ---- a4: packing into the core's column layout  xs[(i % T) * rows + i / T]
-  const int xlen_pad = T * mp.rows;
-  for (int i = tid; i < xlen_pad; i += nt) {
-    double v = 0.0;
-    if (i < b.xlen) {
-      if (PACK == PACK_SYM) {
-        const int j = i - b.pre;              // s_bar[j], j < W_block/2 (Eq. (4))
-        if (j >= 0) v = pack_sym(compand1(c_s, sample(2 * j)), compand1(c_s, sample(2 * j + 1)), mp.eps);
-      } else if (PACK == PACK_ASYM2 || PACK == PACK_ASYM3) {
-        constexpr int M = (PACK == PACK_ASYM2) ? 2 : 3;
-        const int base = b.o0 - (g.Np - 1) + i;   // Eq. (7) under C8, Horner (oracle order)
-        v = compand1(c_s, sample(base + (M - 1) * b.S));
-#pragma unroll
-        for (int q = M - 2; q >= 0; --q)
-          v = __dadd_rn(compand1(c_s, sample(base + q * b.S)), __dmul_rn(mp.eps, v));
-      } else {
-        v = sample(b.o0 - (g.Np - 1) + i);
+  // ---- a2/a3: block peak (coalesced, warp shuffles) and companding factor (Eq. (2))
+  double c_s = 1.0;
+  if (PACK != PACK_FULL) {
+    double m = 0.0;
+    if (e.stage_raw) {
+      for (int i = tid; i < n_valid; i += nt) m = fmax(m, fabs(raw[i]));
+    } else if (aligned) {
+      const double2* g2 = reinterpret_cast<const double2*>(gsrc);
+      for (int i = tid; i < n_valid / 2; i += nt) {
+        const double2 v = __ldg(g2 + i);
+        m = fmax(m, fmax(fabs(v.x), fabs(v.y)));
       }
+      if ((n_valid & 1) && tid == 0) m = fmax(m, fabs(gsrc[n_valid - 1]));
+    } else {
+      for (int i = tid; i < n_valid; i += nt) m = fmax(m, fabs(__ldg(gsrc + i)));
     }
-    xs[(i % T) * mp.rows + i / T] = v;
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((tid & 31) == 0) red[tid >> 5] = m;
+    __syncthreads();
+    double peak = 0.0;
+    for (int wi = 0; wi < (nt + 31) / 32; ++wi) peak = fmax(peak, red[wi]);
+    c_s = (peak == 0.0) ? 1.0 : mp.Q / peak;
+  }
+
+  // ---- a4: companding + packing.  Thread row g builds the T consecutive core words
+  // gT..gT+T-1 and writes them to xs[c * rows + g] (lane-consecutive: conflict-free).
+  for (int gr = tid; gr < mp.rows; gr += nt) {
+#pragma unroll
+    for (int c = 0; c < T; ++c) {
+      const int i = gr * T + c;
+      double v = 0.0;
+      if (i < b.xlen) {
+        if (PACK == PACK_SYM) {
+          const int j = i - b.pre;              // s_bar[j] (Eq. (4))
+          if (j >= 0) v = pack_sym(compand1(c_s, sample(2 * j)), compand1(c_s, sample(2 * j + 1)), mp.eps);
+        } else if (PACK == PACK_ASYM2 || PACK == PACK_ASYM3) {
+          constexpr int M = (PACK == PACK_ASYM2) ? 2 : 3;
+          const int base = b.o0 - (g.Np - 1) + i;   // Eq. (7) under C8, Horner (oracle order)
+          v = compand1(c_s, sample(base + (M - 1) * b.S));
+#pragma unroll
+          for (int q = M - 2; q >= 0; --q)
+            v = __dadd_rn(compand1(c_s, sample(base + q * b.S)), __dmul_rn(mp.eps, v));
+        } else {
+          v = sample(b.o0 - (g.Np - 1) + i);
+        }
+      }
+      xs[c * mp.rows + gr] = v;
+    }
   }
   if (e.dbg_packed && PACK != PACK_FULL) {
     double* dp = e.dbg_packed + dbg_row * e.dbg_packed_stride;
     if (PACK == PACK_SYM) {
       for (int j = tid; j < g.W_block / 2; j += nt)
         dp[j] = pack_sym(compand1(c_s, sample(2 * j)), compand1(c_s, sample(2 * j + 1)), mp.eps);
-    } else {
-      for (int i = tid; i < b.xlen; i += nt) dp[i] = xs[(i % T) * mp.rows + i / T];
     }
   }
   if (e.dbg_cs && tid == 0) e.dbg_cs[dbg_row] = c_s;
   __syncthreads();
+  if (!e.stage_raw) mbar_wait(bar, 0);      // taps landed (overlapped with peak + packing)
+  if (e.dbg_packed && PACK != PACK_SYM && PACK != PACK_FULL) {
+    double* dp = e.dbg_packed + dbg_row * e.dbg_packed_stride;
+    for (int i = tid; i < b.xlen; i += nt) dp[i] = xs[(i % T) * mp.rows + i / T];
+  }
 
   // ---- a5: the Tier-2 core on packed words (hot loop)
   const int ngroups = (b.M_out + T - 1) / T;
-  for (int gi = tid; gi < ngroups; gi += nt) {
+  if (e.reg_path) {
     double acc[T];
-    conv_group<T>(xs, mp.rows, kr, mp.K_pad, gi, acc);
+    const bool mine = tid < ngroups;
+    if (mine) conv_group<T>(xs, mp.rows, kr, mp.K_pad, tid, acc);
+    __syncthreads();                         // every warp done reading xs
+    if (mine) {
 #pragma unroll
-    for (int i = 0; i < T; ++i) {
-      const int m = gi * T + i;
-      if (m < b.M_out) Rs[m] = acc[i];
+      for (int i = 0; i < T; ++i) {
+        const int m = tid * T + i;
+        if (m < b.M_out) Rs[m] = acc[i];
+      }
+    }
+  } else {
+    for (int gi = tid; gi < ngroups; gi += nt) {
+      double acc[T];
+      conv_group<T>(xs, mp.rows, kr, mp.K_pad, gi, acc);
+#pragma unroll
+      for (int i = 0; i < T; ++i) {
+        const int m = gi * T + i;
+        if (m < b.M_out) Rs[m] = acc[i];
+      }
     }
   }
   __syncthreads();
@@ -201,7 +240,7 @@ __device__ __forceinline__ void fused_block(const Geo& g, const Exec& e, const M
   }
 
   // ---- a6/a7: unpack, inverse-compand, discard and place (Eqs. (11)-(17))
-  const double cc = __dmul_rn(c_s, mp.c_k);
+  const double inv = dequant_scale(c_s, mp.c_k);   // Eq. (16)
   const long long gbase = b.g0 + b.o0;        // global index of kept output 0
   long long* dri = e.dbg_rint ? e.dbg_rint + dbg_row * e.dbg_rint_stride : nullptr;
   auto store = [&](int k, double rint_v, double val) {
@@ -225,8 +264,8 @@ __device__ __forceinline__ void fused_block(const Geo& g, const Exec& e, const M
       const Digits3 d = decode_sym(Rs[m], mp.eps, mp.eps_inv, mp.pow2);
       const double Bp = (m >= 1) ? decode_sym_B(Rs[m - 1], mp.eps, mp.eps_inv, mp.pow2) : 0.0;
       const double ev = d.C + Bp, od = d.A;
-      store(2 * p, ev, __ddiv_rn(ev, cc));
-      store(2 * p + 1, od, __ddiv_rn(od, cc));
+      store(2 * p, ev, __dmul_rn(ev, inv));
+      store(2 * p + 1, od, __dmul_rn(od, inv));
     }
   } else if (PACK == PACK_ASYM2 || PACK == PACK_ASYM3) {
     constexpr int M = (PACK == PACK_ASYM2) ? 2 : 3;
@@ -237,7 +276,7 @@ __device__ __forceinline__ void fused_block(const Geo& g, const Exec& e, const M
         const double t = rint(v);
         if (q < M - 1) v = __dmul_rn(__dsub_rn(v, t), mp.eps_inv);
         const int k = q * b.S + m;
-        if (k < b.n_out) store(k, t, __ddiv_rn(t, cc));
+        if (k < b.n_out) store(k, t, __dmul_rn(t, inv));
       }
     }
   } else {
@@ -248,7 +287,7 @@ __device__ __forceinline__ void fused_block(const Geo& g, const Exec& e, const M
 // PACK >= 0: one packing for every block.  PACK < 0: per-block packing from e.dec_pack
 // (conv_adapt_block; "switch between asymmetric, symmetric and no packing").
 template <int PACK>
-__global__ void __launch_bounds__(kMaxThreads) pc_fused_kernel(Geo g, Exec e) {
+__global__ void __launch_bounds__(kMaxThreads, 1) pc_fused_kernel(Geo g, Exec e) {
   extern __shared__ __align__(128) unsigned char smem[];
   const long long job = blockIdx.x;
   const long long sig = job / e.nblk;
@@ -261,6 +300,284 @@ __global__ void __launch_bounds__(kMaxThreads) pc_fused_kernel(Geo g, Exec e) {
       case PACK_ASYM2: fused_block<PACK_ASYM2, kT>(g, e, e.mp[PACK_ASYM2], sig, w, smem); break;
       case PACK_ASYM3: fused_block<PACK_ASYM3, kT>(g, e, e.mp[PACK_ASYM3], sig, w, smem); break;
       default: fused_block<PACK_FULL, kT>(g, e, e.mp[PACK_FULL], sig, w, smem); break;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ persistent, warp-specialized
+// pc_persist_kernel: the production form of the fused path.  Each CTA is persistent (grid =
+// SMs x resident CTAs) and pulls overlap-save blocks from a job counter.  Warp roles:
+//   producer warps  a2-a4: block peak (coalesced loads + shuffles), companding, packing of
+//                   block n+1 into shared-memory stage (n+1)&1 -- overlapped with the core
+//   consumer warps  a5-a7: the FP64 core on stage n&1 (one T-output group per thread),
+//                   then unpacking, inverse companding and placement straight from the
+//                   accumulator registers (no shared-memory round trip)
+// Stages are handed over with mbarriers (full: producers -> consumers, empty: back).  The
+// core taps are TMA bulk-copied once per CTA.  Symmetric packing needs B[m-1] of the
+// previous group for its first even output; those pairs are fixed up after a consumer-only
+// named barrier.
+namespace {
+struct PSmem {
+  uint64_t bar_taps, full[2], empty[2];
+  long long job[2];
+  double cs[2];
+  long long prod_job;
+  double red[32];
+};
+}
+
+template <int PACK, int T>
+__device__ __forceinline__ double produce_block(const Geo& g, const Exec& e, const ModeP& mp, long long job,
+                                              double* xs, PSmem* ps, int ptid, int nprod, int bar_id) {
+  const long long sig = job / e.nblk;
+  const long long w = e.b0 + job % e.nblk;
+  const Blk b = block_info<PACK>(g, mp.K, w);
+  const double* __restrict__ s = e.s + sig * e.s_stride;
+  const long long avail = g.L - b.g0;
+  const int n_valid = (int)(avail < 0 ? 0 : (avail > g.W_block ? g.W_block : avail));
+  const double* gsrc = s + (b.g0 - e.s_off);
+  double c_s = 1.0;
+  if (PACK != PACK_FULL) {
+    // block peak: 8 independent loads in flight per thread, then warp shuffles
+    constexpr int U = 8;
+    double m[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) m[u] = 0.0;
+    if ((reinterpret_cast<uintptr_t>(gsrc) & 15u) == 0) {
+      const double2* g2 = reinterpret_cast<const double2*>(gsrc);
+      const int n2 = n_valid / 2;
+      for (int i0 = ptid; i0 < n2; i0 += U * nprod) {
+        double2 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int i = i0 + u * nprod;
+          v[u] = (i < n2) ? __ldg(g2 + i) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) m[u] = fmax(m[u], fmax(fabs(v[u].x), fabs(v[u].y)));
+      }
+      if ((n_valid & 1) && ptid == 0) m[0] = fmax(m[0], fabs(gsrc[n_valid - 1]));
+    } else {
+      for (int i0 = ptid; i0 < n_valid; i0 += U * nprod) {
+        double v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int i = i0 + u * nprod;
+          v[u] = (i < n_valid) ? __ldg(gsrc + i) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) m[u] = fmax(m[u], fabs(v[u]));
+      }
+    }
+#pragma unroll
+    for (int u = 1; u < U; ++u) m[0] = fmax(m[0], m[u]);
+    for (int o = 16; o > 0; o >>= 1) m[0] = fmax(m[0], __shfl_xor_sync(0xffffffffu, m[0], o));
+    if ((ptid & 31) == 0) ps->red[ptid >> 5] = m[0];
+    named_bar(bar_id, nprod);
+    double peak = 0.0;
+    for (int wi = 0; wi < nprod / 32; ++wi) peak = fmax(peak, ps->red[wi]);
+    c_s = (peak == 0.0) ? 1.0 : mp.Q / peak;         // Eq. (2)
+    named_bar(bar_id, nprod);                        // red[] reusable
+  }
+  auto sample = [&](int i) -> double { return (i < 0 || i >= n_valid) ? 0.0 : __ldg(gsrc + i); };
+  // packing: row gr = core words gr*T .. gr*T+T-1, built H words at a time with all the
+  // loads of a half-row issued before use (latency hiding without register spills)
+  constexpr int H = (T > 8) ? T / 2 : T;           // T even: two half-rows
+  for (int gr = ptid; gr < mp.rows; gr += nprod) {
+#pragma unroll
+    for (int h0 = 0; h0 < T; h0 += H) {
+      const int i0 = gr * T + h0;
+      double v[H];
+      if (PACK == PACK_SYM) {
+        double x[2 * H];
+        const int s0 = 2 * (i0 - b.pre);                 // s_bar[j] uses samples 2j, 2j+1 (Eq. (4))
+#pragma unroll
+        for (int c = 0; c < 2 * H; ++c) x[c] = sample(s0 + c);
+#pragma unroll
+        for (int c = 0; c < H; ++c) {
+          const int i = i0 + c;
+          v[c] = (i < b.xlen && i >= b.pre) ? pack_sym(compand1(c_s, x[2 * c]), compand1(c_s, x[2 * c + 1]), mp.eps)
+                                            : 0.0;
+        }
+      } else if (PACK == PACK_ASYM2 || PACK == PACK_ASYM3) {
+        constexpr int M = (PACK == PACK_ASYM2) ? 2 : 3;
+        double x[M][H];
+        const int base = b.o0 - (g.Np - 1) + i0;        // Eq. (7) under C8
+#pragma unroll
+        for (int q = 0; q < M; ++q)
+#pragma unroll
+          for (int c = 0; c < H; ++c) x[q][c] = sample(base + q * b.S + c);
+#pragma unroll
+        for (int c = 0; c < H; ++c) {
+          double a = compand1(c_s, x[M - 1][c]);         // Horner, oracle order
+#pragma unroll
+          for (int q = M - 2; q >= 0; --q) a = __dadd_rn(compand1(c_s, x[q][c]), __dmul_rn(mp.eps, a));
+          v[c] = (i0 + c < b.xlen) ? a : 0.0;
+        }
+      } else {
+        const int base = b.o0 - (g.Np - 1) + i0;
+#pragma unroll
+        for (int c = 0; c < H; ++c) v[c] = (i0 + c < b.xlen) ? sample(base + c) : 0.0;
+      }
+#pragma unroll
+      for (int c = 0; c < H; ++c) xs[(h0 + c) * mp.rows + gr] = v[c];
+    }
+  }
+  return c_s;
+}
+
+template <int PACK, int T>
+__global__ void __maxnreg__(96) pc_persist_kernel(Geo g, Exec e) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  PSmem* ps = reinterpret_cast<PSmem*>(smem);
+  const ModeP& mp = e.mp[PACK];
+  double* kr = reinterpret_cast<double*>(smem + kSmemHeader);
+  double* xsb = kr + mp.K_pad;
+  const int xs_words = T * mp.rows;
+  const int gmax = e.gmax;
+  double* cbase = xsb + 2 * xs_words;                  // [stage][C_first | B_last][gmax]
+  const int tid = threadIdx.x;
+  const int nprod = e.np_warps * 32;
+  const int ncons = blockDim.x - nprod;
+  const long long njobs = e.nblk * e.nsig;
+
+  if (tid == 0) {
+    mbar_init(&ps->bar_taps, 1);
+    mbar_init(&ps->full[0], nprod);
+    mbar_init(&ps->full[1], nprod);
+    mbar_init(&ps->empty[0], ncons);
+    mbar_init(&ps->empty[1], ncons);
+    mbar_arrive_expect_tx(&ps->bar_taps, (uint32_t)mp.K_pad * 8u);
+    bulk_g2s(kr, mp.kr, (uint32_t)mp.K_pad * 8u, &ps->bar_taps);
+  }
+  __syncthreads();
+
+  // Pipeline fill: every warp helps produce the first block into stage 0, then roles split.
+  if (tid == 0) ps->prod_job = (long long)(atomicAdd(e.counter, 1ULL) - e.base);
+  __syncthreads();
+  const long long job0 = ps->prod_job;
+  if (job0 < njobs) {
+    const double c0 = produce_block<PACK, T>(g, e, mp, job0, xsb, ps, tid, blockDim.x, 0);
+    if (tid == 0) {
+      ps->job[0] = job0;
+      ps->cs[0] = c0;
+    }
+  } else if (tid == 0) {
+    ps->job[0] = -1;
+  }
+  __syncthreads();
+  if (tid < nprod) mbar_arrive(&ps->full[0]);
+  if (job0 >= njobs) return;
+
+  if (tid < nprod) {
+    // ======================= producer warps =======================
+    const int ptid = tid;
+    for (int it = 1;; ++it) {
+      const int stage = it & 1;
+      const uint32_t ph = (it >> 1) & 1;
+      named_bar(2, nprod);                             // previous job slot fully read
+      if (ptid == 0) ps->prod_job = (long long)(atomicAdd(e.counter, 1ULL) - e.base);
+      named_bar(2, nprod);
+      const long long job = ps->prod_job;
+      mbar_wait(&ps->empty[stage], ph ^ 1);            // consumers released this stage
+      if (job >= njobs) {
+        if (ptid == 0) ps->job[stage] = -1;
+        mbar_arrive(&ps->full[stage]);
+        break;
+      }
+      const double c_s = produce_block<PACK, T>(g, e, mp, job, xsb + stage * xs_words, ps, ptid, nprod, 2);
+      if (ptid == 0) {
+        ps->job[stage] = job;
+        ps->cs[stage] = c_s;
+      }
+      mbar_arrive(&ps->full[stage]);                   // release: packed words, job, c_s
+    }
+    return;
+  }
+
+  // ======================= consumer warps =======================
+  const int ctid = tid - nprod;
+  mbar_wait(&ps->bar_taps, 0);
+  for (int it = 0;; ++it) {
+    const int stage = it & 1;
+    const uint32_t ph = (it >> 1) & 1;
+    mbar_wait(&ps->full[stage], ph);
+    const long long job = ps->job[stage];
+    if (job < 0) break;
+    const double c_s = ps->cs[stage];
+    const long long sig = job / e.nblk;
+    const long long w = e.b0 + job % e.nblk;
+    const Blk b = block_info<PACK>(g, mp.K, w);
+    const double* xs = xsb + stage * xs_words;
+    double* __restrict__ r = e.r + sig * e.r_stride;
+    const double inv = dequant_scale(c_s, mp.c_k);   // Eq. (16)
+    const long long gbase = b.g0 + b.o0;
+    auto store = [&](int k, double val) {
+      const long long gi = gbase + k;
+      if (g.mode == 0) {
+        if (gi < g.L + g.N - 1) r[gi - e.r_off] = val;
+      } else {
+        const long long j = gi - (g.N - 1);              // valid lag (C17)
+        if (j >= 0 && j <= g.L - g.N) r[j - e.r_off] = val;
+      }
+    };
+    double* cfirst = cbase + stage * 2 * gmax;
+    double* blast = cfirst + gmax;
+    const int ngroups = (b.M_out + T - 1) / T;
+    const int moff = (w == 0) ? 0 : 1;
+    for (int gi = ctid; gi < ngroups; gi += ncons) {
+      double acc[T];
+      conv_group<T>(xs, mp.rows, kr, mp.K_pad, gi, acc);          // a5
+      if (PACK == PACK_SYM) {                                      // a6/a7, Eqs. (12)-(17)
+        double Bprev = 0.0;
+#pragma unroll
+        for (int i = 0; i < T; ++i) {
+          const int m = gi * T + i;
+          const Digits3 d = decode_sym(acc[i], mp.eps, mp.eps_inv, mp.pow2);
+          if (m < b.M_out && m >= moff) {
+            const int k = 2 * (m - moff);
+            store(k + 1, __dmul_rn(d.A, inv));
+            if (i > 0 || m == 0) {
+              const double ev = d.C + Bprev;
+              store(k, __dmul_rn(ev, inv));
+            } else {
+              cfirst[gi] = d.C;                                    // needs B of group gi-1
+            }
+          }
+          Bprev = d.B;
+        }
+        blast[gi] = Bprev;
+      } else if (PACK == PACK_ASYM2 || PACK == PACK_ASYM3) {
+        constexpr int M = (PACK == PACK_ASYM2) ? 2 : 3;
+#pragma unroll
+        for (int i = 0; i < T; ++i) {
+          const int m = gi * T + i;
+          if (m < b.S) {
+            double v = acc[i];
+#pragma unroll
+            for (int q = 0; q < M; ++q) {                          // balanced digits (C9)
+              const double t = rint_fast(v);
+              if (q < M - 1) v = __dmul_rn(__dsub_rn(v, t), mp.eps_inv);
+              const int k = q * b.S + m;
+              if (k < b.n_out) store(k, __dmul_rn(t, inv));
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < T; ++i) {
+          const int m = gi * T + i;
+          if (m < b.n_out) store(m, acc[i]);
+        }
+      }
+    }
+    mbar_arrive(&ps->empty[stage]);                                // done reading xs[stage]
+    if (PACK == PACK_SYM) {
+      named_bar(1, ncons);
+      for (int gi = ctid + (ctid == 0 ? ncons : 0); gi < ngroups; gi += ncons) {
+        const int m = gi * T;                                      // gi >= 1
+        if (m < b.M_out && m >= moff) store(2 * (m - moff), __dmul_rn(cfirst[gi] + blast[gi - 1], inv));
+      }
     }
   }
 }
@@ -384,6 +701,49 @@ cudaError_t launch_fused(int packing, const Geo& g, const Exec& e, long long n_j
     case PACK_ASYM2: return launch_fused_t<PACK_ASYM2>(g, e, n_jobs, threads, smem, st);
     case PACK_ASYM3: return launch_fused_t<PACK_ASYM3>(g, e, n_jobs, threads, smem, st);
     case -1: return launch_fused_t<-1>(g, e, n_jobs, threads, smem, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int PACK, int T>
+static cudaError_t launch_persist_t(const Geo& g, const Exec& e, long long n_jobs, int threads, size_t smem,
+                                    cudaStream_t st, int* grid_out) {
+  auto kfn = pc_persist_kernel<PACK, T>;
+  cudaError_t err = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (err != cudaSuccess) return err;
+  int occ = 0, dev = 0, sms = 0;
+  err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, threads, smem);
+  if (err != cudaSuccess) return err;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (occ < 1) return cudaErrorInvalidConfiguration;
+  long long grid = (long long)sms * occ;
+  if (grid > n_jobs) grid = n_jobs;
+  *grid_out = (int)grid;
+  kfn<<<(unsigned)grid, threads, smem, st>>>(g, e);
+  return cudaGetLastError();
+}
+
+template <int T>
+static cudaError_t launch_persist_T(int packing, const Geo& g, const Exec& e, long long n_jobs, int threads,
+                                    size_t smem, cudaStream_t st, int* grid_out) {
+  switch (packing) {
+    case PACK_FULL: return launch_persist_t<PACK_FULL, T>(g, e, n_jobs, threads, smem, st, grid_out);
+    case PACK_SYM: return launch_persist_t<PACK_SYM, T>(g, e, n_jobs, threads, smem, st, grid_out);
+    case PACK_ASYM2: return launch_persist_t<PACK_ASYM2, T>(g, e, n_jobs, threads, smem, st, grid_out);
+    case PACK_ASYM3: return launch_persist_t<PACK_ASYM3, T>(g, e, n_jobs, threads, smem, st, grid_out);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_persist(int packing, int T, const Geo& g, const Exec& e, long long n_jobs, int threads,
+                           size_t smem, cudaStream_t st, int* grid_out) {
+  *grid_out = 0;
+  if (n_jobs <= 0) return cudaSuccess;
+  switch (T) {
+    case 12: return launch_persist_T<12>(packing, g, e, n_jobs, threads, smem, st, grid_out);
+    case 14: return launch_persist_T<14>(packing, g, e, n_jobs, threads, smem, st, grid_out);
+    case 16: return launch_persist_T<16>(packing, g, e, n_jobs, threads, smem, st, grid_out);
   }
   return cudaErrorInvalidValue;
 }

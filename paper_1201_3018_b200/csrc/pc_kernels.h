@@ -6,8 +6,11 @@
 
 namespace pc {
 
-constexpr int kT = 8;              // outputs per thread of the direct core (register tile)
-constexpr int kMaxThreads = 256;   // threads per CTA (one CTA per overlap-save block)
+constexpr int kT = 8;              // outputs per thread of the per-block kernel's core
+constexpr int kMaxThreads = 1024;  // per-block kernel: threads per CTA; caps regs at 64
+constexpr int kTP = 16;            // largest outputs-per-thread tile of the persistent kernel
+constexpr int kTPChoices[3] = {16, 14, 12};   // tiles instantiated; the plan picks by lane use
+constexpr int kMaxThreadsP = 512;  // persistent kernel: threads per CTA; caps regs at 128
 constexpr int kSmemHeader = 512;   // mbarrier + reduction scratch, keeps the rest 128B-aligned
 
 // Per-packing parameters of one launch (adaptive plans fill several).
@@ -17,7 +20,7 @@ struct ModeP {
   double c_k;           // kernel companding factor
   double eps, eps_inv;  // packing coefficient and its inverse
   int pow2;             // eps = 2^-b (reading C4)
-  int K, K_pad;         // core taps and taps padded to a multiple of kT
+  int K, K_pad;         // core taps and taps padded to a multiple of the kernel's tile T
   int rows;             // rows of the column layout of the core's input words
 };
 
@@ -28,8 +31,15 @@ struct Exec {
   long long r_off, r_stride;
   long long b0, nblk;   // block range [b0, b0 + nblk) of every signal; grid = n_sig * nblk
   int stage_raw;        // stage the W_block raw samples in shared memory (TMA bulk copy)
+  int reg_path;         // every block has <= blockDim.x groups: results stay in registers
   ModeP mp[4];          // indexed by packing (PACK_FULL .. PACK_ASYM3)
   const int* dec_pack;  // adaptive: per (signal, block) packing, else nullptr
+  // persistent warp-specialized kernel
+  unsigned long long* counter;  // monotonically increasing job counter (plan-owned)
+  unsigned long long base;      // counter value at launch start
+  int np_warps, nc_warps;       // producer / consumer warps per CTA
+  int gmax;                     // max T-groups of any block (sym fix-up arrays)
+  long long nsig;               // signals in the launch (jobs = nsig * nblk)
   // parity/debug dumps (row = sig * P + w), nullptr in production
   double* dbg_packed;
   long long dbg_packed_stride;
@@ -42,6 +52,9 @@ struct Exec {
 
 cudaError_t launch_fused(int packing, const Geo& g, const Exec& e, long long n_jobs, int threads, size_t smem,
                          cudaStream_t st);
+// Persistent warp-specialized variant: grid = SMs x resident CTAs; returns the grid used.
+cudaError_t launch_persist(int packing, int T, const Geo& g, const Exec& e, long long n_jobs, int threads,
+                           size_t smem, cudaStream_t st, int* grid_out);
 cudaError_t launch_kernel_prep(const double* k_in, int N, int Np, int reverse, double K_q, double* k_pad,
                                double* k_int, double* scal, cudaStream_t st);
 cudaError_t launch_build_taps(const double* k_pad, const double* k_int, int Np, int packing, double eps_inv, int K,

@@ -29,9 +29,11 @@ def dev(x):
     return torch.from_numpy(np.ascontiguousarray(x)).to(DEV)
 
 
-def gpu_run(s, k, W_block, packing, Q, mode=O.CONV, eps_rule=O.EPS_POW2, rmax_rule=O.RMAX_PAPER, debug=True):
-    with pcb.Plan(len(s), len(k), W_block, mode, PK[packing], Q, eps_rule=EPS[eps_rule],
-                  rmax_rule=rmax_rule, bound_policy=pcb.BOUND_WARN) as p:
+def gpu_run(s, k, W_block, packing, Q, mode=O.CONV, eps_rule=O.EPS_POW2, rmax_rule=O.RMAX_PAPER, debug=True,
+            tile=0):
+    opts = pcb.opts_default(eps_rule=EPS[eps_rule], rmax_rule=rmax_rule, bound_policy=pcb.BOUND_WARN)
+    opts.reserved[1] = tile
+    with pcb.Plan(len(s), len(k), W_block, mode, PK[packing], Q, opts=opts) as p:
         p.set_kernel(dev(k))
         info = p.info()
         s_d = dev(s)
@@ -80,6 +82,8 @@ def test_packed_bit_exact_pow2(packing, case):
     L, N, W_block, Q = case
     rng = np.random.default_rng(L * 7 + N)
     s, k = rng.laplace(0, 0.3, L), rng.uniform(-1, 1, N)
+    Np = N | 1
+    Q = min(Q, O.max_q_under_bound(None, Np, packing, O.EPS_POW2, O.RMAX_PAPER))   # Eq. (3) within bound
     ref = O.conv_pipeline(s, k, W_block, packing, Q, keep_blocks=True)
     assert ref.kernel.bound_ok and ref.mismatches == 0
     g = gpu_run(s, k, W_block, packing, Q)
@@ -87,6 +91,25 @@ def test_packed_bit_exact_pow2(packing, case):
     assert g["info"]["eps_inv"] == ref.kernel.eps.eps_inv
     check_blocks(g, ref, packing)
     assert np.array_equal(g["r_dbg"], ref.out)
+    assert np.array_equal(g["r"], ref.out)
+
+
+@pytest.mark.parametrize("tile", [12, 14, 16])
+@pytest.mark.parametrize("packing", [O.FULL, O.SYM, O.ASYM2, O.ASYM3])
+@pytest.mark.parametrize("case", [(20000, 513, 4096, 31), (4097, 64, 1024, 60), (9000, 100, 512, 15)])
+def test_every_core_tile(tile, packing, case):
+    """The persistent kernel's tile T (12/14/16) is chosen per plan; force each one."""
+    L, N, W_block, Q = case
+    rng = np.random.default_rng(N + tile)
+    s, k = rng.laplace(0, 0.3, L), rng.uniform(-1, 1, N)
+    if packing == O.FULL:
+        g = gpu_run(s, k, W_block, O.FULL, 0, debug=False, tile=tile)
+        want = O.full_precision(s, k)
+        assert np.max(np.abs(g["r"] - want)) / np.max(np.abs(want)) < 1e-12
+        return
+    Q = min(Q, O.max_q_under_bound(None, N | 1, packing, O.EPS_POW2, O.RMAX_PAPER))
+    ref = O.conv_pipeline(s, k, W_block, packing, Q)
+    g = gpu_run(s, k, W_block, packing, Q, debug=False, tile=tile)
     assert np.array_equal(g["r"], ref.out)
 
 
@@ -123,8 +146,9 @@ def test_full_precision_within_1e12(case):
 def test_xcorr_mode(packing):
     rng = np.random.default_rng(5)
     s, q = rng.laplace(0, 0.3, 9000), rng.uniform(-1, 1, 100)
-    ref = O.conv_pipeline(s, q, 512, packing, 63, mode=O.XCORR, keep_blocks=True)
-    g = gpu_run(s, q, 512, packing, 63, mode=O.XCORR, debug=packing != O.FULL)
+    Q = {O.FULL: 0, O.SYM: 31, O.ASYM2: 63}[packing]          # within Table 1 / dyadic bounds
+    ref = O.conv_pipeline(s, q, 512, packing, Q, mode=O.XCORR, keep_blocks=True)
+    g = gpu_run(s, q, 512, packing, Q, mode=O.XCORR, debug=packing != O.FULL)
     assert g["r"].shape == (9000 - 100 + 1,)
     if packing == O.FULL:
         want = O.full_precision(s, q, O.XCORR)
@@ -237,7 +261,18 @@ def test_adaptive_decisions_and_output(floor):
         r = torch.empty(info["L_out"], dtype=torch.float64, device=DEV)
         p.execute(s_d, r)
         torch.cuda.synchronize()
-        assert np.array_equal(r.cpu().numpy(), y_ref)
+        got = r.cpu().numpy()
+    # packed blocks bit-exact; full-precision blocks (SNR = inf) within 1e-12 (C16)
+    geom = O.Geometry(len(s), len(k), W_block)
+    for w, (m, q, _) in enumerate(dec_ref):
+        g0 = geom.block_start(w)
+        o0, n_out = geom.kept(w)
+        lo, hi = g0 + o0, min(g0 + o0 + n_out, geom.L_out)
+        if m == O.FULL:
+            scale = max(np.max(np.abs(y_ref[lo:hi])), 1e-300)
+            assert np.max(np.abs(got[lo:hi] - y_ref[lo:hi])) / scale < 1e-12, w
+        else:
+            assert np.array_equal(got[lo:hi], y_ref[lo:hi]), w
 
 
 def test_xcorr_max_scores():

@@ -9,6 +9,6 @@ if [ "$1" == "ncu" ]; then
   CMD="python bench.py --steps 3 --warmup 3 --points asym2_10b,full --no-cpu-baseline"
   timeout 300 $CMD > gpurun_out/ncu_plain.log 2>&1 && \
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:pc_fused_kernel -s 3 -c 1 -o gpurun_out/prof_asym2 $CMD > gpurun_out/ncu_full.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:pc_.*_kernel -s 3 -c 1 -o gpurun_out/prof_asym2 $CMD > gpurun_out/ncu_full.log 2>&1
   echo "ncu rc=$?" >> gpurun_out/ncu_full.log
 fi
