@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--workload", default="cfg2")
     ap.add_argument("--points", default=",".join(POINTS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--L", type=int, default=0, help="override the workload length (scaling studies)")
     return ap.parse_args()
 
 
@@ -131,10 +132,10 @@ def barrier(ws):
         dist.barrier()
 
 
-def workload(name, rank):
+def workload(name, rank, L=0):
     from paper_1201_3018_b200 import workloads as WL
     if name == "cfg2":
-        s, k = WL.cfg2(seed=rank)
+        s, k = WL.cfg2(seed=rank, L=L or (1 << 22))
         return s, k, 4096
     if name == "cfg1":
         s, k = WL.cfg1(seed=rank)
@@ -200,7 +201,7 @@ def run_ours(args, ws, rank, local):
     from paper_1201_3018_b200 import binding as pcb
 
     dev = torch.device("cuda", local)
-    s, k, W_block = workload(args.workload, rank)
+    s, k, W_block = workload(args.workload, rank, args.L)
     L, N = len(s), len(k)
     L_out = L + N - 1
     n_buf = max(2, -(-256 * (1 << 20) // (16 * L)))     # rotating buffers: > 126 MB L2 in total

@@ -68,7 +68,8 @@ typedef struct conv_opts {
   int32_t K_q;              /* kernel companding range; 0 means K_q = S_q = Q       */
   int32_t device;           /* CUDA device ordinal, -1 = current device                    */
   int32_t reserved[9];      /* [0]: raw-block staging 0 auto/1 on/2 off (per-block kernel);
-                               [1]: force the persistent core tile (12/14/16; tests); rest 0 */
+                               [1]: force the persistent core tile (12/14/16; tests);
+                               [2]: cap persistent CTAs per SM (diagnostics); rest 0 */
   double u_sys;             /* P:153; used only by the literal paper unpack form          */
 } conv_opts;
 
@@ -162,6 +163,14 @@ int conv_execute_debug(conv_plan* plan, const double* s_dev, double* r_dev, doub
  * Synchronizes `stream`. */
 int conv_adapt_block(conv_plan* plan, const double* s_dev, double snr_floor_db,
                      double calib_offset_db, conv_block_decision* out_host, void* stream);
+
+/* Diagnostics: conv_execute that also records, per persistent CTA c, four uint64 at
+ * cta_records_dev[4c..4c+3] = {SM id, start and end %globaltimer (ns), blocks processed};
+ * the buffer must hold 8 * 148 * 32 entries; entries [4*148*32 + 4c ..] receive CTA c's
+ * consumer-thread-0 clock64 totals {waiting for a packed stage, core, decode+store, fix-up}.  *grid_out receives the CTA count (0 if the
+ * plan runs the per-block kernel, which records nothing). */
+int conv_execute_profile(conv_plan* plan, const double* s_dev, double* r_dev, uint64_t* cta_records_dev,
+                         int32_t* grid_out, void* stream);
 
 int conv_plan_query(const conv_plan* plan, conv_plan_info* info);
 void conv_plan_destroy(conv_plan* plan);

@@ -12,7 +12,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpackedconv.so")
+LIB_PATH = os.environ.get("PC_LIB_PATH") or os.path.join(_HERE, "libpackedconv.so")   # override: experiments
 
 PC_OK, PC_E_CONFIG, PC_E_BOUND, PC_E_BACKEND, PC_E_CUDA, PC_W_UNPACK_MARGIN, PC_E_STATE = 0, 2, 3, 4, 5, 6, 7
 MODE_CONV, MODE_XCORR = 0, 1
@@ -77,6 +77,7 @@ def load():
             "conv_execute_debug": (C.c_int, [P, VP, VP, VP, VP, VP, VP, VP]),
             "conv_adapt_block": (C.c_int, [P, VP, D, D, C.POINTER(conv_block_decision), VP]),
             "conv_plan_query": (C.c_int, [P, C.POINTER(conv_plan_info)]),
+            "conv_execute_profile": (C.c_int, [P, VP, VP, VP, C.POINTER(C.c_int32), VP]),
             "conv_plan_destroy": (None, [P]),
             "conv_status_string": (C.c_char_p, [C.c_int]),
         }
@@ -178,6 +179,15 @@ def adapt_block(plan, s_dev, snr_floor_db, calib_offset_db=0.0, P=None, stream=N
     _check(load().conv_adapt_block(plan, _ptr(s_dev), float(snr_floor_db), float(calib_offset_db), out,
                                    _stream(stream)), "conv_adapt_block")
     return [(d.packing, d.Q, d.snr_lin) for d in out] if out is not None else None
+
+
+def execute_profile(plan, s_dev, r_dev, records_dev, stream=None):
+    """Returns the persistent grid size; records_dev (uint64, 4*148*32) gets per-CTA
+    {smid, t_start_ns, t_end_ns, blocks}."""
+    g = C.c_int32()
+    _check(load().conv_execute_profile(plan, _ptr(s_dev), _ptr(r_dev), _ptr(records_dev), C.byref(g),
+                                       _stream(stream)), "conv_execute_profile")
+    return g.value
 
 
 def plan_query(plan):

@@ -154,7 +154,8 @@ void set_core_layout(const conv_plan* p, int packing, ModeState* m) {
   }
   const int force = p->opts.reserved[1];   // test hook: force the persistent tile
   if (force == 12 || force == 14 || force == 16) m->TP = force;
-  layout_for(m->K, mmax, m->TP, &m->K_padP, &m->rowsP);
+  m->K_padP = (m->K + m->TP - 1) / m->TP * m->TP;
+  m->rowsP = (mmax + m->TP - 1) / m->TP + m->K_padP / m->TP + 1;
 }
 
 // Launch shape of the fused kernel for the packings that may run in this plan.
@@ -222,7 +223,7 @@ bool persist_shape(const conv_plan* p, int packing, PShape* sh) {
   if (nc > pc::kMaxThreadsP / 32 - sh->np_warps) nc = pc::kMaxThreadsP / 32 - sh->np_warps;
   sh->nc_warps = nc;
   sh->threads = 32 * (sh->np_warps + nc);
-  sh->smem = pc::kSmemHeader + (size_t)m.K_padP * 8 + 2 * (size_t)T * m.rowsP * 8 + 4 * (size_t)sh->gmax * 8;
+  sh->smem = pc::kSmemHeader + (size_t)m.K_padP * 8 + 2 * (size_t)(T + 1) * m.rowsP * 8 + 4 * (size_t)sh->gmax * 8;
   return sh->smem <= kMaxSmem;
 }
 
@@ -253,7 +254,8 @@ int plan_packs(const conv_plan* p, int* packs) {
 }
 
 int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride, double* r, long long r_off,
-              long long r_stride, long long b0, long long nblk, long long n_sig, Exec* dbg, cudaStream_t st) {
+              long long r_stride, long long b0, long long nblk, long long n_sig, Exec* dbg, cudaStream_t st,
+              unsigned long long* timing = nullptr, int* grid_out = nullptr) {
   if (!p->kernel_set) return PC_E_STATE;
   if (p->packing == PC_PACK_ADAPTIVE && !p->adapt_ready) return PC_E_STATE;
   if (nblk <= 0 || n_sig <= 0) return PC_OK;
@@ -282,6 +284,8 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
   if (!dbg && p->packing != PC_PACK_ADAPTIVE && p->opts.exec == PC_EXEC_FUSED && persist_shape(p, p->packing, &ps)) {
     e.counter = p->d_counter;
     e.base = p->counter_base;
+    e.dbg_timing = timing;
+    e.max_ctas_per_sm = p->opts.reserved[2];
     e.np_warps = ps.np_warps;
     e.nc_warps = ps.nc_warps;
     e.gmax = ps.gmax;
@@ -292,6 +296,7 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
                                          ps.smem, st, &grid);
     if (err != cudaSuccess) return PC_E_CUDA;
     p->counter_base += (unsigned long long)(nblk * n_sig) + (unsigned long long)grid;
+    if (grid_out) *grid_out = grid;
     return PC_OK;
   }
   return cuda_status(pc::launch_fused(launch_pack, make_geo(p), e, nblk * n_sig, sh.threads, sh.smem, st));
@@ -692,6 +697,16 @@ int conv_adapt_block(conv_plan* p, const double* s, double snr_floor_db, double 
   }
   p->adapt_ready = 1;
   return PC_OK;
+}
+
+int conv_execute_profile(conv_plan* p, const double* s, double* r, uint64_t* rec, int32_t* grid_out, void* stream) {
+  if (!p || !s || !r || !rec || !grid_out) return PC_E_CONFIG;
+  if (cudaSetDevice(p->device) != cudaSuccess) return PC_E_CUDA;
+  int grid = 0;
+  const int rc = run_exec(p, s, 0, 0, r, 0, 0, 0, p->P, 1, nullptr, (cudaStream_t)stream,
+                          reinterpret_cast<unsigned long long*>(rec), &grid);
+  *grid_out = grid;
+  return rc;
 }
 
 int conv_plan_query(const conv_plan* p, conv_plan_info* info) {

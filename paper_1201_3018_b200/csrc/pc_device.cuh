@@ -87,13 +87,17 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 __device__ __forceinline__ void named_bar(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
+#ifndef PC_SUSPEND_HINT_NS
+#define PC_SUSPEND_HINT_NS 1000u
+#endif
+constexpr uint32_t kSuspendHintNs = PC_SUSPEND_HINT_NS;
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "PC_WAIT_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra PC_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(phase), "r"(0x989680u)   // suspend-time hint (ns): sleep instead of spinning
+      "r"(phase), "r"(kSuspendHintNs)   // suspend-time hint (ns): sleep instead of spinning
       : "memory");
 }
 
@@ -175,6 +179,46 @@ __device__ __forceinline__ void conv_group(const double* __restrict__ xs, int ro
     for (int u = 0; u < T; ++u) {
       // new word x[gT + j0 + T-1 + u] -> column (T-1+u) % T, row g + r0 + (T-1+u) / T
       win[(T - 1 + u) % T] = xcol[((T - 1 + u) % T) * rows + r0 + (T - 1 + u) / T];
+#pragma unroll
+      for (int i = 0; i < T; ++i) acc[i] = fma(win[(i + u) % T], kk[u], acc[i]);
+    }
+  }
+}
+
+// Padded row-major layout (persistent kernel): word i of the core's input lives at
+// xs[(i / T) * (T + 1) + i % T].  Thread group g reads rows g, g+1, ...; the odd row pitch
+// T+1 makes lane-consecutive rows conflict-free (2 wavefronts per 8-byte warp load), and
+// every load of the unrolled tap loop is the thread's row pointer plus an immediate.
+__device__ __forceinline__ double lds64(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ double2 lds128(uint32_t a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+  return v;
+}
+template <int T>
+__device__ __forceinline__ void conv_group_padded(uint32_t xs_row, uint32_t kr_addr, int K_pad, double (&acc)[T]) {
+  double win[T];
+#pragma unroll
+  for (int i = 0; i < T; ++i) acc[i] = 0.0;
+#pragma unroll
+  for (int c = 0; c < T - 1; ++c) win[c] = lds64(xs_row + 8u * c);
+  uint32_t xa = xs_row, ka = kr_addr;
+  for (int j0 = 0; j0 < K_pad; j0 += T, xa += 8u * (T + 1), ka += 8u * T) {
+    double kk[T];
+#pragma unroll
+    for (int u = 0; u < T; u += 2) {
+      const double2 k2 = lds128(ka + 8u * u);
+      kk[u] = k2.x;
+      kk[u + 1] = k2.y;
+    }
+#pragma unroll
+    for (int u = 0; u < T; ++u) {
+      // new word x[gT + j0 + T-1 + u]: row +(T-1+u)/T, column (T-1+u)%T
+      win[(T - 1 + u) % T] = lds64(xa + 8u * (((T - 1 + u) / T) * (T + 1) + (T - 1 + u) % T));
 #pragma unroll
       for (int i = 0; i < T; ++i) acc[i] = fma(win[(i + u) % T], kk[u], acc[i]);
     }

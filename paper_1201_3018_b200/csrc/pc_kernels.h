@@ -39,6 +39,7 @@ struct Exec {
   unsigned long long base;      // counter value at launch start
   int np_warps, nc_warps;       // producer / consumer warps per CTA
   int gmax;                     // max T-groups of any block (sym fix-up arrays)
+  int max_ctas_per_sm;          // diagnostics: cap on resident CTAs per SM (0 = occupancy)
   long long nsig;               // signals in the launch (jobs = nsig * nblk)
   // parity/debug dumps (row = sig * P + w), nullptr in production
   double* dbg_packed;
@@ -48,6 +49,7 @@ struct Exec {
   long long* dbg_rint;
   long long dbg_rint_stride;
   double* dbg_cs;
+  unsigned long long* dbg_timing;   // persistent kernel: per CTA {smid, t_start, t_end, jobs}
 };
 
 cudaError_t launch_fused(int packing, const Geo& g, const Exec& e, long long n_jobs, int threads, size_t smem,
