@@ -295,9 +295,20 @@ def run_ours(args, ws, rank, local):
         return
     h = results[HEADLINE]
     full = results.get("full")
+    traffic, traffic_src = None, None
+    prof = os.path.join(ROOT, "profiles", "r01_ncu_cfg2.json")
+    kname = f"pc_persist_kernel<2, {h['tile']}>"
+    if args.workload == "cfg2" and os.path.exists(prof):
+        for rec in json.load(open(prof)).get("ncu_full", []):
+            if kname in rec["kernel"]:
+                rd = float(rec["dram__bytes_read.sum"].split()[0]) * (1e6 if "Mbyte" in rec["dram__bytes_read.sum"] else 1e3)
+                wr = rec["dram__bytes_write.sum"].split()
+                wr = float(wr[0]) * (1e6 if wr[1] == "Mbyte" else 1e3 if wr[1] == "Kbyte" else 1.0)
+                traffic, traffic_src = rd + wr, "profiles/r01_ncu_cfg2.json (ncu --set full, one launch)"
     roof = {"bound": "alu", "achieved": h["fp64_tflops"], "peak": MEASURED_FP64_TFLOPS, "unit": "TFLOP/s",
-            "frac": h["fp64_tflops"] / MEASURED_FP64_TFLOPS, "traffic": None,
-            "kernel": "pc_fused_kernel<ASYM2>", "peak_source": FP64_PEAK_SOURCE,
+            "frac": h["fp64_tflops"] / MEASURED_FP64_TFLOPS, "traffic": traffic, "traffic_unit": "bytes/launch",
+            "traffic_source": traffic_src, "algorithmic_bytes": 8 * (L + L_out),
+            "kernel": kname, "peak_source": FP64_PEAK_SOURCE,
             "algorithmic": "FP64 FMAs of the packed core: sum over blocks of M_out * N' (2 flop each)"}
     line = {
         "metric": "output samples/s, packed vs full-precision conv, 1/2/4/8 B200; % FP64/HBM peak",
