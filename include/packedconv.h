@@ -105,6 +105,16 @@ typedef struct conv_block_decision {
   double snr_lin;           /* Eq. (19) linear prediction (inf for FULL)                    */
 } conv_block_decision;
 
+/* Block-range shard of one rank: blocks [block_begin, block_end), the
+ * input samples it reads [in_begin, in_end) (its range plus the N'+1-sample overlap-save
+ * halo, clipped to L) and the outputs it writes [out_begin, out_end) (conv: global output
+ * index; xcorr: lag index).  Ranks' output ranges are disjoint and cover all outputs. */
+typedef struct conv_shard {
+  int64_t block_begin, block_end;
+  int64_t in_begin, in_end;
+  int64_t out_begin, out_end;
+} conv_shard;
+
 typedef struct conv_plan conv_plan;
 
 void conv_opts_default(conv_opts* opts);
@@ -171,6 +181,12 @@ int conv_adapt_block(conv_plan* plan, const double* s_dev, double snr_floor_db,
  * plan runs the per-block kernel, which records nothing). */
 int conv_execute_profile(conv_plan* plan, const double* s_dev, double* r_dev, uint64_t* cta_records_dev,
                          int32_t* grid_out, void* stream);
+
+/* Host-only (no device needed): the shard of `rank` among `world` ranks for a plan of the
+ * same (L, N, W_block, mode): blocks [P*rank/world, P*(rank+1)/world).  PC_E_CONFIG on
+ * invalid geometry. */
+int conv_shard_range(int64_t L, int32_t N, int32_t W_block, int32_t mode, int32_t rank, int32_t world,
+                     conv_shard* out);
 
 int conv_plan_query(const conv_plan* plan, conv_plan_info* info);
 void conv_plan_destroy(conv_plan* plan);

@@ -44,6 +44,11 @@ class conv_plan_info(C.Structure):
                 ("q_mode", C.c_int32 * 4), ("core_tile", C.c_int32), ("reserved_i", C.c_int32)]
 
 
+class conv_shard(C.Structure):
+    _fields_ = [("block_begin", C.c_int64), ("block_end", C.c_int64), ("in_begin", C.c_int64),
+                ("in_end", C.c_int64), ("out_begin", C.c_int64), ("out_end", C.c_int64)]
+
+
 class conv_block_decision(C.Structure):
     _fields_ = [("packing", C.c_int32), ("Q", C.c_int32), ("snr_lin", C.c_double)]
 
@@ -78,6 +83,7 @@ def load():
             "conv_adapt_block": (C.c_int, [P, VP, D, D, C.POINTER(conv_block_decision), VP]),
             "conv_plan_query": (C.c_int, [P, C.POINTER(conv_plan_info)]),
             "conv_execute_profile": (C.c_int, [P, VP, VP, VP, C.POINTER(C.c_int32), VP]),
+            "conv_shard_range": (C.c_int, [I64, I32, I32, I32, I32, I32, C.POINTER(conv_shard)]),
             "conv_plan_destroy": (None, [P]),
             "conv_status_string": (C.c_char_p, [C.c_int]),
         }
@@ -188,6 +194,14 @@ def execute_profile(plan, s_dev, r_dev, records_dev, stream=None):
     _check(load().conv_execute_profile(plan, _ptr(s_dev), _ptr(r_dev), _ptr(records_dev), C.byref(g),
                                        _stream(stream)), "conv_execute_profile")
     return g.value
+
+
+def shard_range(L, N, W_block, mode, rank, world):
+    """Host-only block-range shard of `rank` (conv_shard_range) as a dict."""
+    sh = conv_shard()
+    _check(load().conv_shard_range(int(L), int(N), int(W_block), int(mode), int(rank), int(world), C.byref(sh)),
+           "conv_shard_range")
+    return {name: getattr(sh, name) for name, _ in conv_shard._fields_}
 
 
 def plan_query(plan):

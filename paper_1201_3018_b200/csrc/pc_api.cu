@@ -709,6 +709,42 @@ int conv_execute_profile(conv_plan* p, const double* s, double* r, uint64_t* rec
   return rc;
 }
 
+int conv_shard_range(int64_t L, int32_t N, int32_t W_block, int32_t mode, int32_t rank, int32_t world,
+                     conv_shard* out) {
+  if (!out || L < 1 || N < 1 || world < 1 || rank < 0 || rank >= world) return PC_E_CONFIG;
+  if (mode == PC_MODE_XCORR && L < N) return PC_E_CONFIG;
+  const long long Np = (N % 2) ? N : N + 1;
+  const long long W = (long long)W_block - Np - 1;
+  if (W < 2 || (W % 2) || W < 2 * Np) return PC_E_CONFIG;
+  const long long P = (L + W - 1) / W;
+  const long long b0 = P * rank / world, b1 = P * (rank + 1) / world;
+  out->block_begin = b0;
+  out->block_end = b1;
+  if (b0 == b1) {
+    out->in_begin = out->in_end = out->out_begin = out->out_end = 0;
+    return PC_OK;
+  }
+  // block w reads [g0(w), g0(w) + W_block) with g0(0) = 0, g0(w) = wW - 2 (reading C7)
+  const long long g_first = b0 == 0 ? 0 : b0 * W - 2;
+  const long long g_last = (b1 - 1) == 0 ? 0 : (b1 - 1) * W - 2;
+  out->in_begin = g_first < L ? g_first : L;
+  out->in_end = (g_last + W_block) < L ? (g_last + W_block) : L;
+  // block 0 keeps global [0, W+N'-1); block w >= 1 keeps [N'-1+wW, N'-1+(w+1)W) (Eq. (17))
+  const long long L_conv = L + N - 1;
+  long long o0 = b0 == 0 ? 0 : Np - 1 + b0 * W;
+  long long o1 = Np - 1 + b1 * W;
+  if (o1 > L_conv) o1 = L_conv;
+  if (o0 > L_conv) o0 = L_conv;
+  if (mode == PC_MODE_XCORR) {                        // lag j = global output - (N-1), 0..L-N
+    const long long lo = N - 1, hi = L;               // valid global outputs [N-1, L)
+    o0 = (o0 < lo ? lo : (o0 > hi ? hi : o0)) - lo;
+    o1 = (o1 < lo ? lo : (o1 > hi ? hi : o1)) - lo;
+  }
+  out->out_begin = o0;
+  out->out_end = o1;
+  return PC_OK;
+}
+
 int conv_plan_query(const conv_plan* p, conv_plan_info* info) {
   if (!p || !info) return PC_E_CONFIG;
   std::memset(info, 0, sizeof(*info));
