@@ -221,6 +221,7 @@ class Plan:
     """Owning wrapper: ``with Plan(L, N, W_block, ...) as p: p.set_kernel(k); p.execute(s, r)``."""
 
     def __init__(self, L, N, W_block, mode=MODE_CONV, packing=PACK_SYM, Q=127, **opts):
+        self.h = None
         self.h = plan_create(L, N, W_block, mode, packing, Q, **opts)
 
     def set_kernel(self, k_dev, stream=None):
@@ -252,7 +253,7 @@ class Plan:
         return plan_query(self.h)
 
     def close(self):
-        if self.h:
+        if getattr(self, "h", None):
             plan_destroy(self.h)
             self.h = None
 

@@ -30,7 +30,6 @@ struct ModeState {
   double c_k = 1.0;
   double* kr = nullptr;
   int K = 0, K_pad = 0, rows = 0;      // per-block kernel layout (tile kT)
-  int K_padP = 0, rowsP = 0, TP = 16;  // persistent kernel layout (tile TP, chosen per plan)
 };
 
 }  // namespace
@@ -141,21 +140,6 @@ void set_core_layout(const conv_plan* p, int packing, ModeState* m) {
   core_sizes(p, packing, &mmax, &mtyp);
   m->K = core_taps(p, packing);
   layout_for(m->K, mmax, pc::kT, &m->K_pad, &m->rows);
-  // persistent tile: the T in {16,14,12} whose groups best fill whole consumer warps for a
-  // typical block (ties within 2% go to the larger T: fewer x-loads per FMA)
-  double best = -1.0;
-  for (int T : pc::kTPChoices) {
-    const double groups = (double)mtyp / T;
-    const double util = groups / (32.0 * std::ceil(groups / 32.0));
-    if (util > best + 0.02) {
-      best = util;
-      m->TP = T;
-    }
-  }
-  const int force = p->opts.reserved[1];   // test hook: force the persistent tile
-  if (force == 12 || force == 14 || force == 16) m->TP = force;
-  m->K_padP = (m->K + m->TP - 1) / m->TP * m->TP;
-  m->rowsP = (mmax + m->TP - 1) / m->TP + m->K_padP / m->TP + 1;
 }
 
 // Launch shape of the fused kernel for the packings that may run in this plan.
@@ -204,26 +188,60 @@ bool launch_shape(const conv_plan* p, const int* packs, int npacks, Shape* sh) {
   return true;
 }
 
-// Persistent warp-specialized kernel: producer warps (4 for short kernels, else 2) and one
-// consumer thread per T-group of a typical block; two packed stages in shared memory.
-struct PShape {
-  int threads, np_warps, nc_warps, gmax;
+// Tiled persistent kernel (pc_tiled.cu): choose the tile T and consumer warps so that
+// typical blocks' groups fill whole warps and tiles; taps resident when <= 4096, else
+// chunks of ~1024 taps (a multiple of T).
+struct TShape {
+  int T, threads, np_warps, G, KC, nchunks, taps_resident, rows_s, K_pad;
+  long long tiles0, tiles1;
   size_t smem;
 };
-bool persist_shape(const conv_plan* p, int packing, PShape* sh) {
-  const ModeState& m = p->ms[packing];
+bool tiled_shape(const conv_plan* p, int packing, TShape* sh) {
   int mmax, mtyp;
   core_sizes(p, packing, &mmax, &mtyp);
-  const int T = m.TP;
-  sh->gmax = (mmax + T - 1) / T;
-  const int gtyp = (mtyp + T - 1) / T;
-  sh->np_warps = m.K < 256 ? 2 : 1;
-  int nc = (gtyp + 31) / 32;
-  if (nc < 2) nc = 2;
-  if (nc > pc::kMaxThreadsP / 32 - sh->np_warps) nc = pc::kMaxThreadsP / 32 - sh->np_warps;
-  sh->nc_warps = nc;
-  sh->threads = 32 * (sh->np_warps + nc);
-  sh->smem = pc::kSmemHeader + (size_t)m.K_padP * 8 + 2 * (size_t)(T + 1) * m.rowsP * 8 + 4 * (size_t)sh->gmax * 8;
+  const int K = core_taps(p, packing);
+  const int force = p->opts.reserved[1];
+  double best = -1.0;
+  for (int T : pc::kTPChoices) {
+    if ((force == 12 || force == 14 || force == 16) && T != force) continue;
+    const double speed = T == 16 ? 1.0 : (T == 14 ? 0.96 : 0.92);   // core-loop calibration (profiles)
+    for (int ncw = 4; ncw >= 2; --ncw) {
+      const int G = 32 * ncw;
+      const long long groups = (mtyp + T - 1) / T;
+      const long long tiles = (groups + G - 1) / G;
+      const double util = (double)groups / (double)(tiles * G);
+      const double score = util * speed * (ncw == 4 ? 1.0 : 0.97);
+      if (score > best + 1e-9) {
+        best = score;
+        sh->T = T;
+        sh->G = G;
+      }
+    }
+  }
+  const int T = sh->T;
+  sh->K_pad = (K + T - 1) / T * T;
+  sh->np_warps = K < 256 ? 2 : 1;
+  sh->threads = sh->G + 32 * sh->np_warps;
+  const int KCmax = 4096;
+  if (sh->K_pad <= KCmax) {
+    sh->taps_resident = 1;
+    sh->nchunks = 1;
+    sh->KC = sh->K_pad;
+  } else {
+    sh->taps_resident = 0;
+    const int nch = (sh->K_pad + 1023) / 1024;
+    sh->KC = ((sh->K_pad + nch - 1) / nch + T - 1) / T * T;
+    sh->nchunks = (sh->K_pad + sh->KC - 1) / sh->KC;
+  }
+  const int front = packing == PC_PACK_SYM ? 1 : 0;
+  sh->rows_s = front + sh->G + sh->KC / T + 1;
+  const long long g0 = (mmax + T - 1) / T;         // block 0 has the most groups
+  const long long g1 = (mtyp + T - 1) / T;
+  sh->tiles0 = (g0 + sh->G - 1) / sh->G;
+  sh->tiles1 = (g1 + sh->G - 1) / sh->G;
+  const size_t stage = (size_t)(((T + 1) * sh->rows_s + 1) & ~1) * 8 + (sh->taps_resident ? 0 : (size_t)sh->KC * 8);
+  sh->smem = pc::kSmemHeader + (sh->taps_resident ? (size_t)sh->K_pad * 8 : 0) + 2 * stage +
+             (packing == PC_PACK_SYM ? 2 * (2 * (size_t)sh->G + 2) * 8 : 0);
   return sh->smem <= kMaxSmem;
 }
 
@@ -262,7 +280,7 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
   int packs[4];
   const int np = plan_packs(p, packs);
   Shape sh;
-  if (!launch_shape(p, packs, np, &sh)) return PC_E_CONFIG;
+  const bool per_block_ok = launch_shape(p, packs, np, &sh);
   Exec e;
   std::memset(&e, 0, sizeof(e));
   if (dbg) e = *dbg;
@@ -274,31 +292,38 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
   e.r_stride = r_stride;
   e.b0 = b0;
   e.nblk = nblk;
-  e.stage_raw = sh.stage_raw;
-  e.reg_path = sh.reg_path;
+  e.stage_raw = per_block_ok ? sh.stage_raw : 0;
+  e.reg_path = per_block_ok ? sh.reg_path : 0;
   for (int i = 0; i < np; ++i) fill_modep(p->ms[packs[i]], &e.mp[packs[i]]);
   e.dec_pack = p->packing == PC_PACK_ADAPTIVE ? p->d_dec_pack : nullptr;
   e.nsig = n_sig;
   const int launch_pack = p->packing == PC_PACK_ADAPTIVE ? -1 : p->packing;
-  PShape ps;
-  if (!dbg && p->packing != PC_PACK_ADAPTIVE && p->opts.exec == PC_EXEC_FUSED && persist_shape(p, p->packing, &ps)) {
+  TShape ts;
+  if (!dbg && p->packing != PC_PACK_ADAPTIVE && p->opts.exec == PC_EXEC_FUSED && tiled_shape(p, p->packing, &ts)) {
     e.counter = p->d_counter;
     e.base = p->counter_base;
     e.dbg_timing = timing;
     e.max_ctas_per_sm = p->opts.reserved[2];
-    e.np_warps = ps.np_warps;
-    e.nc_warps = ps.nc_warps;
-    e.gmax = ps.gmax;
-    e.mp[p->packing].K_pad = p->ms[p->packing].K_padP;
-    e.mp[p->packing].rows = p->ms[p->packing].rowsP;
+    e.np_warps = ts.np_warps;
+    e.nc_warps = ts.G / 32;
+    e.G = ts.G;
+    e.KC = ts.KC;
+    e.nchunks = ts.nchunks;
+    e.taps_resident = ts.taps_resident;
+    e.rows_s = ts.rows_s;
+    e.tiles0 = ts.tiles0;
+    e.tiles1 = ts.tiles1;
+    e.jobs_per_sig = (b0 == 0) ? ts.tiles0 + (nblk - 1) * ts.tiles1 : nblk * ts.tiles1;
+    e.mp[p->packing].K_pad = ts.K_pad;
+    const long long njobs = e.jobs_per_sig * n_sig;
     int grid = 0;
-    cudaError_t err = pc::launch_persist(p->packing, p->ms[p->packing].TP, make_geo(p), e, nblk * n_sig, ps.threads,
-                                         ps.smem, st, &grid);
+    cudaError_t err = pc::launch_tiled(p->packing, ts.T, make_geo(p), e, njobs, ts.threads, ts.smem, st, &grid);
     if (err != cudaSuccess) return PC_E_CUDA;
-    p->counter_base += (unsigned long long)(nblk * n_sig) + (unsigned long long)grid;
+    p->counter_base += (unsigned long long)njobs + (unsigned long long)grid;
     if (grid_out) *grid_out = grid;
     return PC_OK;
   }
+  if (!per_block_ok) return PC_E_CONFIG;   // debug dumps / adaptive need the per-block kernel
   return cuda_status(pc::launch_fused(launch_pack, make_geo(p), e, nblk * n_sig, sh.threads, sh.smem, st));
 }
 
@@ -380,12 +405,15 @@ int conv_plan_create(conv_plan** out, int64_t L, int32_t N, int32_t W_block, int
     conv_plan_destroy(p);
     return PC_E_CUDA;
   }
-  // shared-memory feasibility of the fused kernel for every packing the plan may use
+  // shared-memory feasibility: the tiled kernel (production) or, for adaptive plans, the
+  // per-block kernel (which also serves conv_execute_debug when it fits)
   int packs[4];
   const int np = plan_packs(p, packs);
   for (int i = 0; i < np; ++i) set_core_layout(p, packs[i], &p->ms[packs[i]]);
   Shape sh;
-  if (!launch_shape(p, packs, np, &sh)) {
+  TShape ts;
+  const bool ok = (packing == PC_PACK_ADAPTIVE) ? launch_shape(p, packs, np, &sh) : tiled_shape(p, packing, &ts);
+  if (!ok) {
     conv_plan_destroy(p);
     return PC_E_CONFIG;
   }
@@ -460,7 +488,7 @@ int init_mode(conv_plan* p, int packing, int Q, int K_q, const double* k_dev, cu
     m.bound_ok = R <= m.bound;
     if (!m.bound_ok && p->opts.bound_policy == PC_BOUND_STRICT) return PC_E_BOUND;
   }
-  const int kr_len = m.K_padP > m.K_pad ? m.K_padP : m.K_pad;   // zero taps past K serve both tiles
+  const int kr_len = m.K + 32;   // zero taps past K serve every tile padding (8..16)
   if (!m.kr && cudaMalloc(&m.kr, sizeof(double) * kr_len) != cudaSuccess) return PC_E_CUDA;
   e = pc::launch_build_taps(p->d_k_pad, p->d_k_int, p->Np, packing, m.eps_inv, m.K, kr_len, m.kr, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
@@ -787,7 +815,8 @@ int conv_plan_query(const conv_plan* p, conv_plan_info* info) {
   info->rbar_stride = mm;
   info->rint_stride = p->W + p->Np - 1;
   for (int i = 0; i < 4; ++i) info->q_mode[i] = p->qmode[i];
-  info->core_tile = m.TP;
+  TShape ts;
+  info->core_tile = (p->packing != PC_PACK_ADAPTIVE && tiled_shape(p, pk, &ts)) ? ts.T : 0;
   return PC_OK;
 }
 

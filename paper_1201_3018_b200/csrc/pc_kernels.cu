@@ -304,359 +304,6 @@ __global__ void __launch_bounds__(kMaxThreads, 1) pc_fused_kernel(Geo g, Exec e)
   }
 }
 
-// ------------------------------------------------------------------ persistent, warp-specialized
-// pc_persist_kernel: the production form of the fused path.  Each CTA is persistent (grid =
-// SMs x resident CTAs) and pulls overlap-save blocks from a job counter.  Warp roles:
-//   producer warps  a2-a4: block peak (coalesced loads + shuffles), companding, packing of
-//                   block n+1 into shared-memory stage (n+1)&1 -- overlapped with the core
-//   consumer warps  a5-a7: the FP64 core on stage n&1 (one T-output group per thread),
-//                   then unpacking, inverse companding and placement straight from the
-//                   accumulator registers (no shared-memory round trip)
-// Stages are handed over with mbarriers (full: producers -> consumers, empty: back).  The
-// core taps are TMA bulk-copied once per CTA.  Symmetric packing needs B[m-1] of the
-// previous group for its first even output; those pairs are fixed up after a consumer-only
-// named barrier.
-namespace {
-struct PSmem {
-  uint64_t bar_taps, full[2], empty[2];
-  long long job[2];
-  double cs[2];
-  long long prod_job;
-  double red[32];
-};
-}
-
-template <int PACK, int T>
-__device__ __forceinline__ double produce_block(const Geo& g, const Exec& e, const ModeP& mp, long long job,
-                                              double* xs, PSmem* ps, int ptid, int nprod, int bar_id,
-                                              unsigned long long* t_peak = nullptr) {
-  const long long sig = job / e.nblk;
-  const long long w = e.b0 + job % e.nblk;
-  const Blk b = block_info<PACK>(g, mp.K, w);
-  const double* __restrict__ s = e.s + sig * e.s_stride;
-  const long long avail = g.L - b.g0;
-  const int n_valid = (int)(avail < 0 ? 0 : (avail > g.W_block ? g.W_block : avail));
-  const double* gsrc = s + (b.g0 - e.s_off);
-  double c_s = 1.0;
-  if (PACK != PACK_FULL) {
-    // block peak: 8 independent loads in flight per thread, then warp shuffles
-    constexpr int U = 16;
-    double m[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) m[u] = 0.0;
-    if ((reinterpret_cast<uintptr_t>(gsrc) & 15u) == 0) {
-      const double2* g2 = reinterpret_cast<const double2*>(gsrc);
-      const int n2 = n_valid / 2;
-      for (int i0 = ptid; i0 < n2; i0 += U * nprod) {
-        double2 v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int i = i0 + u * nprod;
-          v[u] = (i < n2) ? __ldg(g2 + i) : make_double2(0.0, 0.0);
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) m[u] = fmax(m[u], fmax(fabs(v[u].x), fabs(v[u].y)));
-      }
-      if ((n_valid & 1) && ptid == 0) m[0] = fmax(m[0], fabs(gsrc[n_valid - 1]));
-    } else {
-      for (int i0 = ptid; i0 < n_valid; i0 += U * nprod) {
-        double v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int i = i0 + u * nprod;
-          v[u] = (i < n_valid) ? __ldg(gsrc + i) : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) m[u] = fmax(m[u], fabs(v[u]));
-      }
-    }
-#pragma unroll
-    for (int u = 1; u < U; ++u) m[0] = fmax(m[0], m[u]);
-    for (int o = 16; o > 0; o >>= 1) m[0] = fmax(m[0], __shfl_xor_sync(0xffffffffu, m[0], o));
-    if ((ptid & 31) == 0) ps->red[ptid >> 5] = m[0];
-    named_bar(bar_id, nprod);
-    double peak = 0.0;
-    for (int wi = 0; wi < nprod / 32; ++wi) peak = fmax(peak, ps->red[wi]);
-    c_s = (peak == 0.0) ? 1.0 : mp.Q / peak;         // Eq. (2)
-    named_bar(bar_id, nprod);                        // red[] reusable
-    if (t_peak) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(*t_peak));
-  }
-  auto sample = [&](int i) -> double { return (i < 0 || i >= n_valid) ? 0.0 : __ldg(gsrc + i); };
-  // packing, word-major: lane-consecutive words read lane-consecutive samples (coalesced;
-  // the block was just read by the peak pass, so these hit L2) and land in the padded
-  // row-major stage at (i / T) * (T + 1) + i % T (conflict-free).  U words per thread in
-  // flight.  Words past xlen only feed discarded outputs; they are zeroed.
-  constexpr int U = (PACK == PACK_ASYM3) ? 4 : 8;
-  const int words = mp.rows * T;
-  const int base = b.o0 - (g.Np - 1);                 // asym/full: local sample of word 0, segment 0
-  for (int i0 = ptid; i0 < words; i0 += U * nprod) {
-    double v[U];
-    if (PACK == PACK_SYM) {
-      double2 x[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int i = i0 + u * nprod;
-        const int j = i - b.pre;                       // s_bar[j] uses samples 2j, 2j+1 (Eq. (4))
-        x[u] = make_double2(0.0, 0.0);
-        if (i < b.xlen && j >= 0) {
-          if (2 * j + 1 < n_valid) x[u] = __ldg(reinterpret_cast<const double2*>(gsrc) + j);
-          else if (2 * j < n_valid) x[u].x = __ldg(gsrc + 2 * j);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int i = i0 + u * nprod;
-        v[u] = (i < b.xlen && i >= b.pre) ? pack_sym(compand1(c_s, x[u].x), compand1(c_s, x[u].y), mp.eps) : 0.0;
-      }
-    } else if (PACK == PACK_ASYM2 || PACK == PACK_ASYM3) {
-      constexpr int M = (PACK == PACK_ASYM2) ? 2 : 3;
-      double x[M][U];
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-#pragma unroll
-        for (int q = 0; q < M; ++q) {
-          const int i = i0 + u * nprod;
-          x[q][u] = (i < b.xlen) ? sample(base + q * b.S + i) : 0.0;   // Eq. (7) under C8
-        }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        double a = compand1(c_s, x[M - 1][u]);         // Horner, oracle order
-#pragma unroll
-        for (int q = M - 2; q >= 0; --q) a = __dadd_rn(compand1(c_s, x[q][u]), __dmul_rn(mp.eps, a));
-        v[u] = (i0 + u * nprod < b.xlen) ? a : 0.0;
-      }
-    } else {
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int i = i0 + u * nprod;
-        v[u] = (i < b.xlen) ? sample(base + i) : 0.0;
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int i = i0 + u * nprod;
-      if (i < words) xs[(i / T) * (T + 1) + i % T] = v[u];
-    }
-  }
-  return c_s;
-}
-
-template <int PACK, int T>
-__global__ void __maxnreg__(96) pc_persist_kernel(Geo g, Exec e) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  PSmem* ps = reinterpret_cast<PSmem*>(smem);
-  const ModeP& mp = e.mp[PACK];
-  double* kr = reinterpret_cast<double*>(smem + kSmemHeader);
-  double* xsb = kr + mp.K_pad;
-  const int xs_words = (T + 1) * mp.rows;              // padded row-major stage
-  const int gmax = e.gmax;
-  double* cbase = xsb + 2 * xs_words;                  // [stage][C_first | B_last][gmax]
-  const int tid = threadIdx.x;
-  const int nprod = e.np_warps * 32;
-  const int ncons = blockDim.x - nprod;
-  const long long njobs = e.nblk * e.nsig;
-
-  unsigned long long t_start = 0, t_fill = 0, t_peak0 = 0;
-  if (tid == 0) {
-    mbar_init(&ps->bar_taps, 1);
-    mbar_init(&ps->full[0], nprod);
-    mbar_init(&ps->full[1], nprod);
-    mbar_init(&ps->empty[0], ncons);
-    mbar_init(&ps->empty[1], ncons);
-    mbar_arrive_expect_tx(&ps->bar_taps, (uint32_t)mp.K_pad * 8u);
-    bulk_g2s(kr, mp.kr, (uint32_t)mp.K_pad * 8u, &ps->bar_taps);
-  }
-  // Programmatic dependent launch: the prologue above (barrier init, tap TMA: plan-owned,
-  // read-only) overlaps the previous kernel's tail; nothing touches the input, the output
-  // or the job counter before the previous grid has completed.
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  __syncthreads();
-  if (e.dbg_timing) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
-
-  // Pipeline fill: every warp helps produce the first block into stage 0, then roles split.
-  if (tid == 0) ps->prod_job = (long long)(atomicAdd(e.counter, 1ULL) - e.base);
-  __syncthreads();
-  const long long job0 = ps->prod_job;
-  if (job0 < njobs) {
-    const double c0 = produce_block<PACK, T>(g, e, mp, job0, xsb, ps, tid, blockDim.x, 0,
-                                             e.dbg_timing ? &t_peak0 : nullptr);
-    if (tid == 0) {
-      ps->job[0] = job0;
-      ps->cs[0] = c0;
-    }
-  } else if (tid == 0) {
-    ps->job[0] = -1;
-  }
-  __syncthreads();
-  if (e.dbg_timing) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_fill));
-  if (tid < nprod) mbar_arrive(&ps->full[0]);
-  if (job0 >= njobs) return;
-
-  if (tid < nprod) {
-    // ======================= producer warps =======================
-    const int ptid = tid;
-    for (int it = 1;; ++it) {
-      const int stage = it & 1;
-      const uint32_t ph = (it >> 1) & 1;
-      mbar_wait(&ps->empty[stage], ph ^ 1);            // consumers released this stage
-      named_bar(2, nprod);                             // previous job slot fully read
-      if (ptid == 0) ps->prod_job = (long long)(atomicAdd(e.counter, 1ULL) - e.base);
-      named_bar(2, nprod);
-      const long long job = ps->prod_job;
-      if (job >= njobs) {
-        if (ptid == 0) ps->job[stage] = -1;
-        mbar_arrive(&ps->full[stage]);
-        break;
-      }
-      const double c_s = produce_block<PACK, T>(g, e, mp, job, xsb + stage * xs_words, ps, ptid, nprod, 2);
-      if (ptid == 0) {
-        ps->job[stage] = job;
-        ps->cs[stage] = c_s;
-      }
-      mbar_arrive(&ps->full[stage]);                   // release: packed words, job, c_s
-    }
-    return;
-  }
-
-  // ======================= consumer warps =======================
-  const int ctid = tid - nprod;
-  unsigned long long* trace = (e.dbg_timing && ctid == 0) ? e.dbg_timing + 8ull * 148 * 32 + 16ull * blockIdx.x : nullptr;
-  int ntr = 0;
-  auto stamp = [&]() {
-    if (trace && ntr < 16) {
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      trace[ntr++] = t;
-    }
-  };
-  stamp();
-  mbar_wait(&ps->bar_taps, 0);
-  stamp();
-  int it = 0;
-  long long c_wait = 0, c_conv = 0, c_dec = 0, c_fix = 0;   // profiling (dbg_timing only)
-  for (;; ++it) {
-    const int stage = it & 1;
-    const uint32_t ph = (it >> 1) & 1;
-    long long c0 = e.dbg_timing ? clock64() : 0;
-    mbar_wait(&ps->full[stage], ph);
-    if (e.dbg_timing) c_wait += clock64() - c0;
-    stamp();
-    const long long job = ps->job[stage];
-    if (job < 0) break;
-    const double c_s = ps->cs[stage];
-    const long long sig = job / e.nblk;
-    const long long w = e.b0 + job % e.nblk;
-    const Blk b = block_info<PACK>(g, mp.K, w);
-    const double* xs = xsb + stage * xs_words;
-    double* __restrict__ r = e.r + sig * e.r_stride;
-    const double inv = dequant_scale(c_s, mp.c_k);   // Eq. (16)
-    const long long gbase = b.g0 + b.o0;
-    auto store = [&](int k, double val) {
-#ifdef PC_DIAG_NO_STORE
-      if (val != 1.2345e300) return;   // diagnostics build: measure without output stores
-#endif
-      const long long gi = gbase + k;
-      if (g.mode == 0) {
-        if (gi < g.L + g.N - 1) r[gi - e.r_off] = val;
-      } else {
-        const long long j = gi - (g.N - 1);              // valid lag (C17)
-        if (j >= 0 && j <= g.L - g.N) r[j - e.r_off] = val;
-      }
-    };
-    double* cfirst = cbase + stage * 2 * gmax;
-    double* blast = cfirst + gmax;
-    const int ngroups = (b.M_out + T - 1) / T;
-    const int moff = (w == 0) ? 0 : 1;
-    for (int gi = ctid; gi < ngroups; gi += ncons) {
-      double acc[T];
-      long long c1 = e.dbg_timing ? clock64() : 0;
-      conv_group_padded<T>(smem_u32(xs) + 8u * (T + 1) * gi, smem_u32(kr), mp.K_pad, acc);   // a5
-      if (e.dbg_timing) {
-        // consume acc before reading the clock so the core is not scheduled past it
-        double chk = 0.0;
-#pragma unroll
-        for (int i = 0; i < T; ++i) chk += acc[i];
-        if (chk == 1.2345e300) r[0] = chk;
-        const long long c2 = clock64();
-        c_conv += c2 - c1;
-        c1 = c2;
-      }
-      if (PACK == PACK_SYM) {                                      // a6/a7, Eqs. (12)-(17)
-        double Bprev = 0.0;
-#pragma unroll
-        for (int i = 0; i < T; ++i) {
-          const int m = gi * T + i;
-          const Digits3 d = decode_sym(acc[i], mp.eps, mp.eps_inv, mp.pow2);
-          if (m < b.M_out && m >= moff) {
-            const int k = 2 * (m - moff);
-            store(k + 1, __dmul_rn(d.A, inv));
-            if (i > 0 || m == 0) {
-              const double ev = d.C + Bprev;
-              store(k, __dmul_rn(ev, inv));
-            } else {
-              cfirst[gi] = d.C;                                    // needs B of group gi-1
-            }
-          }
-          Bprev = d.B;
-        }
-        blast[gi] = Bprev;
-      } else if (PACK == PACK_ASYM2 || PACK == PACK_ASYM3) {
-        constexpr int M = (PACK == PACK_ASYM2) ? 2 : 3;
-#pragma unroll
-        for (int i = 0; i < T; ++i) {
-          const int m = gi * T + i;
-          if (m < b.S) {
-            double v = acc[i];
-#pragma unroll
-            for (int q = 0; q < M; ++q) {                          // balanced digits (C9)
-              const double t = rint_fast(v);
-              if (q < M - 1) v = __dmul_rn(__dsub_rn(v, t), mp.eps_inv);
-              const int k = q * b.S + m;
-              if (k < b.n_out) store(k, __dmul_rn(t, inv));
-            }
-          }
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < T; ++i) {
-          const int m = gi * T + i;
-          if (m < b.n_out) store(m, acc[i]);
-        }
-      }
-      if (e.dbg_timing) c_dec += clock64() - c1;
-    }
-    mbar_arrive(&ps->empty[stage]);                                // done reading xs[stage]
-    stamp();
-    long long c3 = e.dbg_timing ? clock64() : 0;
-    if (PACK == PACK_SYM) {
-      named_bar(1, ncons);
-      for (int gi = ctid + (ctid == 0 ? ncons : 0); gi < ngroups; gi += ncons) {
-        const int m = gi * T;                                      // gi >= 1
-        if (m < b.M_out && m >= moff) store(2 * (m - moff), __dmul_rn(cfirst[gi] + blast[gi - 1], inv));
-      }
-    }
-    if (e.dbg_timing) c_fix += clock64() - c3;
-  }
-  if (e.dbg_timing && ctid == 0) {
-    unsigned long long t_end, smid;
-    unsigned int sm32;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm32));
-    smid = sm32;
-    unsigned long long* o = e.dbg_timing + 4ull * blockIdx.x;
-    o[0] = smid;
-    o[1] = t_start;
-    o[2] = t_end;
-    o[3] = (unsigned long long)it;
-    unsigned long long* q = e.dbg_timing + 4ull * 148 * 32 + 4ull * blockIdx.x;
-    q[0] = c_wait;
-    q[1] = c_conv;
-    q[2] = t_peak0 - t_start;
-    q[3] = t_fill - t_start;
-  }
-}
-
 // ------------------------------------------------------------------ a8: block statistics
 // Per block: peak p and sigma from the second moment on the fixed grid z = [[x 2^20/p]]
 // with an exact int64 sum (reading C12).
@@ -783,75 +430,6 @@ cudaError_t launch_fused(int packing, const Geo& g, const Exec& e, long long n_j
     case PACK_ASYM2: return launch_fused_t<PACK_ASYM2>(g, e, n_jobs, threads, smem, st);
     case PACK_ASYM3: return launch_fused_t<PACK_ASYM3>(g, e, n_jobs, threads, smem, st);
     case -1: return launch_fused_t<-1>(g, e, n_jobs, threads, smem, st);
-  }
-  return cudaErrorInvalidValue;
-}
-
-// Host-side launch cost matters (a cfg2 step is ~100 us): the smem opt-in and the
-// occupancy query run once per (kernel, smem, threads) and are cached.
-template <int PACK, int T>
-static cudaError_t launch_persist_t(const Geo& g, const Exec& e, long long n_jobs, int threads, size_t smem,
-                                    cudaStream_t st, int* grid_out) {
-  auto kfn = pc_persist_kernel<PACK, T>;
-  static size_t c_smem = 0;
-  static int c_threads = 0, c_grid = 0, c_dev = -1;
-  int dev = 0;
-  cudaError_t err = cudaGetDevice(&dev);
-  if (err != cudaSuccess) return err;
-  if (smem != c_smem || threads != c_threads || dev != c_dev) {
-    err = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (err != cudaSuccess) return err;
-    int occ = 0, sms = 0;
-    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, threads, smem);
-    if (err != cudaSuccess) return err;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (occ < 1) return cudaErrorInvalidConfiguration;
-    c_smem = smem;
-    c_threads = threads;
-    c_dev = dev;
-    c_grid = sms * occ;
-  }
-  long long grid = c_grid;
-  if (e.max_ctas_per_sm > 0) {
-    int sms = 0;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if ((long long)e.max_ctas_per_sm * sms < grid) grid = (long long)e.max_ctas_per_sm * sms;
-  }
-  if (grid > n_jobs) grid = n_jobs;
-  *grid_out = (int)grid;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3((unsigned)threads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kfn, g, e);
-}
-
-template <int T>
-static cudaError_t launch_persist_T(int packing, const Geo& g, const Exec& e, long long n_jobs, int threads,
-                                    size_t smem, cudaStream_t st, int* grid_out) {
-  switch (packing) {
-    case PACK_FULL: return launch_persist_t<PACK_FULL, T>(g, e, n_jobs, threads, smem, st, grid_out);
-    case PACK_SYM: return launch_persist_t<PACK_SYM, T>(g, e, n_jobs, threads, smem, st, grid_out);
-    case PACK_ASYM2: return launch_persist_t<PACK_ASYM2, T>(g, e, n_jobs, threads, smem, st, grid_out);
-    case PACK_ASYM3: return launch_persist_t<PACK_ASYM3, T>(g, e, n_jobs, threads, smem, st, grid_out);
-  }
-  return cudaErrorInvalidValue;
-}
-
-cudaError_t launch_persist(int packing, int T, const Geo& g, const Exec& e, long long n_jobs, int threads,
-                           size_t smem, cudaStream_t st, int* grid_out) {
-  *grid_out = 0;
-  if (n_jobs <= 0) return cudaSuccess;
-  switch (T) {
-    case 12: return launch_persist_T<12>(packing, g, e, n_jobs, threads, smem, st, grid_out);
-    case 14: return launch_persist_T<14>(packing, g, e, n_jobs, threads, smem, st, grid_out);
-    case 16: return launch_persist_T<16>(packing, g, e, n_jobs, threads, smem, st, grid_out);
   }
   return cudaErrorInvalidValue;
 }

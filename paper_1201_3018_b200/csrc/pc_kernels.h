@@ -8,9 +8,7 @@ namespace pc {
 
 constexpr int kT = 8;              // outputs per thread of the per-block kernel's core
 constexpr int kMaxThreads = 1024;  // per-block kernel: threads per CTA; caps regs at 64
-constexpr int kTP = 16;            // largest outputs-per-thread tile of the persistent kernel
-constexpr int kTPChoices[3] = {16, 14, 12};   // tiles instantiated; the plan picks by lane use
-constexpr int kMaxThreadsP = 512;  // persistent kernel: threads per CTA; caps regs at 128
+constexpr int kTPChoices[3] = {16, 14, 12};   // tiled-kernel tiles instantiated; the plan picks
 constexpr int kSmemHeader = 512;   // mbarrier + reduction scratch, keeps the rest 128B-aligned
 
 // Per-packing parameters of one launch (adaptive plans fill several).
@@ -41,6 +39,13 @@ struct Exec {
   int gmax;                     // max T-groups of any block (sym fix-up arrays)
   int max_ctas_per_sm;          // diagnostics: cap on resident CTAs per SM (0 = occupancy)
   long long nsig;               // signals in the launch (jobs = nsig * nblk)
+  // tiled kernel: jobs = (signal, block, tile); tile = G groups of T outputs; taps in chunks
+  int G;                        // consumer threads = groups per tile
+  int KC, nchunks;              // taps per chunk (multiple of T), chunks per job
+  int taps_resident;            // 1: all K_pad taps stay in shared memory (nchunks == 1)
+  int rows_s;                   // rows of a stage's padded word window
+  long long tiles0, tiles1;     // tiles of block 0 / of every other block
+  long long jobs_per_sig;       // jobs of one signal in this launch
   // parity/debug dumps (row = sig * P + w), nullptr in production
   double* dbg_packed;
   long long dbg_packed_stride;
@@ -54,9 +59,9 @@ struct Exec {
 
 cudaError_t launch_fused(int packing, const Geo& g, const Exec& e, long long n_jobs, int threads, size_t smem,
                          cudaStream_t st);
-// Persistent warp-specialized variant: grid = SMs x resident CTAs; returns the grid used.
-cudaError_t launch_persist(int packing, int T, const Geo& g, const Exec& e, long long n_jobs, int threads,
-                           size_t smem, cudaStream_t st, int* grid_out);
+// Tiled persistent warp-specialized kernel (pc_tiled.cu): grid = SMs x resident CTAs.
+cudaError_t launch_tiled(int packing, int T, const Geo& g, const Exec& e, long long n_jobs, int threads, size_t smem,
+                         cudaStream_t st, int* grid_out);
 cudaError_t launch_kernel_prep(const double* k_in, int N, int Np, int reverse, double K_q, double* k_pad,
                                double* k_int, double* scal, cudaStream_t st);
 cudaError_t launch_build_taps(const double* k_pad, const double* k_int, int Np, int packing, double eps_inv, int K,

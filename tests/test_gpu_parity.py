@@ -338,3 +338,37 @@ def test_cfg1_full_size_all_packings():
         g = gpu_run(s, k, 1024, packing, Q)
         check_blocks(g, ref, packing)
         assert np.array_equal(g["r"], ref.out)
+
+
+# --------------------------------------------------------------------- large kernels: tap chunks, tiles
+@pytest.mark.parametrize("packing", [O.FULL, O.SYM, O.ASYM2, O.ASYM3])
+@pytest.mark.parametrize("case", [(70000, 4096, 16384), (40000, 1024, 16384), (100000, 8192, 32768)])
+def test_large_kernels_tap_chunks_and_tiles(packing, case):
+    """cfg3/cfg4-shaped geometries: taps processed in chunks, blocks split into several
+    output tiles (the symmetric tile boundary uses the extra-word path)."""
+    L, N, W_block = case
+    rng = np.random.default_rng(N)
+    s, k = rng.laplace(0, 0.3, L), rng.normal(0, 1 / np.sqrt(N), N)
+    if packing == O.FULL:
+        g = gpu_run(s, k, W_block, O.FULL, 0, debug=False)
+        want = O.full_precision(s, k)
+        assert np.max(np.abs(g["r"] - want)) / np.max(np.abs(want)) < 1e-12
+        return
+    Q = 3 if packing != O.ASYM2 else 127
+    ref = O.conv_pipeline(s, k, W_block, packing, Q, rmax_rule=O.RMAX_L1)
+    assert ref.kernel.bound_ok and ref.mismatches == 0
+    g = gpu_run(s, k, W_block, packing, Q, rmax_rule=O.RMAX_L1, debug=False)
+    assert np.array_equal(g["r"], ref.out)
+
+
+def test_cfg4_shaped_xcorr_large_query():
+    rng = np.random.default_rng(7)
+    L, N = 1 << 17, 8192
+    x = WL.cfg4_signal(3, L)
+    q = x[40000:40000 + N] + rng.normal(0, 0.01, N)
+    for packing, Q in ((O.ASYM2, 127), (O.SYM, 3)):
+        ref = O.conv_pipeline(x, q, 32768, packing, Q, mode=O.XCORR, rmax_rule=O.RMAX_L1)
+        assert ref.kernel.bound_ok and ref.mismatches == 0
+        g = gpu_run(x, q, 32768, packing, Q, mode=O.XCORR, rmax_rule=O.RMAX_L1, debug=False)
+        assert np.array_equal(g["r"], ref.out)
+        assert int(np.argmax(g["r"])) == 40000
