@@ -372,3 +372,65 @@ def test_cfg4_shaped_xcorr_large_query():
         g = gpu_run(x, q, 32768, packing, Q, mode=O.XCORR, rmax_rule=O.RMAX_L1, debug=False)
         assert np.array_equal(g["r"], ref.out)
         assert int(np.argmax(g["r"])) == 40000
+
+
+# --------------------------------------------------------------------- full BASELINE sizes (sampled)
+def test_cfg3_full_size_direct_sampled():
+    """Config 3 at full size (L = 2^24, N = 4096, W_block = 16384) on the direct core: asym2
+    9-bit (L1, dyadic) bit-exact on sampled blocks; full precision within 1e-12 on a window."""
+    s, k = WL.cfg3(seed=0)
+    _sampled_full_size(s, k, 16384, O.ASYM2, 255, O.RMAX_L1, 40.0)
+    g = gpu_run(s, k, 16384, O.FULL, 0, debug=False)
+    lo, hi = 5_000_000, 5_000_000 + 20000
+    want = np.convolve(s[lo - 4095:hi], k)[4095:4095 + (hi - lo)]
+    got = g["r"][lo:hi]
+    assert np.max(np.abs(got - want)) / np.max(np.abs(want)) < 1e-12
+
+
+def test_cfg4_full_size_signals_scores():
+    """Config 4 shape: 2^20-sample database signals, N = 8192 query, W_block = 32768; packed
+    scores/lags bit-exact against the oracle on 3 signals; the query's source signal wins."""
+    n_sig, L, N = 3, 1 << 20, 8192
+    q, i0, off = WL.cfg4_query(seed=0, n_signals=n_sig, L=L, N=N)
+    db = np.stack([WL.cfg4_signal(i, L) for i in range(n_sig)])
+    with pcb.Plan(L, N, 32768, pcb.MODE_XCORR, pcb.PACK_ASYM2, 127, rmax_rule=pcb.RMAX_L1) as p:
+        p.set_kernel(dev(q))
+        sc = torch.empty(n_sig, dtype=torch.float64, device=DEV)
+        lag = torch.empty(n_sig, dtype=torch.int64, device=DEV)
+        p.xcorr_max(dev(db), n_sig, L, sc, lag)
+        torch.cuda.synchronize()
+        sc, lag = sc.cpu().numpy(), lag.cpu().numpy()
+    for i in range(n_sig):
+        c = O.conv_pipeline(db[i], q, 32768, O.ASYM2, 127, mode=O.XCORR, rmax_rule=O.RMAX_L1).out
+        assert (sc[i], lag[i]) == O.xcorr_score(c)
+    assert int(np.argmax(sc)) == i0 and lag[i0] == off
+
+
+def test_cfg5_full_size_adaptive_sampled():
+    """Config 5 at full size (L = 2^26, N = 1024, W_block = 4096), floor 40 dB: every block's
+    decision equals the oracle's; outputs bit-exact (packed) / 1e-12 (full) on sampled blocks."""
+    s, k = WL.cfg5(seed=0)
+    W_block, floor = 4096, 40.0
+    dec_ref, qmode = O.adapt_decisions(s, k, W_block, floor)
+    geom = O.Geometry(len(s), len(k), W_block)
+    with pcb.Plan(len(s), len(k), W_block, pcb.MODE_CONV, pcb.PACK_ADAPTIVE, 0, rmax_rule=pcb.RMAX_L1) as p:
+        p.set_kernel(dev(k))
+        s_d = dev(s)
+        dec = p.adapt_block(s_d, floor)
+        assert [(d[0], d[1]) for d in dec] == [(PK[m], q) for m, q, _ in dec_ref]
+        r = torch.empty(geom.L_out, dtype=torch.float64, device=DEV)
+        p.execute(s_d, r)
+        torch.cuda.synchronize()
+        got = r.cpu().numpy()
+    states = {m: O.prepare_kernel(k, geom, m, qmode[m], None, O.CONV, O.EPS_POW2, O.RMAX_L1) for m in qmode}
+    states[O.FULL] = O.prepare_kernel(k, geom, O.FULL, 0)
+    for w in sorted({0, 1, geom.P // 2, geom.P - 1}):
+        m, Q, _ = dec_ref[w]
+        br = O.process_block(s, w, geom, states[m], Q)
+        o0, n = geom.kept(w)
+        lo = geom.block_start(w) + o0
+        n = min(n, geom.L_out - lo)
+        if m == O.FULL:
+            assert np.max(np.abs(got[lo:lo + n] - br.out[:n])) <= 1e-12 * np.max(np.abs(br.out[:n]))
+        else:
+            assert np.array_equal(got[lo:lo + n], br.out[:n])
