@@ -95,7 +95,7 @@ typedef struct conv_plan_info {
   int64_t rint_stride;      /* per-block stride of the debug integer dump (= W + N' - 1)   */
   int32_t q_mode[4];        /* ADAPTIVE: max Q per packing under its bound          */
   int32_t core_tile;        /* outputs per thread of the persistent core (12, 14 or 16)      */
-  int32_t reserved_i;
+  int32_t fft_n;            /* FFT core: complex points N (real transform length 2N), else 0 */
 } conv_plan_info;
 
 /* Per-block decision of conv_adapt_block. */
@@ -187,6 +187,15 @@ int conv_execute_profile(conv_plan* plan, const double* s_dev, double* r_dev, ui
  * invalid geometry. */
 int conv_shard_range(int64_t L, int32_t N, int32_t W_block, int32_t mode, int32_t rank, int32_t world,
                      conv_shard* out);
+
+/* FFT core (opts.core = PC_CORE_FFT): the packed words are convolved through a
+ * hand-written FP64 FFT, so the packed outputs are approximate and exact integers are
+ * recovered only while the error stays below half an LSB.  The kernels keep the largest
+ * last-digit residual (in LSB) seen since the last reset; this call copies it to
+ * *resid_host (synchronizes `stream`), resets it if `reset`, and returns
+ * PC_W_UNPACK_MARGIN if it exceeded 0.25 LSB (SURVEY §5 unpack-residual monitor).
+ * Direct-core plans are exact: *resid_host = 0, PC_OK. */
+int conv_plan_residual(conv_plan* plan, double* resid_host, int32_t reset, void* stream);
 
 int conv_plan_query(const conv_plan* plan, conv_plan_info* info);
 void conv_plan_destroy(conv_plan* plan);

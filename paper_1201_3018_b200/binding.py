@@ -41,7 +41,7 @@ class conv_plan_info(C.Structure):
                 ("R_max", C.c_int64), ("bound", C.c_int64), ("bound_ok", C.c_int32), ("eps_b", C.c_int32),
                 ("eps", C.c_double), ("eps_inv", C.c_double), ("c_k", C.c_double), ("k_peak", C.c_double),
                 ("packed_stride", C.c_int64), ("rbar_stride", C.c_int64), ("rint_stride", C.c_int64),
-                ("q_mode", C.c_int32 * 4), ("core_tile", C.c_int32), ("reserved_i", C.c_int32)]
+                ("q_mode", C.c_int32 * 4), ("core_tile", C.c_int32), ("fft_n", C.c_int32)]
 
 
 class conv_shard(C.Structure):
@@ -84,6 +84,7 @@ def load():
             "conv_plan_query": (C.c_int, [P, C.POINTER(conv_plan_info)]),
             "conv_execute_profile": (C.c_int, [P, VP, VP, VP, C.POINTER(C.c_int32), VP]),
             "conv_shard_range": (C.c_int, [I64, I32, I32, I32, I32, I32, C.POINTER(conv_shard)]),
+            "conv_plan_residual": (C.c_int, [P, C.POINTER(C.c_double), I32, VP]),
             "conv_plan_destroy": (None, [P]),
             "conv_status_string": (C.c_char_p, [C.c_int]),
         }
@@ -204,6 +205,16 @@ def shard_range(L, N, W_block, mode, rank, world):
     return {name: getattr(sh, name) for name, _ in conv_shard._fields_}
 
 
+def plan_residual(plan, reset=True, stream=None):
+    """FFT core: largest last-digit residual (LSB) since the last reset and the status
+    (PC_OK or PC_W_UNPACK_MARGIN if > 0.25 LSB)."""
+    r = C.c_double()
+    rc = load().conv_plan_residual(plan, C.byref(r), int(bool(reset)), _stream(stream))
+    if rc not in (PC_OK, PC_W_UNPACK_MARGIN):
+        _check(rc, "conv_plan_residual")
+    return r.value, rc
+
+
 def plan_query(plan):
     info = conv_plan_info()
     _check(load().conv_plan_query(plan, C.byref(info)), "conv_plan_query")
@@ -251,6 +262,9 @@ class Plan:
 
     def info(self):
         return plan_query(self.h)
+
+    def residual(self, reset=True, stream=None):
+        return plan_residual(self.h, reset, stream)
 
     def close(self):
         if getattr(self, "h", None):

@@ -64,6 +64,12 @@ struct conv_plan {
   // persistent kernel job counter (monotonic; base tracked on the host)
   unsigned long long* d_counter = nullptr;
   unsigned long long counter_base = 0;
+  // FFT core
+  int fft_N = 0;                       // complex points (real transform length 2N)
+  double2* d_tw = nullptr;             // exp(-2 pi i m / N)
+  double2* d_tw2 = nullptr;            // exp(-2 pi i k / 2N), k <= N
+  double2* d_H = nullptr;              // spectrum of the core taps, k <= N
+  double* d_resid = nullptr;           // max last-digit residual (LSB)
 };
 
 namespace {
@@ -245,6 +251,47 @@ bool tiled_shape(const conv_plan* p, int packing, TShape* sh) {
   return sh->smem <= kMaxSmem;
 }
 
+// FFT core geometry: part sizes and counts for 2N real points.  A block's first part gives
+// 2N - K + 1 outputs; later parts 2N - K (a symmetric part after the first also needs the
+// word before it, for B of its first even output).
+struct FShape {
+  int part0_out, part_out;
+  long long parts0, parts1;
+};
+bool fft_shape(const conv_plan* p, int packing, int N, FShape* f) {
+  int mmax, mtyp;
+  core_sizes(p, packing, &mmax, &mtyp);
+  const int K = core_taps(p, packing);
+  f->part0_out = 2 * N - K + 1;
+  f->part_out = 2 * N - K;
+  if (f->part_out < 1) return false;
+  auto parts = [&](int M) -> long long {
+    return M <= f->part0_out ? 1 : 1 + (M - f->part0_out + f->part_out - 1) / f->part_out;
+  };
+  int m0, m1;
+  {
+    const Geo g = make_geo(p);
+    switch (packing) {
+      case PC_PACK_SYM: m0 = pc::block_info<pc::PACK_SYM>(g, K, 0).M_out; m1 = pc::block_info<pc::PACK_SYM>(g, K, 1).M_out; break;
+      case PC_PACK_ASYM2: m0 = pc::block_info<pc::PACK_ASYM2>(g, K, 0).M_out; m1 = pc::block_info<pc::PACK_ASYM2>(g, K, 1).M_out; break;
+      case PC_PACK_ASYM3: m0 = pc::block_info<pc::PACK_ASYM3>(g, K, 0).M_out; m1 = pc::block_info<pc::PACK_ASYM3>(g, K, 1).M_out; break;
+      default: m0 = pc::block_info<pc::PACK_FULL>(g, K, 0).M_out; m1 = pc::block_info<pc::PACK_FULL>(g, K, 1).M_out; break;
+    }
+  }
+  f->parts0 = parts(m0);
+  f->parts1 = parts(m1);
+  return true;
+}
+// smallest N (complex points, 1024..8192) whose first part holds a typical block
+int choose_fft_N(const conv_plan* p, int packing) {
+  int mmax, mtyp;
+  core_sizes(p, packing, &mmax, &mtyp);
+  const int K = core_taps(p, packing);
+  for (int N = 1024; N <= 8192; N *= 2)
+    if (2 * N - K + 1 >= mtyp) return N;
+  return 2 * 8192 - K >= 1 ? 8192 : 0;
+}
+
 int cuda_status(cudaError_t e) { return e == cudaSuccess ? PC_OK : PC_E_CUDA; }
 
 void fill_modep(const ModeState& m, ModeP* mp) {
@@ -298,6 +345,22 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
   e.dec_pack = p->packing == PC_PACK_ADAPTIVE ? p->d_dec_pack : nullptr;
   e.nsig = n_sig;
   const int launch_pack = p->packing == PC_PACK_ADAPTIVE ? -1 : p->packing;
+  if (p->opts.core == PC_CORE_FFT) {
+    if (dbg) return PC_E_CONFIG;                      // per-step dumps exist for the direct core
+    FShape fs;
+    if (!fft_shape(p, p->packing, p->fft_N, &fs)) return PC_E_CONFIG;
+    pc::FftArgs f;
+    f.tw = p->d_tw;
+    f.tw2 = p->d_tw2;
+    f.H = p->d_H;
+    f.resid = p->d_resid;
+    f.part0_out = fs.part0_out;
+    f.part_out = fs.part_out;
+    f.parts0 = fs.parts0;
+    f.parts1 = fs.parts1;
+    e.jobs_per_sig = (b0 == 0) ? fs.parts0 + (nblk - 1) * fs.parts1 : nblk * fs.parts1;
+    return cuda_status(pc::launch_fft_conv(p->packing, p->fft_N, make_geo(p), e, f, e.jobs_per_sig * n_sig, st));
+  }
   TShape ts;
   if (!dbg && p->packing != PC_PACK_ADAPTIVE && p->opts.exec == PC_EXEC_FUSED && tiled_shape(p, p->packing, &ts)) {
     e.counter = p->d_counter;
@@ -370,7 +433,8 @@ int conv_plan_create(conv_plan** out, int64_t L, int32_t N, int32_t W_block, int
   conv_opts o;
   conv_opts_default(&o);
   if (opts) o = *opts;
-  if (o.core != PC_CORE_DIRECT) return PC_E_CONFIG;   // FFT core: not in this build
+  if (o.core != PC_CORE_DIRECT && o.core != PC_CORE_FFT) return PC_E_CONFIG;
+  if (o.core == PC_CORE_FFT && packing == PC_PACK_ADAPTIVE) return PC_E_CONFIG;
   const int Np = (N % 2) ? N : N + 1;                 // P:45, C13
   const long long W = (long long)W_block - Np - 1;
   if (W < 2 || (W % 2) || W < 2LL * Np) return PC_E_CONFIG;
@@ -412,7 +476,42 @@ int conv_plan_create(conv_plan** out, int64_t L, int32_t N, int32_t W_block, int
   for (int i = 0; i < np; ++i) set_core_layout(p, packs[i], &p->ms[packs[i]]);
   Shape sh;
   TShape ts;
-  const bool ok = (packing == PC_PACK_ADAPTIVE) ? launch_shape(p, packs, np, &sh) : tiled_shape(p, packing, &ts);
+  bool ok;
+  if (o.core == PC_CORE_FFT) {
+    p->fft_N = choose_fft_N(p, packing);
+    FShape fs;
+    ok = p->fft_N > 0 && fft_shape(p, packing, p->fft_N, &fs);
+    if (ok) {
+      // twiddle tables, rounded once from long double (recurrences are too inexact)
+      const int N = p->fft_N;
+      double2* tw = (double2*)std::malloc(sizeof(double2) * N);
+      double2* tw2 = (double2*)std::malloc(sizeof(double2) * (N + 1));
+      const long double two_pi = 6.283185307179586476925286766559005768L;
+      for (int m = 0; m < N; ++m) {
+        const long double a = two_pi * (long double)m / (long double)N;
+        tw[m] = make_double2((double)cosl(a), (double)(-sinl(a)));
+      }
+      for (int k = 0; k <= N; ++k) {
+        const long double a = two_pi * (long double)k / (long double)(2 * N);
+        tw2[k] = make_double2((double)cosl(a), (double)(-sinl(a)));
+      }
+      cudaError_t err = cudaMalloc(&p->d_tw, sizeof(double2) * N);
+      if (err == cudaSuccess) err = cudaMalloc(&p->d_tw2, sizeof(double2) * (N + 1));
+      if (err == cudaSuccess) err = cudaMalloc(&p->d_H, sizeof(double2) * (N + 1));
+      if (err == cudaSuccess) err = cudaMalloc(&p->d_resid, sizeof(double));
+      if (err == cudaSuccess) err = cudaMemcpy(p->d_tw, tw, sizeof(double2) * N, cudaMemcpyHostToDevice);
+      if (err == cudaSuccess) err = cudaMemcpy(p->d_tw2, tw2, sizeof(double2) * (N + 1), cudaMemcpyHostToDevice);
+      if (err == cudaSuccess) err = cudaMemset(p->d_resid, 0, sizeof(double));
+      std::free(tw);
+      std::free(tw2);
+      if (err != cudaSuccess) {
+        conv_plan_destroy(p);
+        return PC_E_CUDA;
+      }
+    }
+  } else {
+    ok = (packing == PC_PACK_ADAPTIVE) ? launch_shape(p, packs, np, &sh) : tiled_shape(p, packing, &ts);
+  }
   if (!ok) {
     conv_plan_destroy(p);
     return PC_E_CONFIG;
@@ -438,6 +537,10 @@ void conv_plan_destroy(conv_plan* p) {
   cudaFree(p->d_out);
   cudaFree(p->d_xc);
   cudaFree(p->d_counter);
+  cudaFree(p->d_tw);
+  cudaFree(p->d_tw2);
+  cudaFree(p->d_H);
+  cudaFree(p->d_resid);
   delete p;
 }
 
@@ -573,6 +676,12 @@ int conv_plan_set_kernel(conv_plan* p, const double* k_dev, void* stream) {
     p->k_peak = hk[1];
   } else {
     if ((rc = init_mode(p, p->packing, p->Q, p->K_q, k_dev, st))) return rc;
+    if (p->opts.core == PC_CORE_FFT) {
+      const ModeState& m = p->ms[p->packing];
+      cudaError_t e = pc::launch_fft_spectrum(p->fft_N, m.kr, m.K, p->d_tw, p->d_tw2, p->d_H, st);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) return PC_E_CUDA;
+    }
   }
   p->kernel_set = 1;
   return PC_OK;
@@ -727,6 +836,19 @@ int conv_adapt_block(conv_plan* p, const double* s, double snr_floor_db, double 
   return PC_OK;
 }
 
+int conv_plan_residual(conv_plan* p, double* resid_host, int32_t reset, void* stream) {
+  if (!p || !resid_host) return PC_E_CONFIG;
+  *resid_host = 0.0;
+  if (!p->d_resid) return PC_OK;                     // direct core: exact, no residual
+  if (cudaSetDevice(p->device) != cudaSuccess) return PC_E_CUDA;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemcpyAsync(resid_host, p->d_resid, sizeof(double), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess && reset) e = cudaMemsetAsync(p->d_resid, 0, sizeof(double), st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return PC_E_CUDA;
+  return *resid_host > 0.25 ? PC_W_UNPACK_MARGIN : PC_OK;
+}
+
 int conv_execute_profile(conv_plan* p, const double* s, double* r, uint64_t* rec, int32_t* grid_out, void* stream) {
   if (!p || !s || !r || !rec || !grid_out) return PC_E_CONFIG;
   if (cudaSetDevice(p->device) != cudaSuccess) return PC_E_CUDA;
@@ -816,7 +938,8 @@ int conv_plan_query(const conv_plan* p, conv_plan_info* info) {
   info->rint_stride = p->W + p->Np - 1;
   for (int i = 0; i < 4; ++i) info->q_mode[i] = p->qmode[i];
   TShape ts;
-  info->core_tile = (p->packing != PC_PACK_ADAPTIVE && tiled_shape(p, pk, &ts)) ? ts.T : 0;
+  info->core_tile = (p->packing != PC_PACK_ADAPTIVE && p->opts.core == PC_CORE_DIRECT && tiled_shape(p, pk, &ts)) ? ts.T : 0;
+  info->fft_n = p->fft_N;
   return PC_OK;
 }
 

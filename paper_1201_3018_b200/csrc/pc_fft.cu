@@ -1,0 +1,454 @@
+// pc_fft.cu -- FFT overlap-save core (SURVEY §8(a) a5 for config 3; "any off-the-shelf
+// core", P:127 frequency-domain FLOP model).  Hand-written FP64 FFT in shared memory; no cuFFT.
+//
+// One CTA per (signal, block, part) job.  The packed core words of the part's window (real,
+// length 2N) are loaded as N complex points z[n] = x[2n] + i x[2n+1]; a radix-16 Stockham FFT
+// (all 16 points of a butterfly in registers, read-all / sync / write-all passes, so no
+// ping-pong buffer: N = 8192 complex fits in 139 KB with one pad element per 16) transforms
+// them; the real-FFT split/merge is fused with the product by the precomputed spectrum H of
+// the core taps (H[k], k = 0..N, of the 2N-point real transform); the inverse transform
+// yields the circular convolution p = x (*) h, whose entries p[m + K - 1] are the core
+// outputs out[m] = sum_j x[m + j] kr[j] (kr = reversed taps).  The outputs are approximate;
+// rounding to digits (unpacking) makes them exact integers as long as the FFT error stays
+// below half an LSB -- monitored: the largest last-digit residual is kept per plan.
+//
+// Twiddles come from tables rounded once from long-double values on the host (recurrences
+// break exactness at cfg3 sizes).
+#include "pc_device.cuh"
+#include "pc_kernels.h"
+
+namespace pc {
+
+namespace {
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+// multiply by -i (forward) or +i (inverse): sign = -1 forward
+__device__ __forceinline__ double2 mul_i(double2 a, int sign) {
+  return sign < 0 ? make_double2(a.y, -a.x) : make_double2(-a.y, a.x);
+}
+
+// padded shared-memory index: one pad element every 16 (bank-conflict-free strided writes)
+__device__ __forceinline__ int pidx(int e) { return e + (e >> 4); }
+
+template <int SIGN>
+__device__ __forceinline__ void dft4(double2& a0, double2& a1, double2& a2, double2& a3) {
+  const double2 s02 = cadd(a0, a2), d02 = csub(a0, a2);
+  const double2 s13 = cadd(a1, a3), d13 = mul_i(csub(a1, a3), SIGN);
+  a0 = cadd(s02, s13);
+  a2 = csub(s02, s13);
+  a1 = cadd(d02, d13);
+  a3 = csub(d02, d13);
+}
+
+// exp(SIGN * 2 pi i m / 16), m = 0..9, correctly rounded constants
+template <int SIGN>
+__device__ __forceinline__ double2 w16(int m) {
+  const double c1 = 0.92387953251128673848, s1 = 0.38268343236508978178;   // cos/sin(pi/8)
+  const double r2 = 0.70710678118654752440;                                // cos/sin(pi/4)
+  double c, s;
+  switch (m) {
+    case 0: c = 1.0; s = 0.0; break;
+    case 1: c = c1; s = s1; break;
+    case 2: c = r2; s = r2; break;
+    case 3: c = s1; s = c1; break;
+    case 4: c = 0.0; s = 1.0; break;
+    case 5: c = -s1; s = c1; break;
+    case 6: c = -r2; s = r2; break;
+    case 7: c = -c1; s = s1; break;
+    case 8: c = -1.0; s = 0.0; break;
+    default: c = -c1; s = -s1; break;   // 9
+  }
+  return make_double2(c, SIGN * s);
+}
+
+// In-register DFT of 16 points (radix 4 x 4): v[q] <- sum_p v[p] exp(SIGN 2 pi i p q / 16)
+template <int SIGN>
+__device__ __forceinline__ void dft16(double2 (&v)[16]) {
+#pragma unroll
+  for (int p2 = 0; p2 < 4; ++p2) dft4<SIGN>(v[p2], v[4 + p2], v[8 + p2], v[12 + p2]);
+  // v[4*q1 + p2] now holds a[p2][q1]; twiddle by W16^(p2 q1)
+#pragma unroll
+  for (int p2 = 1; p2 < 4; ++p2)
+#pragma unroll
+    for (int q1 = 1; q1 < 4; ++q1) v[4 * q1 + p2] = cmul(v[4 * q1 + p2], w16<SIGN>(p2 * q1));
+#pragma unroll
+  for (int q1 = 0; q1 < 4; ++q1) dft4<SIGN>(v[4 * q1 + 0], v[4 * q1 + 1], v[4 * q1 + 2], v[4 * q1 + 3]);
+  // v[4*q1 + q2] holds X[q1 + 4 q2]; reorder to natural
+  double2 t[16];
+#pragma unroll
+  for (int q1 = 0; q1 < 4; ++q1)
+#pragma unroll
+    for (int q2 = 0; q2 < 4; ++q2) t[q1 + 4 * q2] = v[4 * q1 + q2];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = t[i];
+}
+
+template <int SIGN, int R>
+__device__ __forceinline__ void dft_small(double2* v) {
+  if (R == 2) {
+    const double2 a = v[0], b = v[1];
+    v[0] = cadd(a, b);
+    v[1] = csub(a, b);
+  } else if (R == 4) {
+    dft4<SIGN>(v[0], v[1], v[2], v[3]);
+  } else {   // R == 8: radix 2 x 4
+    // a[p2][q1] = DFT4 over p1 of v[2 p1 + p2]
+    double2 e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6];
+    double2 o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
+    dft4<SIGN>(e0, e1, e2, e3);
+    dft4<SIGN>(o0, o1, o2, o3);
+    const double r2 = 0.70710678118654752440;
+    o1 = cmul(o1, make_double2(r2, SIGN * r2));
+    o2 = mul_i(o2, SIGN);
+    o3 = cmul(o3, make_double2(-r2, SIGN * r2));
+    v[0] = cadd(e0, o0);
+    v[4] = csub(e0, o0);
+    v[1] = cadd(e1, o1);
+    v[5] = csub(e1, o1);
+    v[2] = cadd(e2, o2);
+    v[6] = csub(e2, o2);
+    v[3] = cadd(e3, o3);
+    v[7] = csub(e3, o3);
+  }
+}
+
+}  // namespace
+
+__host__ __device__ constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n / 2); }
+
+// One radix-16 Stockham pass (sub-transform length LS before the pass).
+template <int N, int SIGN, int LS>
+__device__ __forceinline__ void stockham16(double2* s, const double2* __restrict__ tw) {
+  constexpr int NB = N / 16;
+  const int j = threadIdx.x;
+  const int k = j & (LS - 1);
+  double2 v[16];
+#pragma unroll
+  for (int p = 0; p < 16; ++p) v[p] = s[pidx(j + p * NB)];
+  __syncthreads();
+  if (LS > 1) {
+    const int step = k * (N / (LS * 16));
+#pragma unroll
+    for (int p = 1; p < 16; ++p) {
+      double2 w = __ldg(tw + p * step);
+      if (SIGN > 0) w.y = -w.y;
+      v[p] = cmul(v[p], w);
+    }
+  }
+  dft16<SIGN>(v);
+  const int ob = (j - k) * 16 + k;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) s[pidx(ob + q * LS)] = v[q];
+  __syncthreads();
+}
+
+// Final Stockham pass of radix R in {2, 4, 8} (16/R butterflies per thread).
+template <int N, int SIGN, int LS, int R>
+__device__ __forceinline__ void stockham_last(double2* s, const double2* __restrict__ tw) {
+  constexpr int NB = N / 16, NBT = 16 / R;
+  double2 v[16];
+#pragma unroll
+  for (int bb = 0; bb < NBT; ++bb)
+#pragma unroll
+    for (int p = 0; p < R; ++p) v[bb * R + p] = s[pidx(threadIdx.x + bb * NB + p * (N / R))];
+  __syncthreads();
+#pragma unroll
+  for (int bb = 0; bb < NBT; ++bb) {
+    const int j = threadIdx.x + bb * NB;
+    const int k = j & (LS - 1);
+    const int step = k * (N / (LS * R));
+#pragma unroll
+    for (int p = 1; p < R; ++p) {
+      double2 w = __ldg(tw + p * step);
+      if (SIGN > 0) w.y = -w.y;
+      v[bb * R + p] = cmul(v[bb * R + p], w);
+    }
+    dft_small<SIGN, R>(v + bb * R);
+  }
+#pragma unroll
+  for (int bb = 0; bb < NBT; ++bb) {
+    const int j = threadIdx.x + bb * NB;
+    const int k = j & (LS - 1);
+    const int ob = (j - k) * R + k;
+#pragma unroll
+    for (int q = 0; q < R; ++q) s[pidx(ob + q * LS)] = v[bb * R + q];
+  }
+  __syncthreads();
+}
+
+// In-place N-point complex DFT of s (padded layout) with blockDim.x == N/16 threads.
+// SIGN = -1 forward, +1 inverse (unscaled).  tw[m] = exp(-2 pi i m / N), m < N.
+// N = 16^P * R, R in {1, 2, 4, 8}: P radix-16 passes then one radix-R pass.
+template <int N, int SIGN>
+__device__ void fft_smem(double2* s, const double2* __restrict__ tw) {
+  constexpr int LG = ilog2(N);
+  constexpr int P = LG / 4, R = 1 << (LG % 4);
+  static_assert(P >= 1 && P <= 3, "N in 2^10 .. 2^13");
+  stockham16<N, SIGN, 1>(s, tw);
+  if (P >= 2) stockham16<N, SIGN, (P >= 2 ? 16 : 1)>(s, tw);
+  if (P >= 3) stockham16<N, SIGN, (P >= 3 ? 256 : 1)>(s, tw);
+  constexpr int LSF = (P == 1) ? 16 : (P == 2 ? 256 : 4096);
+  if (R > 1) stockham_last<N, SIGN, LSF, (R > 1 ? R : 2)>(s, tw);
+}
+
+// Real-FFT split + product by H + merge for the inverse (see header comment):
+// on entry s = Z = FFT_N(z); on exit s = Z' such that IFFT_N(Z') (unscaled) gives
+// N * p packed as p[2n] + i p[2n+1]; the 1/N is folded in here.
+template <int N>
+__device__ void spectrum_product(double2* s, const double2* __restrict__ H, const double2* __restrict__ tw2) {
+  const double sc = 1.0 / (double)N;   // exact (power of two)
+  for (int k = threadIdx.x; k <= N / 2; k += blockDim.x) {
+    if (k == 0) {
+      const double2 z0 = s[pidx(0)];
+      const double X0 = z0.x + z0.y, XN = z0.x - z0.y;   // X[0], X[N] (real)
+      const double2 P0 = make_double2(X0 * H[0].x, X0 * H[0].y);
+      const double2 PN = make_double2(XN * H[N].x, XN * H[N].y);
+      // Z'[0] = (P0 + conj PN)/2 + i (P0 - conj PN)/2
+      const double2 e = make_double2(0.5 * (P0.x + PN.x), 0.5 * (P0.y - PN.y));
+      const double2 o = make_double2(0.5 * (P0.x - PN.x), 0.5 * (P0.y + PN.y));
+      s[pidx(0)] = make_double2((e.x - o.y) * sc, (e.y + o.x) * sc);
+      continue;
+    }
+    const int kp = N - k;
+    const double2 Zk = s[pidx(k)], Zkp = s[pidx(kp)];
+    const double2 Wk = __ldg(tw2 + k), Wkp = __ldg(tw2 + kp);          // exp(-2 pi i k / 2N)
+    // E[k] = (Z[k] + conj Z[k'])/2,  O[k] = -i/2 (Z[k] - conj Z[k'])
+    const double2 Ek = make_double2(0.5 * (Zk.x + Zkp.x), 0.5 * (Zk.y - Zkp.y));
+    const double2 Ok = make_double2(0.5 * (Zk.y + Zkp.y), -0.5 * (Zk.x - Zkp.x));
+    const double2 Ekp = cconj(Ek), Okp = cconj(Ok);
+    const double2 Xk = cadd(Ek, cmul(Wk, Ok));
+    const double2 Xkp = cadd(Ekp, cmul(Wkp, Okp));
+    const double2 Pk = cmul(Xk, __ldg(H + k)), Pkp = cmul(Xkp, __ldg(H + kp));
+    // Z'[k] = (P[k] + conj P[k'])/2 + i conj(W_k) (P[k] - conj P[k'])/2
+    auto merge = [&](double2 a, double2 b, double2 W) {
+      const double2 e = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
+      const double2 d = make_double2(0.5 * (a.x - b.x), 0.5 * (a.y + b.y));
+      const double2 o = cmul(d, cconj(W));
+      return make_double2((e.x - o.y) * sc, (e.y + o.x) * sc);
+    };
+    const double2 Zpk = merge(Pk, Pkp, Wk);
+    const double2 Zpkp = merge(Pkp, Pk, Wkp);
+    s[pidx(k)] = Zpk;
+    if (kp != k) s[pidx(kp)] = Zpkp;
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------------ kernel spectrum (a1, FFT core)
+// H = 2N-point real DFT of h[n] = kr[K-1-n] (n < K), k = 0..N.
+template <int N>
+__global__ void __launch_bounds__(N / 16) pc_fft_spectrum(const double* __restrict__ kr, int K,
+                                                          const double2* __restrict__ tw,
+                                                          const double2* __restrict__ tw2, double2* __restrict__ H) {
+  extern __shared__ __align__(16) double2 sm[];
+  for (int n = threadIdx.x; n < N; n += blockDim.x) {
+    const int a = 2 * n, b = 2 * n + 1;
+    sm[pidx(n)] = make_double2(a < K ? kr[K - 1 - a] : 0.0, b < K ? kr[K - 1 - b] : 0.0);
+  }
+  __syncthreads();
+  fft_smem<N, -1>(sm, tw);
+  for (int k = threadIdx.x; k <= N; k += blockDim.x) {
+    const double2 Zk = sm[pidx(k % N)], Zkp = sm[pidx((N - k) % N)];
+    const double2 E = make_double2(0.5 * (Zk.x + Zkp.x), 0.5 * (Zk.y - Zkp.y));
+    const double2 O = make_double2(0.5 * (Zk.y + Zkp.y), -0.5 * (Zk.x - Zkp.x));
+    H[k] = cadd(E, cmul(__ldg(tw2 + k), O));
+  }
+}
+
+// ------------------------------------------------------------------ the FFT-core conv kernel
+template <int PACK, int N>
+__global__ void __launch_bounds__(N / 16, 1) pc_fft_conv_kernel(Geo g, Exec e, FftArgs f) {
+  extern __shared__ __align__(16) double2 sm[];
+  __shared__ double red[32];
+  __shared__ double bx[2];
+  const ModeP& mp = e.mp[PACK];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const long long job = blockIdx.x;
+  const long long sig = job / e.jobs_per_sig;
+  long long r0 = job % e.jobs_per_sig;
+  long long w;
+  int part;
+  if (e.b0 == 0 && r0 < f.parts0) {
+    w = 0;
+    part = (int)r0;
+  } else {
+    if (e.b0 == 0) r0 -= f.parts0;
+    w = e.b0 + (e.b0 == 0 ? 1 : 0) + r0 / f.parts1;
+    part = (int)(r0 % f.parts1);
+  }
+  const Blk b = block_info<PACK>(g, mp.K, w);
+  const double* gsrc = e.s + sig * e.s_stride + (b.g0 - e.s_off);
+  const long long avail = g.L - b.g0;
+  const int n_valid = (int)(avail < 0 ? 0 : (avail > g.W_block ? g.W_block : avail));
+
+  // a2/a3: block peak and c_s (Eq. (2))
+  double c_s = 1.0;
+  if (PACK != PACK_FULL) {
+    double m = 0.0;
+    for (int i = tid; i < n_valid; i += nt) m = fmax(m, fabs(__ldg(gsrc + i)));
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((tid & 31) == 0) red[tid >> 5] = m;
+    __syncthreads();
+    double peak = 0.0;
+    for (int wi = 0; wi < nt / 32; ++wi) peak = fmax(peak, red[wi]);
+    c_s = (peak == 0.0) ? 1.0 : mp.Q / peak;
+  }
+  const double inv = dequant_scale(c_s, mp.c_k);
+  // part window: core outputs [m_lo, m_hi); sym parts after the first also need word m_lo-1
+  const int front = (PACK == PACK_SYM && part > 0) ? 1 : 0;
+  const int m_lo = (part == 0) ? 0 : f.part0_out + (part - 1) * f.part_out;
+  const int m_hi = min(b.M_out, m_lo + (part == 0 ? f.part0_out : f.part_out));
+  const int cw0 = m_lo - front;                 // core word at window position 0
+  auto sample = [&](int i) -> double { return (i < 0 || i >= n_valid) ? 0.0 : __ldg(gsrc + i); };
+  auto word = [&](int cw) -> double {           // a4: the core's input word cw
+    if (cw < 0 || cw >= b.xlen) return 0.0;
+    if (PACK == PACK_SYM) {
+      const int j = cw - b.pre;
+      if (j < 0) return 0.0;
+      return pack_sym(compand1(c_s, sample(2 * j)), compand1(c_s, sample(2 * j + 1)), mp.eps);
+    } else if (PACK == PACK_ASYM2 || PACK == PACK_ASYM3) {
+      constexpr int M = (PACK == PACK_ASYM2) ? 2 : 3;
+      const int base = b.o0 - (g.Np - 1) + cw;
+      double v = compand1(c_s, sample(base + (M - 1) * b.S));
+#pragma unroll
+      for (int q = M - 2; q >= 0; --q) v = __dadd_rn(compand1(c_s, sample(base + q * b.S)), __dmul_rn(mp.eps, v));
+      return v;
+    }
+    return sample(b.o0 - (g.Np - 1) + cw);
+  };
+  // window of 2N real words (outputs need cw0 .. cw0 + (m_hi-m_lo+front) + K - 2)
+  const int wlen = (m_hi - m_lo + front) + mp.K - 1;
+  for (int n = tid; n < N; n += nt) {
+    const int a = 2 * n, c = 2 * n + 1;
+    sm[pidx(n)] = make_double2(a < wlen ? word(cw0 + a) : 0.0, c < wlen ? word(cw0 + c) : 0.0);
+  }
+  __syncthreads();
+  fft_smem<N, -1>(sm, f.tw);                                        // a5: forward
+  spectrum_product<N>(sm, f.H, f.tw2);
+  fft_smem<N, +1>(sm, f.tw);                                        // a5: inverse
+  // p[q] = Re/Im of sm[q/2]; core output m (window-relative mw = m - cw0) = p[mw + K - 1]
+  auto pval = [&](int q) -> double {
+    const double2 z = sm[pidx(q >> 1)];
+    return (q & 1) ? z.y : z.x;
+  };
+  const int K1 = mp.K - 1;
+  double* __restrict__ r = e.r + sig * e.r_stride;
+  const long long gbase = b.g0 + b.o0;
+  const long long L_conv = g.L + g.N - 1;
+  auto store = [&](int k, double val) {
+    const long long gg = gbase + k;
+    if (g.mode == 0) {
+      if (gg < L_conv) r[gg - e.r_off] = val;
+    } else {
+      const long long j = gg - (g.N - 1);
+      if (j >= 0 && j <= g.L - g.N) r[j - e.r_off] = val;
+    }
+  };
+  double resid = 0.0;                                               // last-digit residual (LSB)
+  if (PACK == PACK_SYM) {
+    const int moff = (w == 0) ? 0 : 1;
+    for (int m = m_lo + tid; m < m_hi; m += nt) {
+      if (m < moff) continue;
+      const double v = pval(m - cw0 + K1);
+      const Digits3 d = decode_sym(v, mp.eps, mp.eps_inv, mp.pow2);
+      const double rem = __dsub_rn(v, __dmul_rn(d.C, mp.eps_inv));
+      resid = fmax(resid, fabs(__dmul_rn(__dsub_rn(rem, d.A), mp.eps_inv) - d.B));
+      double Bp = 0.0;
+      if (m >= 1) Bp = decode_sym(pval(m - 1 - cw0 + K1), mp.eps, mp.eps_inv, mp.pow2).B;
+      const int k = 2 * (m - moff);
+      store(k + 1, __dmul_rn(d.A, inv));
+      store(k, __dmul_rn(d.C + Bp, inv));
+    }
+  } else if (PACK == PACK_ASYM2 || PACK == PACK_ASYM3) {
+    constexpr int M = (PACK == PACK_ASYM2) ? 2 : 3;
+    for (int m = m_lo + tid; m < m_hi; m += nt) {
+      double v = pval(m - cw0 + K1);
+#pragma unroll
+      for (int q = 0; q < M; ++q) {
+        const double t = rint(v);
+        if (q == M - 1) resid = fmax(resid, fabs(v - t));
+        if (q < M - 1) v = __dmul_rn(__dsub_rn(v, t), mp.eps_inv);
+        const int k = q * b.S + m;
+        if (k < b.n_out) store(k, __dmul_rn(t, inv));
+      }
+    }
+  } else {
+    for (int m = m_lo + tid; m < m_hi; m += nt) store(m, pval(m - cw0 + K1));
+  }
+  if (PACK != PACK_FULL) {
+    for (int o = 16; o > 0; o >>= 1) resid = fmax(resid, __shfl_xor_sync(0xffffffffu, resid, o));
+    if ((tid & 31) == 0 && resid > 0.0)
+      atomicMax(reinterpret_cast<unsigned long long*>(f.resid), (unsigned long long)__double_as_longlong(resid));
+  }
+  (void)bx;
+}
+
+// ------------------------------------------------------------------ launchers
+template <int N>
+static cudaError_t launch_fft_N(int packing, const Geo& g, const Exec& e, const FftArgs& f, long long n_jobs,
+                                cudaStream_t st) {
+  const size_t smem = (size_t)(N + N / 16) * sizeof(double2);
+  cudaError_t err = cudaSuccess;
+  switch (packing) {
+#define PC_FFT_CASE(PK)                                                                                  \
+  case PK: {                                                                                             \
+    auto kfn = pc_fft_conv_kernel<PK, N>;                                                               \
+    static bool set = false;                                                                             \
+    if (!set) {                                                                                          \
+      err = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);          \
+      if (err != cudaSuccess) return err;                                                                \
+      set = true;                                                                                        \
+    }                                                                                                    \
+    kfn<<<(unsigned)n_jobs, N / 16, smem, st>>>(g, e, f);                                               \
+    break;                                                                                               \
+  }
+    PC_FFT_CASE(PACK_FULL)
+    PC_FFT_CASE(PACK_SYM)
+    PC_FFT_CASE(PACK_ASYM2)
+    PC_FFT_CASE(PACK_ASYM3)
+#undef PC_FFT_CASE
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fft_conv(int packing, int N, const Geo& g, const Exec& e, const FftArgs& f, long long n_jobs,
+                            cudaStream_t st) {
+  if (n_jobs <= 0) return cudaSuccess;
+  switch (N) {
+    case 1024: return launch_fft_N<1024>(packing, g, e, f, n_jobs, st);
+    case 2048: return launch_fft_N<2048>(packing, g, e, f, n_jobs, st);
+    case 4096: return launch_fft_N<4096>(packing, g, e, f, n_jobs, st);
+    case 8192: return launch_fft_N<8192>(packing, g, e, f, n_jobs, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int N>
+static cudaError_t launch_spec_N(const double* kr, int K, const double2* tw, const double2* tw2, double2* H,
+                                 cudaStream_t st) {
+  const size_t smem = (size_t)(N + N / 16) * sizeof(double2);
+  auto kfn = pc_fft_spectrum<N>;
+  cudaError_t err = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (err != cudaSuccess) return err;
+  kfn<<<1, N / 16, smem, st>>>(kr, K, tw, tw2, H);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fft_spectrum(int N, const double* kr, int K, const double2* tw, const double2* tw2, double2* H,
+                                cudaStream_t st) {
+  switch (N) {
+    case 1024: return launch_spec_N<1024>(kr, K, tw, tw2, H, st);
+    case 2048: return launch_spec_N<2048>(kr, K, tw, tw2, H, st);
+    case 4096: return launch_spec_N<4096>(kr, K, tw, tw2, H, st);
+    case 8192: return launch_spec_N<8192>(kr, K, tw, tw2, H, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace pc

@@ -57,6 +57,20 @@ struct Exec {
   unsigned long long* dbg_timing;   // persistent kernel: per CTA {smid, t_start, t_end, jobs}
 };
 
+// FFT overlap-save core (pc_fft.cu).
+struct FftArgs {
+  const double2* tw;     // exp(-2 pi i m / N), m < N          (N complex points)
+  const double2* tw2;    // exp(-2 pi i k / 2N), k <= N         (real-FFT split/merge)
+  const double2* H;      // 2N-point real DFT of the core taps, k <= N
+  double* resid;         // plan-owned max last-digit residual (LSB), atomicMax on the bits
+  int part0_out, part_out;   // core outputs of a block's first / later parts
+  long long parts0, parts1;  // parts of block 0 / of every other block
+};
+cudaError_t launch_fft_conv(int packing, int N, const Geo& g, const Exec& e, const FftArgs& f, long long n_jobs,
+                            cudaStream_t st);
+cudaError_t launch_fft_spectrum(int N, const double* kr, int K, const double2* tw, const double2* tw2, double2* H,
+                                cudaStream_t st);
+
 cudaError_t launch_fused(int packing, const Geo& g, const Exec& e, long long n_jobs, int threads, size_t smem,
                          cudaStream_t st);
 // Tiled persistent warp-specialized kernel (pc_tiled.cu): grid = SMs x resident CTAs.

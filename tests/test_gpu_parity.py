@@ -434,3 +434,79 @@ def test_cfg5_full_size_adaptive_sampled():
             assert np.max(np.abs(got[lo:lo + n] - br.out[:n])) <= 1e-12 * np.max(np.abs(br.out[:n]))
         else:
             assert np.array_equal(got[lo:lo + n], br.out[:n])
+
+
+# --------------------------------------------------------------------- FFT core (config 3)
+def fft_run(s, k, W_block, packing, Q, mode=O.CONV, rmax_rule=O.RMAX_L1, policy=None):
+    opts = pcb.opts_default(core=pcb.CORE_FFT, rmax_rule=rmax_rule,
+                            bound_policy=pcb.BOUND_WARN if policy is None else policy)
+    with pcb.Plan(len(s), len(k), W_block, mode, PK[packing], Q, opts=opts) as p:
+        p.set_kernel(dev(k))
+        info = p.info()
+        r = torch.full((info["L_out"],), float("nan"), dtype=torch.float64, device=DEV)
+        p.execute(dev(s), r)
+        torch.cuda.synchronize()
+        res, rc = p.residual()
+        return r.cpu().numpy(), res, rc, info
+
+
+@pytest.mark.parametrize("case", [(1 << 18, 4096, 16384), (50000, 1000, 4096), (30000, 63, 1024), (9000, 512, 2048)])
+def test_fft_full_precision(case):
+    L, N, W_block = case
+    rng = np.random.default_rng(N)
+    s, k = rng.laplace(0, 0.2, L), rng.normal(0, 1 / np.sqrt(N), N)
+    got, _, _, info = fft_run(s, k, W_block, O.FULL, 0)
+    want = O.full_precision(s, k)
+    assert info["fft_n"] > 0
+    assert np.max(np.abs(got - want)) / np.max(np.abs(want)) < 1e-12
+
+
+@pytest.mark.parametrize("packing,Q", [(O.ASYM2, 127), (O.ASYM2, 255), (O.ASYM3, 7), (O.SYM, 7), (O.SYM, 12)])
+def test_fft_packed_exact_cfg3_geometry(packing, Q):
+    """Config 3 geometry (N = 4096, W_block = 16384) on a 2^18-sample slice: the FFT core's
+    packed outputs round to the exact integers (bit-exact dequantized outputs), residual
+    monitor below 0.25 LSB.  asym2 at 8/9 bits is the config's operating point."""
+    s, k = WL.cfg3(seed=0, L=1 << 18)
+    ref = O.conv_pipeline(s, k, 16384, packing, Q, rmax_rule=O.RMAX_L1)
+    assert ref.kernel.bound_ok and ref.mismatches == 0
+    got, res, rc, info = fft_run(s, k, 16384, packing, Q)
+    assert rc == pcb.PC_OK and res < 0.25, res
+    assert np.array_equal(got, ref.out)
+
+
+@pytest.mark.parametrize("packing", [O.SYM, O.ASYM2, O.FULL])
+def test_fft_multi_part_blocks_and_xcorr(packing):
+    """Blocks split into several FFT parts (large W_block, small transform) and xcorr mode."""
+    rng = np.random.default_rng(3)
+    s, q = rng.laplace(0, 0.3, 60000), rng.uniform(-1, 1, 700)
+    Q = {O.SYM: 3, O.ASYM2: 63, O.FULL: 0}[packing]
+    for mode in (O.CONV, O.XCORR):
+        got, res, rc, info = fft_run(s, q, 16384, packing, Q, mode=mode)
+        if packing == O.FULL:
+            want = O.full_precision(s, q, mode)
+            assert np.max(np.abs(got - want)) / np.max(np.abs(want)) < 1e-12
+        else:
+            ref = O.conv_pipeline(s, q, 16384, packing, Q, mode=mode, rmax_rule=O.RMAX_L1)
+            assert rc == pcb.PC_OK and np.array_equal(got, ref.out)
+
+
+def test_fft_residual_monitor_flags_overflowing_precision():
+    """Fault injection: symmetric packing past its FFT precision (WARN policy) -> the monitor
+    reports a residual above 0.25 LSB (PC_W_UNPACK_MARGIN) instead of silently passing."""
+    s, k = WL.cfg3(seed=0, L=1 << 17)
+    _, res_lo, rc_lo, _ = fft_run(s, k, 16384, O.SYM, 4)
+    _, res_hi, rc_hi, _ = fft_run(s, k, 16384, O.SYM, 40)
+    assert res_lo < 0.25 and rc_lo == pcb.PC_OK
+    assert res_hi > res_lo and rc_hi == pcb.PC_W_UNPACK_MARGIN
+
+
+def test_cfg3_full_size_fft_sampled():
+    """Config 3 at full size through the FFT core: asym2 9-bit bit-exact on sampled blocks."""
+    s, k = WL.cfg3(seed=0)
+    geom = O.Geometry(len(s), len(k), 16384)
+    blocks = sorted({0, 1, geom.P // 2, geom.P - 1})
+    ref = O.conv_pipeline(s, k, 16384, O.ASYM2, 255, rmax_rule=O.RMAX_L1, blocks=blocks)
+    got, res, rc, _ = fft_run(s, k, 16384, O.ASYM2, 255)
+    sel = ~np.isnan(ref.out)
+    assert rc == pcb.PC_OK and res < 0.25
+    assert np.array_equal(got[sel], ref.out[sel])
