@@ -11,7 +11,11 @@ asymmetric packing M=2 at 10 bits (Q = 511), L1 companding range (reading C3), d
 signal per GPU.  N GPUs: N independent cfg2 signals (seed = rank), one per rank, no
 collective on the data path ("scaling": "weak").
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+Other workloads (--workload cfg1|cfg3|cfg4|cfg5) measure the remaining configs the same
+way (cfg3 also through the FFT core; cfg4 = batched cross-correlation of database signals
+with the NCCL score gather; cfg5 = SNR-constrained adaptation + execution).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload cfgX]
 """
 from __future__ import annotations
 
@@ -30,17 +34,26 @@ sys.path.insert(0, ROOT)
 
 MEASURED_FP64_TFLOPS = 34.0   # profiles/r01_fp64_peak.log: sustained DFMA, 148 SMs @ 1965 MHz
 FP64_PEAK_SOURCE = "measured (tools/fp64_peak.cu, profiles/r01_fp64_peak.log); not in MEASURED_PEAKS.json"
+HBM_GBS = 6540.2              # MEASURED_PEAKS.json hbm_gbs (copy)
 
-POINTS = {
-    # name: (packing, Q, rmax_rule)  -- packing codes of include/packedconv.h
-    "asym2_10b": (2, 511, 1),
-    "asym2_8b": (2, 127, 1),
-    "asym3_8b": (3, 127, 1),
-    "sym_8b": (1, 127, 1),
-    "sym_6b": (1, 31, 1),
-    "full": (0, 0, 0),
+FULL, SYM, ASYM2, ASYM3 = 0, 1, 2, 3
+DIRECT, FFT = 0, 1
+# workload -> (W_block, points {name: (packing, Q, rmax_rule, core)}, headline, full-precision point)
+WORKLOADS = {
+    "cfg1": (1024, {"asym2_9b": (ASYM2, 255, 0, DIRECT), "asym2_8b": (ASYM2, 127, 0, DIRECT),
+                    "sym_q44": (SYM, 44, 0, DIRECT), "full": (FULL, 0, 0, DIRECT)}, "asym2_9b", "full"),
+    "cfg2": (4096, {"asym2_10b": (ASYM2, 511, 1, DIRECT), "asym2_8b": (ASYM2, 127, 1, DIRECT),
+                    "asym3_8b": (ASYM3, 127, 1, DIRECT), "sym_8b": (SYM, 127, 1, DIRECT),
+                    "sym_6b": (SYM, 31, 1, DIRECT), "full": (FULL, 0, 0, DIRECT)}, "asym2_10b", "full"),
+    "cfg3": (16384, {"asym2_9b_fft": (ASYM2, 255, 1, FFT), "asym2_8b_fft": (ASYM2, 127, 1, FFT),
+                     "sym_q12_fft": (SYM, 12, 1, FFT), "full_fft": (FULL, 0, 0, FFT),
+                     "asym2_9b_direct": (ASYM2, 255, 1, DIRECT), "full_direct": (FULL, 0, 0, DIRECT)},
+             "asym2_9b_fft", "full_fft"),
+    "cfg4": (32768, {"asym2_8b": (ASYM2, 127, 1, DIRECT), "sym_q7": (SYM, 7, 1, DIRECT),
+                     "full": (FULL, 0, 0, DIRECT)}, "asym2_8b", "full"),
+    "cfg5": (4096, {"adapt_40db": (4, 40.0, 1, DIRECT), "adapt_50db": (4, 50.0, 1, DIRECT),
+                    "adapt_60db": (4, 60.0, 1, DIRECT), "full": (FULL, 0, 0, DIRECT)}, "adapt_40db", "full"),
 }
-HEADLINE = "asym2_10b"
 
 
 def parse():
@@ -49,10 +62,12 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg2")
-    ap.add_argument("--points", default=",".join(POINTS))
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--points", default="", help="comma-separated subset of the workload's points")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--L", type=int, default=0, help="override the workload length (scaling studies)")
+    ap.add_argument("--L", type=int, default=0, help="override the signal length (scaling studies)")
+    ap.add_argument("--signals", type=int, default=0, help="cfg4: database signals in total (default 1024)")
+    ap.add_argument("--force-warps", type=int, default=0, help="diagnostics: consumer warps per CTA")
     return ap.parse_args()
 
 
@@ -132,47 +147,78 @@ def barrier(ws):
         dist.barrier()
 
 
-def workload(name, rank, L=0):
+def _cfg4_sig(i):
     from paper_1201_3018_b200 import workloads as WL
-    if name == "cfg2":
-        s, k = WL.cfg2(seed=rank, L=L or (1 << 22))
-        return s, k, 4096
+    return WL.cfg4_signal(i)
+
+
+def workload(name, rank, world, args):
+    """(signal(s), kernel, W_block, n_signals_local, first_signal) for this rank."""
+    from paper_1201_3018_b200 import workloads as WL
+    W_block = WORKLOADS[name][0]
     if name == "cfg1":
-        s, k = WL.cfg1(seed=rank)
-        return s, k, 1024
-    if name == "cfg5":
-        s, k = WL.cfg5(seed=rank, L=1 << 24)
-        return s, k, 4096
-    raise SystemExit(f"unknown workload {name}")
+        s, k = WL.cfg1(seed=rank, L=args.L or 65536)
+    elif name == "cfg2":
+        s, k = WL.cfg2(seed=rank, L=args.L or (1 << 22))
+    elif name == "cfg3":
+        s, k = WL.cfg3(seed=rank, L=args.L or (1 << 24))
+    elif name == "cfg5":
+        s, k = WL.cfg5(seed=rank, L=args.L or (1 << 26))
+    else:                                           # cfg4: this rank's share of the database
+        import multiprocessing as mp
+        n = args.signals or 1024
+        a, b = n * rank // world, n * (rank + 1) // world
+        with mp.get_context("fork").Pool(min(16, os.cpu_count() or 1)) as pool:
+            sigs = pool.map(_cfg4_sig, range(a, b))
+        q, _, _ = WL.cfg4_query(seed=0, n_signals=n)
+        return np.stack(sigs), q, W_block, b - a, a
+    return s, k, W_block, 1, 0
+
+
+def core_fma(info, packing):
+    """Algorithmic FP64 FMAs of the packed core per signal: sum over blocks of M_out * K."""
+    Np, W, P, K = info["Np"], info["W"], info["P"], info["taps"]
+    if packing == FULL:
+        m_first, m_rest = W + Np - 1, W
+    elif packing == SYM:
+        m_first, m_rest = (W + Np - 1) // 2, W // 2 + 1
+    else:
+        M = 2 if packing == ASYM2 else 3
+        m_first, m_rest = -(-(W + Np - 1) // M), -(-W // M)
+    return (m_first + (P - 1) * m_rest) * K
 
 
 def cpu_baseline(s, k, W_block, point, target_s=12.0):
     """The oracle as it stands, on a bounded sample of the same workload: consecutive
     blocks from block 1 until ~target_s seconds of CPU work; value = output samples/s."""
     import oracle as O
-    packing, Q, rmax = POINTS[point]
+    packing, Q, rmax, _ = point
+    if packing not in (FULL, SYM, ASYM2, ASYM3):
+        packing, Q, rmax = FULL, 0, 0
     geom = O.Geometry(len(s), len(k), W_block)
     ks = O.prepare_kernel(k, geom, packing, Q, None, O.CONV, O.EPS_POW2, rmax)
     t0 = time.perf_counter()
-    n = 0
-    w = 1
+    n, w = 0, 1
     while time.perf_counter() - t0 < target_s and w < geom.P:
         O.process_block(s, w, geom, ks, Q)
         n += 1
         w += 1
     dt = time.perf_counter() - t0
     return {"value": n * geom.W / dt, "unit": "output samples/s", "cores": 1, "kind": "oracle",
-            "sample": f"{n} consecutive overlap-save blocks ({n * geom.W} outputs) of {point} at cfg2, "
-                      f"NumPy oracle single-threaded (np.convolve)"}
+            "sample": f"{n} consecutive overlap-save blocks ({n * geom.W} outputs), NumPy oracle "
+                      f"single-threaded (np.convolve)"}
 
 
 def run_reference(args, ws, rank):
     if rank != 0:
         return
-    s, k, W_block = workload(args.workload, 0)
+    W_block, points, head, _ = WORKLOADS[args.workload]
+    s, k, _, nsig, _ = workload(args.workload if args.workload != "cfg4" else "cfg2", 0, 1, args)
     import oracle as O
-    packing, Q, rmax = POINTS[HEADLINE]
-    geom = O.Geometry(len(s), len(k), W_block)
+    packing, Q, rmax, _ = points[head]
+    if packing not in (FULL, SYM, ASYM2, ASYM3):
+        packing, Q, rmax = ASYM2, 535, 1
+    geom = O.Geometry(len(s), len(k), W_block if args.workload != "cfg4" else 4096)
     ks = O.prepare_kernel(k, geom, packing, Q, None, O.CONV, O.EPS_POW2, rmax)
     blocks_per_step = 8
     for i in range(args.warmup):
@@ -182,13 +228,12 @@ def run_reference(args, ws, rank):
         for j in range(blocks_per_step):
             O.process_block(s, 1 + (i * blocks_per_step + j) % (geom.P - 1), geom, ks, Q)
     dt = time.perf_counter() - t0
-    outs = args.steps * blocks_per_step * geom.W
-    v = outs / dt
+    v = args.steps * blocks_per_step * geom.W / dt
     line = {"metric": "output samples/s, packed vs full-precision conv", "value": v, "unit": "output samples/s",
             "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.workload, "point": HEADLINE, "L": len(s), "N": len(k), "W_block": W_block,
+            "config": {"workload": args.workload, "point": head, "L": len(s), "N": len(k), "W_block": geom.W_block,
                        "step": f"{blocks_per_step} overlap-save blocks (bounded sample of the workload)"},
             "cpu_baseline": {"value": v, "unit": "output samples/s", "cores": 1, "kind": "oracle",
                              "sample": f"{blocks_per_step} blocks per step, NumPy oracle single-threaded"},
@@ -199,30 +244,51 @@ def run_reference(args, ws, rank):
 def run_ours(args, ws, rank, local):
     import torch
     from paper_1201_3018_b200 import binding as pcb
+    from paper_1201_3018_b200 import distributed as D
 
     dev = torch.device("cuda", local)
-    s, k, W_block = workload(args.workload, rank, args.L)
-    L, N = len(s), len(k)
-    L_out = L + N - 1
-    n_buf = max(2, -(-256 * (1 << 20) // (16 * L)))     # rotating buffers: > 126 MB L2 in total
-    S = [torch.from_numpy(s).to(dev) for _ in range(n_buf)]
+    W_block, points, head, full_pt = WORKLOADS[args.workload]
+    sel = [p for p in (args.points.split(",") if args.points else points) if p in points]
+    x, k, W_block, nsig, first = workload(args.workload, rank, ws, args)
+    xcorr = args.workload == "cfg4"
+    L, N = x.shape[-1], len(k)
+    L_out = (L - N + 1) if xcorr else (L + N - 1)
+    per_buf = 8 * x.size + 8 * L_out * nsig
+    n_buf = 1 if xcorr else max(2, -(-256 * (1 << 20) // per_buf))     # rotating buffers: > 126 MB L2
+    S = [torch.from_numpy(np.ascontiguousarray(x)).to(dev) for _ in range(n_buf)]
     R = [torch.empty(L_out, dtype=torch.float64, device=dev) for _ in range(n_buf)]
     k_d = torch.from_numpy(k).to(dev)
     stream = torch.cuda.current_stream(dev)
-    results = {}
-    outputs = {}
+    results, outputs = {}, {}
     sampler_summary = None
-    for name in args.points.split(","):
-        packing, Q, rmax = POINTS[name]
-        plan = pcb.Plan(L, N, W_block, pcb.MODE_CONV, packing, Q, rmax_rule=rmax)
+    for name in sel:
+        packing, Q, rmax, core = points[name]
+        adaptive = packing == 4
+        opts = pcb.opts_default(rmax_rule=rmax, core=core)
+        opts.reserved[3] = args.force_warps
+        plan = pcb.Plan(L, N, W_block, pcb.MODE_XCORR if xcorr else pcb.MODE_CONV, packing,
+                        0 if adaptive else Q, opts=opts)
         plan.set_kernel(k_d)
         info = plan.info()
+        if xcorr:
+            score = torch.empty(nsig, dtype=torch.float64, device=dev)
+            lag = torch.empty(nsig, dtype=torch.int64, device=dev)
+
+        def step(i):
+            if xcorr:
+                plan.xcorr_max(S[0], nsig, L, score, lag)
+            elif adaptive:
+                pcb.adapt_block(plan.h, S[i % n_buf], Q, 0.0, None)
+                plan.execute(S[i % n_buf], R[i % n_buf])
+            else:
+                plan.execute(S[i % n_buf], R[i % n_buf])
+
         for i in range(args.warmup):
-            plan.execute(S[i % n_buf], R[i % n_buf])
+            step(i)
         torch.cuda.synchronize(dev)
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        sampler = ClockSampler(local) if name == HEADLINE else None
+        sampler = ClockSampler(local) if name == head else None
         if sampler:
             sampler.__enter__()
             time.sleep(0.3)
@@ -231,41 +297,47 @@ def run_ours(args, ws, rank, local):
         t0.record(stream)
         for i in range(args.steps):
             ev[i][0].record(stream)
-            plan.execute(S[i % n_buf], R[i % n_buf])
+            step(i)
             ev[i][1].record(stream)
         t1.record(stream)
         torch.cuda.synchronize(dev)
         barrier(ws)
+        match = None
+        if xcorr:                                    # NCCL gather of the 16 B/signal scores
+            if ws > 1:
+                match = D.gather_best_match(score, lag, first)
+            else:
+                j = int(torch.argmax(score).item())
+                match = (first + j, float(score[j].item()), int(lag[j].item()))
         if sampler:
-            # keep sampling under load long enough to see the clocks (untimed repeats)
             t_end = time.time() + 1.0
             while time.time() < t_end:
-                for i in range(50):
-                    plan.execute(S[i % n_buf], R[i % n_buf])
+                for i in range(20):
+                    step(i)
                 torch.cuda.synchronize(dev)
             sampler.__exit__()
             sampler_summary = sampler.summary()
-        ms = t0.elapsed_time(t1)
-        ms = max_over_ranks(ms, ws)
+        ms = max_over_ranks(t0.elapsed_time(t1), ws)
         kern_ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
-        # algorithmic FP64 work of the core per launch: sum over blocks of M_out * K FMAs
-        Np, W, P, K = info["Np"], info["W"], info["P"], info["taps"]
-        if packing == 0:
-            m_first, m_rest = W + Np - 1, W
-        elif packing == 1:
-            m_first, m_rest = (W + Np - 1) // 2, W // 2 + 1
-        else:
-            M = 2 if packing == 2 else 3
-            m_first, m_rest = -(-(W + Np - 1) // M), -(-W // M)
-        fma = (m_first + (P - 1) * m_rest) * K
-        results[name] = {"ms_per_step": ms / args.steps, "kernel_ms": kern_ms,
-                         "value": ws * L_out * args.steps / (ms / 1e3),
-                         "fp64_tflops": 2.0 * fma / (kern_ms / 1e3) / 1e12, "fma_per_output": fma / L_out,
-                         "R_max": info["R_max"], "Q": Q, "bound_ok": info["bound_ok"], "tile": info["core_tile"]}
-        outputs[name] = R[(args.steps - 1) % n_buf].clone()
-        if name == HEADLINE:
-            # end to end through the C ABI with HOST buffers (pinned): H2D + run + D2H per step
-            sh = torch.from_numpy(s).pin_memory()
+        fma = core_fma(info, packing if not adaptive else FULL) * nsig
+        rec = {"ms_per_step": ms / args.steps, "kernel_ms": kern_ms,
+               "value": ws * L_out * nsig * args.steps / (ms / 1e3), "R_max": info["R_max"], "Q": Q,
+               "bound_ok": info["bound_ok"], "tile": info["core_tile"], "fft_n": info["fft_n"],
+               "core": "fft" if core == FFT else "direct"}
+        if core == DIRECT and not adaptive:
+            rec["fp64_tflops"] = 2.0 * fma / (kern_ms / 1e3) / 1e12
+            rec["fma_per_output"] = fma / (L_out * nsig)
+        if core == FFT:
+            res, rc = plan.residual()
+            rec["fft_residual_lsb"] = res
+            rec["hbm_gbs_algorithmic"] = 8 * (L + L_out) / (kern_ms / 1e3) / 1e9
+        if xcorr:
+            rec["best_match"] = match
+        results[name] = rec
+        if not xcorr:
+            outputs[name] = R[(args.steps - 1) % n_buf].clone()
+        if name == head and not adaptive and not xcorr:
+            sh = torch.from_numpy(np.ascontiguousarray(x)).pin_memory()
             rh = torch.empty(L_out, dtype=torch.float64).pin_memory()
             for i in range(2):
                 plan.execute_host(sh, rh)
@@ -279,47 +351,52 @@ def run_ours(args, ws, rank, local):
             e1.record(stream)
             torch.cuda.synchronize(dev)
             e_ms = max_over_ranks(e0.elapsed_time(e1), ws)
-            results[name]["e2e"] = {"value": ws * L_out * n_e2e / (e_ms / 1e3), "unit": "output samples/s",
-                                    "h2d_bytes_per_step": 8 * L, "d2h_bytes_per_step": 8 * L_out,
-                                    "steps": n_e2e}
+            rec["e2e"] = {"value": ws * L_out * n_e2e / (e_ms / 1e3), "unit": "output samples/s",
+                          "h2d_bytes_per_step": 8 * L, "d2h_bytes_per_step": 8 * L_out, "steps": n_e2e}
         plan.close()
-    # accuracy of every point against the GPU full-precision path (same input)
-    if "full" in outputs:
-        ref = outputs["full"].double()
+    if full_pt in outputs:
+        ref = outputs[full_pt].double()
         for name, out in outputs.items():
-            if name == "full":
+            if name == full_pt or points[name][0] == FULL:
                 continue
             err = torch.sum((ref - out) ** 2).item()
             results[name]["snr_db_vs_full"] = 10 * np.log10(torch.sum(ref * ref).item() / err) if err > 0 else None
     if rank != 0:
         return
-    h = results[HEADLINE]
-    full = results.get("full")
+    h = results[head]
+    full = results.get(full_pt)
     traffic, traffic_src = None, None
     prof = os.path.join(ROOT, "profiles", "r01_ncu_cfg2.json")
-    kname = f"pc_persist_kernel<2, {h['tile']}>"
     if args.workload == "cfg2" and os.path.exists(prof):
-        for rec in json.load(open(prof)).get("ncu_full", []):
-            if kname in rec["kernel"]:
-                rd = float(rec["dram__bytes_read.sum"].split()[0]) * (1e6 if "Mbyte" in rec["dram__bytes_read.sum"] else 1e3)
-                wr = rec["dram__bytes_write.sum"].split()
-                wr = float(wr[0]) * (1e6 if wr[1] == "Mbyte" else 1e3 if wr[1] == "Kbyte" else 1.0)
-                traffic, traffic_src = rd + wr, "profiles/r01_ncu_cfg2.json (ncu --set full, one launch)"
-    roof = {"bound": "alu", "achieved": h["fp64_tflops"], "peak": MEASURED_FP64_TFLOPS, "unit": "TFLOP/s",
-            "frac": h["fp64_tflops"] / MEASURED_FP64_TFLOPS, "traffic": traffic, "traffic_unit": "bytes/launch",
-            "traffic_source": traffic_src, "algorithmic_bytes": 8 * (L + L_out),
-            "kernel": kname, "peak_source": FP64_PEAK_SOURCE,
-            "algorithmic": "FP64 FMAs of the packed core: sum over blocks of M_out * N' (2 flop each)"}
+        for recd in json.load(open(prof)).get("ncu_full", []):
+            if f"pc_tiled_kernel<2, {h['tile']}>" in recd["kernel"]:
+                rd = recd["dram__bytes_read.sum"].split()
+                wr = recd["dram__bytes_write.sum"].split()
+                mult = {"Mbyte": 1e6, "Kbyte": 1e3, "Gbyte": 1e9, "byte": 1.0}
+                traffic = float(rd[0]) * mult[rd[1]] + float(wr[0]) * mult[wr[1]]
+                traffic_src = "profiles/r01_ncu_cfg2.json (ncu --set full, one launch)"
+    if "fp64_tflops" in h:
+        roof = {"bound": "alu", "achieved": h["fp64_tflops"], "peak": MEASURED_FP64_TFLOPS, "unit": "TFLOP/s",
+                "frac": h["fp64_tflops"] / MEASURED_FP64_TFLOPS, "traffic": traffic, "traffic_unit": "bytes/launch",
+                "traffic_source": traffic_src, "algorithmic_bytes": 8 * (L + L_out) * nsig,
+                "kernel": f"pc_tiled_kernel<{points[head][0]}, {h['tile']}>", "peak_source": FP64_PEAK_SOURCE,
+                "algorithmic": "FP64 FMAs of the packed core: sum over blocks of M_out * K (2 flop each)"}
+    else:
+        gbs = h.get("hbm_gbs_algorithmic", 8 * (L + L_out) * nsig / (h["kernel_ms"] / 1e3) / 1e9)
+        roof = {"bound": "hbm", "achieved": gbs, "peak": HBM_GBS, "unit": "GB/s", "frac": gbs / HBM_GBS,
+                "traffic": None, "kernel": "pc_fft_conv_kernel" if h["core"] == "fft" else "pc_fused_kernel",
+                "algorithmic": "8 B read + 8 B written per sample"}
     line = {
         "metric": "output samples/s, packed vs full-precision conv, 1/2/4/8 B200; % FP64/HBM peak",
         "value": h["value"], "unit": "output samples/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": h["ms_per_step"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.workload, "L": L, "N": N, "W_block": W_block, "point": HEADLINE,
-                   "packing": "asym2", "bits": 10, "Q": 511, "rmax_rule": "l1", "eps": "pow2",
-                   "l2": f"{n_buf} rotating input/output buffer pairs ({n_buf * 16 * L >> 20} MiB) > 126 MB L2",
-                   "parallelism": f"{ws} independent signals (one per GPU), no collective"},
-        "gpu_launches": args.steps,
+        "config": {"workload": args.workload, "L": L, "N": N, "W_block": W_block, "point": head,
+                   "signals_per_gpu": nsig,
+                   "l2": (f"{n_buf} rotating input/output buffer pairs ({n_buf * per_buf >> 20} MiB) > 126 MB L2"
+                          if n_buf > 1 else f"input {8 * x.size >> 20} MiB > 126 MB L2"),
+                   "parallelism": f"{ws} rank(s), independent {'database signals + NCCL score gather' if xcorr else 'signals'}"},
+        "gpu_launches": args.steps * (2 if points[head][0] == 4 else 1),
         "roofline": roof,
         "e2e": h.get("e2e"),
         "packed_vs_full": (h["value"] / full["value"]) if full else None,
@@ -327,8 +404,8 @@ def run_ours(args, ws, rank, local):
         "points": results,
         "clocks": sampler_summary,
     }
-    if ws == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(s, k, W_block, HEADLINE)
+    if ws == 1 and not args.no_cpu_baseline and not xcorr:
+        line["cpu_baseline"] = cpu_baseline(x, k, W_block, points[head])
     print(json.dumps(line))
 
 

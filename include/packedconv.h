@@ -69,7 +69,8 @@ typedef struct conv_opts {
   int32_t device;           /* CUDA device ordinal, -1 = current device                    */
   int32_t reserved[9];      /* [0]: raw-block staging 0 auto/1 on/2 off (per-block kernel);
                                [1]: force the persistent core tile (12/14/16; tests);
-                               [2]: cap persistent CTAs per SM (diagnostics); rest 0 */
+                               [2]: cap persistent CTAs per SM (diagnostics);
+                               [3]: force consumer warps per CTA (2..4; diagnostics); rest 0 */
   double u_sys;             /* P:153; used only by the literal paper unpack form          */
 } conv_opts;
 
@@ -170,7 +171,7 @@ int conv_execute_debug(conv_plan* plan, const double* s_dev, double* r_dev, doub
  * packing of {SYM, ASYM2} whose Eq. (19) prediction at its maximum Q under its bound
  * meets snr_floor_db - calib_offset_db, else FULL.  Decisions are installed for the next
  * conv_execute on the same input and copied to out_host (P entries) if non-NULL.
- * Synchronizes `stream`. */
+ * Synchronizes `stream` only when out_host is non-NULL (otherwise stream-ordered). */
 int conv_adapt_block(conv_plan* plan, const double* s_dev, double snr_floor_db,
                      double calib_offset_db, conv_block_decision* out_host, void* stream);
 

@@ -212,6 +212,7 @@ bool tiled_shape(const conv_plan* p, int packing, TShape* sh) {
     if ((force == 12 || force == 14 || force == 16) && T != force) continue;
     const double speed = T == 16 ? 1.0 : (T == 14 ? 0.96 : 0.92);   // core-loop calibration (profiles)
     for (int ncw = 4; ncw >= 2; --ncw) {
+      if (p->opts.reserved[3] > 0 && ncw != p->opts.reserved[3]) continue;   // diagnostics: force G
       const int G = 32 * ncw;
       const long long groups = (mtyp + T - 1) / T;
       const long long tiles = (groups + G - 1) / G;
@@ -240,7 +241,7 @@ bool tiled_shape(const conv_plan* p, int packing, TShape* sh) {
     sh->nchunks = (sh->K_pad + sh->KC - 1) / sh->KC;
   }
   const int front = packing == PC_PACK_SYM ? 1 : 0;
-  sh->rows_s = front + sh->G + sh->KC / T + 1;
+  sh->rows_s = front + sh->G + sh->KC / T;   // the window reads rows up to G-1 + KC/T (+front)
   const long long g0 = (mmax + T - 1) / T;         // block 0 has the most groups
   const long long g1 = (mtyp + T - 1) / T;
   sh->tiles0 = (g0 + sh->G - 1) / sh->G;
@@ -829,10 +830,8 @@ int conv_adapt_block(conv_plan* p, const double* s, double snr_floor_db, double 
     std::free(hp);
     std::free(hs);
     if (e != cudaSuccess) return PC_E_CUDA;
-  } else if (cudaStreamSynchronize(st) != cudaSuccess) {
-    return PC_E_CUDA;
   }
-  p->adapt_ready = 1;
+  p->adapt_ready = 1;   // decisions live on the device: the next execute is stream-ordered
   return PC_OK;
 }
 
