@@ -68,6 +68,7 @@ def parse():
     ap.add_argument("--L", type=int, default=0, help="override the signal length (scaling studies)")
     ap.add_argument("--signals", type=int, default=0, help="cfg4: database signals in total (default 1024)")
     ap.add_argument("--force-warps", type=int, default=0, help="diagnostics: consumer warps per CTA")
+    ap.add_argument("--opt", action="append", default=[], help="diagnostics: conv_opts.reserved[i]=v as i=v")
     return ap.parse_args()
 
 
@@ -249,6 +250,8 @@ def run_ours(args, ws, rank, local):
     dev = torch.device("cuda", local)
     W_block, points, head, full_pt = WORKLOADS[args.workload]
     sel = [p for p in (args.points.split(",") if args.points else points) if p in points]
+    if head not in sel:                              # diagnostics subset: first selected point leads
+        head = sel[0]
     x, k, W_block, nsig, first = workload(args.workload, rank, ws, args)
     xcorr = args.workload == "cfg4"
     L, N = x.shape[-1], len(k)
@@ -266,6 +269,9 @@ def run_ours(args, ws, rank, local):
         adaptive = packing == 4
         opts = pcb.opts_default(rmax_rule=rmax, core=core)
         opts.reserved[3] = args.force_warps
+        for kv in args.opt:
+            i, v = kv.split("=")
+            opts.reserved[int(i)] = int(v)
         plan = pcb.Plan(L, N, W_block, pcb.MODE_XCORR if xcorr else pcb.MODE_CONV, packing,
                         0 if adaptive else Q, opts=opts)
         plan.set_kernel(k_d)

@@ -54,6 +54,8 @@ struct conv_plan {
   double* d_sigma = nullptr;
   double* d_peak = nullptr;
   int* d_cand = nullptr;
+  int* d_lists = nullptr;              // adaptive: per-packing ascending block lists [4][P]
+  int* d_counts = nullptr;             // adaptive: their lengths [4]
   int adapt_ready = 0;
   // host end-to-end staging
   double* d_in = nullptr;
@@ -62,8 +64,7 @@ struct conv_plan {
   double* d_xc = nullptr;
   size_t d_xc_bytes = 0;
   // persistent kernel job counter (monotonic; base tracked on the host)
-  unsigned long long* d_counter = nullptr;
-  unsigned long long counter_base = 0;
+  unsigned* d_counter = nullptr;        // tiled kernel: per-SM job queues + done counter (zero between launches)
   // FFT core
   int fft_N = 0;                       // complex points (real transform length 2N)
   double2* d_tw = nullptr;             // exp(-2 pi i m / N)
@@ -194,11 +195,12 @@ bool launch_shape(const conv_plan* p, const int* packs, int npacks, Shape* sh) {
   return true;
 }
 
-// Tiled persistent kernel (pc_tiled.cu): choose the tile T and consumer warps so that
-// typical blocks' groups fill whole warps and tiles; taps resident when <= 4096, else
-// chunks of ~1024 taps (a multiple of T).
+// Tiled persistent kernel (pc_tiled.cu), one CTA per SM: choose the tile T and the parts per
+// job (G = 32 * npart groups, npart in {1, 2, 4}) so that typical blocks' groups fill whole
+// tiles; taps resident when <= 4096, else chunks of ~1024 taps (a multiple of T); as many
+// stage-ring slots as shared memory holds (2..8) after the per-warp output staging rows.
 struct TShape {
-  int T, threads, np_warps, G, KC, nchunks, taps_resident, rows_s, K_pad;
+  int T, threads, G, KC, nchunks, taps_resident, rows_s, K_pad, nstages;
   long long tiles0, tiles1;
   size_t smem;
 };
@@ -211,13 +213,14 @@ bool tiled_shape(const conv_plan* p, int packing, TShape* sh) {
   for (int T : pc::kTPChoices) {
     if ((force == 12 || force == 14 || force == 16) && T != force) continue;
     const double speed = T == 16 ? 1.0 : (T == 14 ? 0.96 : 0.92);   // core-loop calibration (profiles)
-    for (int ncw = 4; ncw >= 2; --ncw) {
-      if (p->opts.reserved[3] > 0 && ncw != p->opts.reserved[3]) continue;   // diagnostics: force G
-      const int G = 32 * ncw;
+    for (int npart : {4, 2, 1}) {
+      if (p->opts.reserved[3] > 0 && npart != p->opts.reserved[3]) continue;   // diagnostics: force G
+      const int G = 32 * npart;
       const long long groups = (mtyp + T - 1) / T;
       const long long tiles = (groups + G - 1) / G;
       const double util = (double)groups / (double)(tiles * G);
-      const double score = util * speed * (ncw == 4 ? 1.0 : 0.97);
+      // fewer parts per job: more jobs (ring slots, producer work) per resident warp
+      const double score = util * speed * (npart == 4 ? 1.0 : (npart == 2 ? 0.9 : 0.75));
       if (score > best + 1e-9) {
         best = score;
         sh->T = T;
@@ -227,8 +230,7 @@ bool tiled_shape(const conv_plan* p, int packing, TShape* sh) {
   }
   const int T = sh->T;
   sh->K_pad = (K + T - 1) / T * T;
-  sh->np_warps = K < 256 ? 2 : 1;
-  sh->threads = sh->G + 32 * sh->np_warps;
+  sh->threads = pc::kTiledThreads;
   const int KCmax = 4096;
   if (sh->K_pad <= KCmax) {
     sh->taps_resident = 1;
@@ -247,9 +249,14 @@ bool tiled_shape(const conv_plan* p, int packing, TShape* sh) {
   sh->tiles0 = (g0 + sh->G - 1) / sh->G;
   sh->tiles1 = (g1 + sh->G - 1) / sh->G;
   const size_t stage = (size_t)(((T + 1) * sh->rows_s + 1) & ~1) * 8 + (sh->taps_resident ? 0 : (size_t)sh->KC * 8);
-  sh->smem = pc::kSmemHeader + (sh->taps_resident ? (size_t)sh->K_pad * 8 : 0) + 2 * stage +
-             (packing == PC_PACK_SYM ? 2 * (2 * (size_t)sh->G + 2) * 8 : 0);
-  return sh->smem <= kMaxSmem;
+  const size_t fixed = pc::kTiledHeader + (sh->taps_resident ? (size_t)sh->K_pad * 8 : 0) +
+                       (size_t)pc::kTiledConsWarps * 32 * (T + 1) * 8;
+  if (fixed + 2 * stage > kMaxSmem) return false;
+  sh->nstages = (int)((kMaxSmem - fixed) / stage);
+  if (sh->nstages > pc::kTiledMaxStages) sh->nstages = pc::kTiledMaxStages;
+  sh->smem = fixed + (size_t)sh->nstages * stage;
+  if (sh->smem < kMaxSmem / 2 + 4096) sh->smem = kMaxSmem / 2 + 4096;   // one CTA per SM
+  return true;
 }
 
 // FFT core geometry: part sizes and counts for 2N real points.  A block's first part gives
@@ -363,14 +370,46 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
     return cuda_status(pc::launch_fft_conv(p->packing, p->fft_N, make_geo(p), e, f, e.jobs_per_sig * n_sig, st));
   }
   TShape ts;
+  if (!dbg && p->packing == PC_PACK_ADAPTIVE && p->opts.exec == PC_EXEC_FUSED && n_sig == 1 && b0 == 0 &&
+      nblk == p->P && p->d_lists) {
+    // a8 -> a2..a7: one tiled launch per packing over its block list (pc_adapt_lists)
+    TShape sh3[3];
+    const int order[3] = {PC_PACK_ASYM2, PC_PACK_SYM, PC_PACK_FULL};
+    bool ok = true;
+    for (int i = 0; i < 3; ++i) ok = ok && p->ms[order[i]].valid && tiled_shape(p, order[i], &sh3[i]);
+    if (ok) {
+      for (int i = 0; i < 3; ++i) {
+        const int pk = order[i];
+        const TShape& t = sh3[i];
+        Exec el = e;
+        el.dec_pack = nullptr;
+        el.blk_list = p->d_lists + (size_t)pk * p->P;
+        el.blk_count = p->d_counts + pk;
+        el.sm_ctr = p->d_counter;
+        el.dbg_timing = timing;
+        el.G = t.G;
+        el.nstages = t.nstages;
+        el.KC = t.KC;
+        el.nchunks = t.nchunks;
+        el.taps_resident = t.taps_resident;
+        el.rows_s = t.rows_s;
+        el.tiles0 = t.tiles0;
+        el.tiles1 = t.tiles1;
+        el.jobs_per_sig = t.tiles0 + (p->P - 1) * t.tiles1;   // upper bound: grid size only
+        el.mp[pk].K_pad = t.K_pad;
+        int grid = 0;
+        cudaError_t err = pc::launch_tiled(pk, t.T, make_geo(p), el, el.jobs_per_sig, t.threads, t.smem, st, &grid);
+        if (err != cudaSuccess) return PC_E_CUDA;
+        if (grid_out) *grid_out = grid;
+      }
+      return PC_OK;
+    }
+  }
   if (!dbg && p->packing != PC_PACK_ADAPTIVE && p->opts.exec == PC_EXEC_FUSED && tiled_shape(p, p->packing, &ts)) {
-    e.counter = p->d_counter;
-    e.base = p->counter_base;
+    e.sm_ctr = p->d_counter;
     e.dbg_timing = timing;
-    e.max_ctas_per_sm = p->opts.reserved[2];
-    e.np_warps = ts.np_warps;
-    e.nc_warps = ts.G / 32;
     e.G = ts.G;
+    e.nstages = ts.nstages;
     e.KC = ts.KC;
     e.nchunks = ts.nchunks;
     e.taps_resident = ts.taps_resident;
@@ -383,7 +422,6 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
     int grid = 0;
     cudaError_t err = pc::launch_tiled(p->packing, ts.T, make_geo(p), e, njobs, ts.threads, ts.smem, st, &grid);
     if (err != cudaSuccess) return PC_E_CUDA;
-    p->counter_base += (unsigned long long)njobs + (unsigned long long)grid;
     if (grid_out) *grid_out = grid;
     return PC_OK;
   }
@@ -464,8 +502,8 @@ int conv_plan_create(conv_plan** out, int64_t L, int32_t N, int32_t W_block, int
   e = cudaMalloc(&p->d_k_pad, sizeof(double) * Np);
   if (e == cudaSuccess) e = cudaMalloc(&p->d_k_int, sizeof(double) * Np);
   if (e == cudaSuccess) e = cudaMalloc(&p->d_scal, sizeof(double) * 4);
-  if (e == cudaSuccess) e = cudaMalloc(&p->d_counter, sizeof(unsigned long long));
-  if (e == cudaSuccess) e = cudaMemset(p->d_counter, 0, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_counter, (pc::kCtrDone + 1) * sizeof(unsigned));
+  if (e == cudaSuccess) e = cudaMemset(p->d_counter, 0, (pc::kCtrDone + 1) * sizeof(unsigned));
   if (e != cudaSuccess) {
     conv_plan_destroy(p);
     return PC_E_CUDA;
@@ -531,6 +569,8 @@ void conv_plan_destroy(conv_plan* p) {
   cudaFree(p->d_dec_pack);
   cudaFree(p->d_dec_q);
   cudaFree(p->d_dec_snr);
+  cudaFree(p->d_lists);
+  cudaFree(p->d_counts);
   cudaFree(p->d_sigma);
   cudaFree(p->d_peak);
   cudaFree(p->d_cand);
@@ -790,6 +830,8 @@ int conv_adapt_block(conv_plan* p, const double* s, double snr_floor_db, double 
     if (e == cudaSuccess) e = cudaMalloc(&p->d_sigma, sizeof(double) * P);
     if (e == cudaSuccess) e = cudaMalloc(&p->d_peak, sizeof(double) * P);
     if (e == cudaSuccess) e = cudaMalloc(&p->d_cand, sizeof(int) * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_lists, sizeof(int) * 4 * P);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_counts, sizeof(int) * 4);
     if (e != cudaSuccess) return PC_E_CUDA;
   }
   int hc[8] = {0};
@@ -807,6 +849,7 @@ int conv_adapt_block(conv_plan* p, const double* s, double snr_floor_db, double 
   if (e == cudaSuccess)
     e = pc::launch_adapt_decide(P, p->d_sigma, p->d_peak, p->k_sigma, p->k_peak, p->d_cand, p->d_cand + 4, nc, thr,
                                 p->d_dec_pack, p->d_dec_q, p->d_dec_snr, st);
+  if (e == cudaSuccess) e = pc::launch_adapt_lists(P, p->d_dec_pack, p->d_lists, p->d_counts, st);
   if (e != cudaSuccess) return PC_E_CUDA;
   if (out) {
     int* hp = (int*)std::malloc(sizeof(int) * P * 2);

@@ -374,6 +374,47 @@ __global__ void pc_adapt_decide(long long P, const double* __restrict__ sigma, c
   dec_snr[w] = lin;
 }
 
+// ------------------------------------------------------------------ a8: per-packing block lists
+// Compacts the per-block decisions into one ascending block list per packing (FULL, SYM,
+// ASYM2, ASYM3), so the tiled kernel can run each packing's blocks in its own launch.
+// One CTA of 1024 threads: ballot prefix within warps, a scan over warp totals per round.
+__global__ void __launch_bounds__(1024) pc_adapt_lists(long long P, const int* __restrict__ dec_pack,
+                                                       int* __restrict__ lists, int* __restrict__ counts) {
+  __shared__ int woff[4][32];   // per round: warp counts, then their exclusive offsets
+  __shared__ int base[4];       // list lengths before the round
+  __shared__ int rtot[4];       // round totals
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid < 4) base[tid] = 0;
+  for (long long r0 = 0; r0 < P; r0 += 1024) {
+    const long long w = r0 + tid;
+    const int d = (w < P) ? dec_pack[w] : -1;
+    int pre = 0;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const unsigned bal = __ballot_sync(0xffffffffu, d == m);
+      if (d == m) pre = __popc(bal & ((1u << lane) - 1u));
+      if (lane == 0) woff[m][wid] = __popc(bal);
+    }
+    __syncthreads();
+    if (wid < 4) {                                  // warp m scans packing m's 32 warp counts
+      const int v = woff[wid][lane];
+      int x = v;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      woff[wid][lane] = x - v;
+      if (lane == 31) rtot[wid] = x;
+    }
+    __syncthreads();
+    if (d >= 0) lists[(size_t)d * P + base[d] + woff[d][wid] + pre] = (int)w;
+    __syncthreads();
+    if (tid < 4) base[tid] += rtot[tid];
+    __syncthreads();
+  }
+  if (tid < 4) counts[tid] = base[tid];
+}
+
 // ------------------------------------------------------------------ a9: xcorr score
 // One CTA per signal: max over valid lags, lowest lag on ties (C17).
 __global__ void pc_xcorr_max(const double* __restrict__ c, long long n_lags, long long stride,
@@ -457,6 +498,11 @@ cudaError_t launch_adapt_decide(long long P, const double* sigma, const double* 
                                 cudaStream_t st) {
   pc_adapt_decide<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(P, sigma, peak, sig_k, peak_k, cand, qmode, ncand,
                                                                  thr, dp, dq, ds);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_adapt_lists(long long P, const int* dec_pack, int* lists, int* counts, cudaStream_t st) {
+  pc_adapt_lists<<<1, 1024, 0, st>>>(P, dec_pack, lists, counts);
   return cudaGetLastError();
 }
 

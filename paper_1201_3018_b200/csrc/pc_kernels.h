@@ -9,7 +9,13 @@ namespace pc {
 constexpr int kT = 8;              // outputs per thread of the per-block kernel's core
 constexpr int kMaxThreads = 1024;  // per-block kernel: threads per CTA; caps regs at 64
 constexpr int kTPChoices[3] = {16, 14, 12};   // tiled-kernel tiles instantiated; the plan picks
-constexpr int kSmemHeader = 512;   // mbarrier + reduction scratch, keeps the rest 128B-aligned
+constexpr int kSmemHeader = 512;
+constexpr int kTiledHeader = 2048;      // tiled kernel: mbarriers, stage metadata, counters
+constexpr int kTiledMaxStages = 24;     // tiled kernel: stage ring slots (>= 16 / npart jobs in flight)
+constexpr int kTiledProdWarps = 4;      // tiled kernel: producer warps (peak, companding, packing)
+constexpr int kTiledConsWarps = 16;     // tiled kernel: consumer warps (core + unpack), 4 per SMSP
+constexpr int kTiledThreads = 32 * (kTiledProdWarps + kTiledConsWarps);
+constexpr int kCtrDone = 256;     // sm_ctr[kCtrDone] counts retired CTAs; queues are sm_ctr[0, nsm)   // mbarrier + reduction scratch, keeps the rest 128B-aligned
 
 // Per-packing parameters of one launch (adaptive plans fill several).
 struct ModeP {
@@ -32,16 +38,17 @@ struct Exec {
   int reg_path;         // every block has <= blockDim.x groups: results stay in registers
   ModeP mp[4];          // indexed by packing (PACK_FULL .. PACK_ASYM3)
   const int* dec_pack;  // adaptive: per (signal, block) packing, else nullptr
+  const int* blk_list;  // tiled kernel, adaptive: ascending blocks of this launch's packing (device), else nullptr
+  const int* blk_count; // tiled kernel, adaptive: number of entries of blk_list (device)
   // persistent warp-specialized kernel
-  unsigned long long* counter;  // monotonically increasing job counter (plan-owned)
-  unsigned long long base;      // counter value at launch start
-  int np_warps, nc_warps;       // producer / consumer warps per CTA
+  unsigned* sm_ctr;             // per-SM job queue counters [kCtrDone] + done counter (plan-owned, zero between launches)
+  int nsm;                      // SMs (queues)
   int gmax;                     // max T-groups of any block (sym fix-up arrays)
-  int max_ctas_per_sm;          // diagnostics: cap on resident CTAs per SM (0 = occupancy)
   long long nsig;               // signals in the launch (jobs = nsig * nblk)
   // tiled kernel: jobs = (signal, block, tile); tile = G groups of T outputs; taps in chunks
   int G;                        // consumer threads = groups per tile
   int KC, nchunks;              // taps per chunk (multiple of T), chunks per job
+  int nstages;                  // stage ring slots (2 .. kTiledMaxStages)
   int taps_resident;            // 1: all K_pad taps stay in shared memory (nchunks == 1)
   int rows_s;                   // rows of a stage's padded word window
   long long tiles0, tiles1;     // tiles of block 0 / of every other block
@@ -84,6 +91,7 @@ cudaError_t launch_block_stats(const Geo& g, const double* s, double* sigma, dou
 cudaError_t launch_adapt_decide(long long P, const double* sigma, const double* peak, double sig_k, double peak_k,
                                 const int* cand, const int* qmode, int ncand, double thr, int* dp, int* dq, double* ds,
                                 cudaStream_t st);
+cudaError_t launch_adapt_lists(long long P, const int* dec_pack, int* lists, int* counts, cudaStream_t st);
 cudaError_t launch_xcorr_max(const double* c, long long n_signals, long long n_lags, long long stride,
                              double* score, long long* lag, cudaStream_t st);
 

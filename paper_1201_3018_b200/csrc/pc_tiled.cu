@@ -17,6 +17,8 @@
 // empty (consumers -> producers).  Symmetric packing needs B of the word before the tile for
 // the tile's first even output: consumer warp 0 computes that one extra core output by a
 // warp-split dot product (exact under the dyadic eps, reading C4).
+#include <cstdio>
+
 #include "pc_device.cuh"
 #include "pc_kernels.h"
 
@@ -25,15 +27,20 @@ namespace pc {
 namespace {
 
 struct TSmem {
-  uint64_t bar_taps, full[2], empty[2];
-  long long job[2];
-  double cs[2], inv[2];
+  uint64_t bar_taps, full[kTiledMaxStages], empty[kTiledMaxStages];
+  long long job[kTiledMaxStages];   // -1: sentinel (no more work)
+  long long seq[kTiledMaxStages];   // stage sequence number the slot holds
+  double inv[kTiledMaxStages];      // (c_s c_k)^-1 of the stage's block (Eq. (16))
+  int smsp_ctr[4];                  // consumer warp-job claim counters, one per SM sub-partition
   long long prod_job;
-  double prod_cs;
-  long long prod_blk;
+  long long turn;                   // next job sequence to claim (claims happen in sequence order)
+  long long fjob[16];               // pipeline fill: jobs of sequences 0 .. nf-1
+  double fcs[16], finv[16];         // their c_s and (c_s c_k)^-1
+  long long m_end;                  // first job sequence whose claim failed (-1: not yet)
   double red[32];
+  long long cyc[4];   // diagnostics (consumer thread 0): wait, core, unpack/store cycles; clock mark
 };
-static_assert(sizeof(TSmem) <= kSmemHeader, "header");
+static_assert(sizeof(TSmem) <= kTiledHeader, "header");
 
 struct JobPos {
   long long sig, w;
@@ -42,6 +49,19 @@ struct JobPos {
 
 __device__ __forceinline__ JobPos job_pos(const Exec& e, long long job) {
   JobPos p;
+  if (e.blk_list) {                                  // adaptive: this launch's blocks, ascending
+    const bool first0 = e.blk_list[0] == 0;          // block 0 (tiles0 tiles) can only come first
+    p.sig = 0;
+    if (first0 && job < e.tiles0) {
+      p.w = 0;
+      p.t = (int)job;
+      return p;
+    }
+    const long long r = first0 ? job - e.tiles0 : job;
+    p.w = e.blk_list[(first0 ? 1 : 0) + r / e.tiles1];
+    p.t = (int)(r % e.tiles1);
+    return p;
+  }
   p.sig = job / e.jobs_per_sig;
   long long r = job % e.jobs_per_sig;
   if (e.b0 == 0) {                                   // block 0 (if in range) has tiles0 tiles
@@ -120,7 +140,7 @@ __device__ __forceinline__ void pack_window(const Geo& g, const Blk& b, const Mo
 // a2/a3: block peak over the W_block samples (16 loads in flight per thread, shuffles),
 // companding factor c_s = Q / peak (Eq. (2)).  All `nprod` threads call it.
 template <int PACK>
-__device__ __forceinline__ double block_cs(const ModeP& mp, const double* gsrc, int n_valid, TSmem* ps, int ptid,
+__device__ __forceinline__ double block_cs(const ModeP& mp, const double* gsrc, int n_valid, double* red, int ptid,
                                            int nprod, int bar_id) {
   if (PACK == PACK_FULL) return 1.0;
   constexpr int U = 16;
@@ -147,12 +167,150 @@ __device__ __forceinline__ double block_cs(const ModeP& mp, const double* gsrc, 
 #pragma unroll
   for (int u = 1; u < U; ++u) m[0] = fmax(m[0], m[u]);
   for (int o = 16; o > 0; o >>= 1) m[0] = fmax(m[0], __shfl_xor_sync(0xffffffffu, m[0], o));
-  if ((ptid & 31) == 0) ps->red[ptid >> 5] = m[0];
+  if ((ptid & 31) == 0) red[ptid >> 5] = m[0];
   named_bar(bar_id, nprod);
   double peak = 0.0;
-  for (int wi = 0; wi < nprod / 32; ++wi) peak = fmax(peak, ps->red[wi]);
+  for (int wi = 0; wi < nprod / 32; ++wi) peak = fmax(peak, red[wi]);
   named_bar(bar_id, nprod);
   return (peak == 0.0) ? 1.0 : mp.Q / peak;
+}
+
+// The same for one warp (producer warps work on different jobs): shuffles only.
+template <int PACK>
+__device__ __forceinline__ double warp_cs(const ModeP& mp, const double* gsrc, int n_valid, int lane) {
+  if (PACK == PACK_FULL) return 1.0;
+  constexpr int U = 16;
+  double m[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) m[u] = 0.0;
+  if ((reinterpret_cast<uintptr_t>(gsrc) & 15u) == 0) {
+    const double2* g2 = reinterpret_cast<const double2*>(gsrc);
+    const int n2 = n_valid / 2;
+    for (int i0 = lane; i0 < n2; i0 += U * 32) {
+      double2 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * 32;
+        v[u] = (i < n2) ? __ldg(g2 + i) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) m[u] = fmax(m[u], fmax(fabs(v[u].x), fabs(v[u].y)));
+    }
+    if ((n_valid & 1) && lane == 0) m[0] = fmax(m[0], fabs(gsrc[n_valid - 1]));
+  } else {
+    for (int i = lane; i < n_valid; i += 32) m[0] = fmax(m[0], fabs(__ldg(gsrc + i)));
+  }
+#pragma unroll
+  for (int u = 1; u < U; ++u) m[0] = fmax(m[0], m[u]);
+  for (int o = 16; o > 0; o >>= 1) m[0] = fmax(m[0], __shfl_xor_sync(0xffffffffu, m[0], o));
+  return (m[0] == 0.0) ? 1.0 : mp.Q / m[0];
+}
+
+__device__ __forceinline__ long long fdiv_floor(long long a, long long b) {
+  const long long q = a / b;
+  return (a % b != 0 && ((a < 0) != (b < 0))) ? q - 1 : q;
+}
+__device__ __forceinline__ long long fdiv_ceil(long long a, long long b) { return -fdiv_floor(-a, b); }
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid_() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+// Watchdog wait (development safety net): a wait that has not completed after 4 s reports
+// where it is stuck and traps, so a scheduling bug fails the launch instead of hanging.
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase), "r"(kSuspendHintNs)
+      : "memory");
+  return ok != 0;
+}
+__device__ __noinline__ void mbar_stuck(int where, long long n, int st, uint32_t phase) {
+  printf("pc_tiled_kernel: wait %d stuck (block %d thread %d seq %lld slot %d parity %u)\n", where,
+         (int)blockIdx.x, (int)threadIdx.x, n, st, phase);
+  __trap();
+}
+__device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t phase, int where, long long n, int st) {
+  if (mbar_try(bar, phase)) return;
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    if (mbar_try(bar, phase)) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 4000000000ull) mbar_stuck(where, n, st, phase);
+  }
+}
+
+// Diagnostics layout of Exec::dbg_timing (conv_execute_profile), CTA c:
+//   [4c + 0..3]            smid, t_start, t_end (ns), jobs consumed
+//   [kTimCyc + 4c + 0..3]  consumer warp 0: cycles waiting on `full`, in the core, in unpack/store; fill ns
+//   [kTimTr + 16c + j]     t (ns) when job j's core finished (j < 16)
+constexpr int kTimCyc = 4 * 148 * 32, kTimTr = 8 * 148 * 32;
+//   [kTimW + ((c * 16 + w) * 16 + j) * 4 + 0..3]  consumer warp w, part j < 16: job sequence,
+//                                                   t full-ready, t core done, t stored (ns)
+//   [kTimP + ((c * 4 + w) * 16 + j) * 4 + 0..3]   producer warp w, job j < 16: job sequence,
+//                                                   t turn, t claimed, t published (ns)
+constexpr int kTimW = 24 * 148 * 32, kTimP = kTimW + 148 * 16 * 16 * 4;
+// total: kTimP + 148 * 4 * 16 * 4 uint64 entries
+
+// Job claim (one full warp).  Per-SM queues balance the FP64 work across SMs: SM s owns jobs
+// [J s / nsm, J (s+1) / nsm) and the CTAs resident on it share that queue; a CTA whose queue
+// is empty steals from the others (warp-parallel scan), so every job runs even if some SM
+// hosts no CTA.  Returns -1 when no job is left anywhere.
+__device__ __forceinline__ long long claim_job(const Exec& e, long long njobs, int lane) {
+  unsigned* ctr = e.sm_ctr;
+  const int nsm = e.nsm;
+  const int s = (int)(smid_() % (unsigned)nsm);
+  long long job = -1;
+  if (lane == 0) {
+    const long long lo = njobs * s / nsm, hi = njobs * (s + 1) / nsm;
+    if (lo < hi) {
+      const unsigned n = atomicAdd(ctr + s, 1u);
+      if (lo + n < hi) job = lo + n;
+    }
+  }
+  job = __shfl_sync(0xffffffffu, job, 0);
+  if (job >= 0) return job;
+  for (int base = 1; base < nsm; base += 32) {
+    const int t = (s + base + lane) % nsm;
+    const long long lo = njobs * t / nsm, hi = njobs * (t + 1) / nsm;
+    const bool has = (base + lane < nsm) && lo + (long long)*(volatile unsigned*)(ctr + t) < hi;
+    unsigned mask = __ballot_sync(0xffffffffu, has);
+    while (mask) {
+      const int l = __ffs(mask) - 1;
+      long long got = -1;
+      if (lane == l) {
+        const unsigned n = atomicAdd(ctr + t, 1u);
+        if (lo + n < hi) got = lo + n;
+      }
+      got = __shfl_sync(0xffffffffu, got, l);
+      if (got >= 0) return got;
+      mask &= mask - 1;
+    }
+  }
+  return -1;
+}
+
+// Called once per CTA after its last claim: the last CTA of the launch resets the queues,
+// so every launch (and every replay of a captured graph) starts from zero.
+__device__ __forceinline__ void retire_cta(const Exec& e) {
+  __threadfence();
+  if (atomicAdd(e.sm_ctr + kCtrDone, 1u) == gridDim.x - 1) {
+    for (int i = 0; i < e.nsm; ++i) e.sm_ctr[i] = 0u;
+    e.sm_ctr[kCtrDone] = 0u;
+    __threadfence();
+  }
 }
 
 }  // namespace
@@ -182,31 +340,35 @@ __device__ __forceinline__ void conv_chunk_padded(uint32_t xs_row, uint32_t kr_a
 }
 
 template <int PACK, int T>
-__global__ void __maxnreg__(96) pc_tiled_kernel(Geo g, Exec e) {
+__global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec e) {
   extern __shared__ __align__(128) unsigned char smem[];
   TSmem* ps = reinterpret_cast<TSmem*>(smem);
   const ModeP& mp = e.mp[PACK];
-  const int G = e.G;                       // consumer threads = groups per tile
+  const int G = e.G;                       // groups per tile = 32 * npart
+  const int npart = G >> 5;                // consumer warps per job (one 32-group part each)
   const int KC = e.KC;                     // taps per chunk (multiple of T)
   const int nch = e.nchunks;
+  const int NS = e.nstages;
   const int front = (PACK == PACK_SYM) ? 1 : 0;   // one row before the tile: the extra word
   const int rows_s = e.rows_s;
   const int stage_x = ((T + 1) * rows_s + 1) & ~1;   // doubles of a stage's word window (16B-aligned end)
   const int stage_words = stage_x + (e.taps_resident ? 0 : KC);
-  double* kr_res = reinterpret_cast<double*>(smem + kSmemHeader);          // resident taps
-  double* stg = kr_res + (e.taps_resident ? mp.K_pad : 0);                  // 2 stages
-  double* fix = stg + 2 * stage_words;                                      // sym: [2][2][G+1]
+  double* kr_res = reinterpret_cast<double*>(smem + kTiledHeader);          // resident taps
+  double* stg = kr_res + (e.taps_resident ? mp.K_pad : 0);                  // NS stages
+  double* wout = stg + (size_t)NS * stage_words;                            // per consumer warp: 32 (T+1)
   const int tid = threadIdx.x;
-  const int nprod = e.np_warps * 32;
-  const int ncons = blockDim.x - nprod;
-  const long long njobs = e.jobs_per_sig * e.nsig;
+  const int nprod = kTiledProdWarps * 32;
 
   if (tid == 0) {
     mbar_init(&ps->bar_taps, 1);
-    mbar_init(&ps->full[0], nprod);
-    mbar_init(&ps->full[1], nprod);
-    mbar_init(&ps->empty[0], ncons);
-    mbar_init(&ps->empty[1], ncons);
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&ps->full[i], 32);
+      mbar_init(&ps->empty[i], npart);
+      ps->seq[i] = -1;
+    }
+    for (int i = 0; i < 4; ++i) ps->smsp_ctr[i] = 0;
+    ps->turn = 1;
+    ps->m_end = -1;
     const uint32_t tb = e.taps_resident ? (uint32_t)mp.K_pad * 8u : 0u;
     mbar_arrive_expect_tx(&ps->bar_taps, tb);
     if (tb) bulk_g2s(kr_res, mp.kr, tb, &ps->bar_taps);
@@ -215,6 +377,12 @@ __global__ void __maxnreg__(96) pc_tiled_kernel(Geo g, Exec e) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
   __syncthreads();
+  if (e.dbg_timing && tid == 0) e.dbg_timing[kTimCyc + 4 * blockIdx.x + 2] = gtimer();   // t_start (stash)
+  long long njobs = e.jobs_per_sig * e.nsig;
+  if (e.blk_list) {                                  // adaptive: count written by pc_adapt_lists
+    const long long nb = *e.blk_count;
+    njobs = nb == 0 ? 0 : (e.blk_list[0] == 0 ? e.tiles0 + (nb - 1) * e.tiles1 : nb * e.tiles1);
+  }
 
   // Locate a job's block and input.
   auto job_block = [&](long long job, JobPos& jp, Blk& b, const double*& gsrc, int& n_valid) {
@@ -224,202 +392,332 @@ __global__ void __maxnreg__(96) pc_tiled_kernel(Geo g, Exec e) {
     const long long avail = g.L - b.g0;
     n_valid = (int)(avail < 0 ? 0 : (avail > g.W_block ? g.W_block : avail));
   };
-  // Hand a packed stage to the consumers (+ the tap chunk by TMA when not resident).
-  auto publish = [&](int stage, int c, long long job, double c_s, double inv, int ptid) {
-    double* xs = stg + stage * stage_words;
+  // Hand stage `st` to the consumers (+ the tap chunk by TMA when not resident).
+  auto publish = [&](long long n, int st, int c, long long job, double inv, int ptid) {
     if (ptid == 0) {
-      ps->job[stage] = job;
-      ps->cs[stage] = c_s;
-      ps->inv[stage] = inv;
+      ps->job[st] = job;
+      ps->inv[st] = inv;
+      ps->seq[st] = n;
     }
-    if (!e.taps_resident && ptid == 0) {
+    if (job >= 0 && !e.taps_resident && ptid == 0) {
       const int nt = (c == nch - 1) ? mp.K_pad - c * KC : KC;
-      mbar_arrive_expect_tx(&ps->full[stage], (uint32_t)nt * 8u);
-      bulk_g2s(xs + stage_x, mp.kr + (size_t)c * KC, (uint32_t)nt * 8u, &ps->full[stage]);
+      double* xs = stg + (size_t)st * stage_words;
+      mbar_arrive_expect_tx(&ps->full[st], (uint32_t)nt * 8u);
+      bulk_g2s(xs + stage_x, mp.kr + (size_t)c * KC, (uint32_t)nt * 8u, &ps->full[st]);
     } else {
-      mbar_arrive(&ps->full[stage]);
+      mbar_arrive(&ps->full[st]);
     }
   };
 
-  // Pipeline fill: every warp helps compand and pack chunk 0 of the first job into stage 0.
-  if (tid == 0) ps->prod_job = (long long)(atomicAdd(e.counter, 1ULL) - e.base);
-  __syncthreads();
-  const long long job0 = ps->prod_job;
-  long long cur_blk = -1;
-  double c_s = 1.0, inv = 0.0;
-  if (job0 < njobs) {
-    JobPos jp;
-    Blk b;
-    const double* gsrc;
-    int n_valid;
-    job_block(job0, jp, b, gsrc, n_valid);
-    c_s = block_cs<PACK>(mp, gsrc, n_valid, ps, tid, blockDim.x, 0);
-    inv = dequant_scale(c_s, mp.c_k);
-    cur_blk = jp.sig * g.P + jp.w;
-    pack_window<PACK, T>(g, b, mp, gsrc, n_valid, c_s, jp.t * G * T - front * T, rows_s, stg, tid, blockDim.x);
+  // Pipeline fill: the first nf jobs (one per producer warp when a job is one stage) are
+  // claimed in parallel, then companded and packed by all warps, five warps per job.
+  const int nf = (nch == 1) ? min(kTiledProdWarps, NS) : 1;
+  const int lane_ = tid & 31, warp_ = tid >> 5;
+  if (warp_ < nf) {
+    const long long j = claim_job(e, njobs, lane_);
+    if (lane_ == 0) ps->fjob[warp_] = j;
   }
   __syncthreads();
-  if (tid < nprod) {
-    if (job0 < njobs) {
-      publish(0, 0, job0, c_s, inv, tid);
-    } else {
-      if (tid == 0) ps->job[0] = -1;
-      mbar_arrive(&ps->full[0]);
-    }
+  if (tid == 0) {                                    // successful claims first: no holes before M_end
+    int k = 0;
+    for (int q = 0; q < nf; ++q)
+      if (ps->fjob[q] >= 0) ps->fjob[k++] = ps->fjob[q];
+    for (int q = k; q < nf; ++q) ps->fjob[q] = -1;
+    ps->m_end = (k < nf) ? k : -1;
+    ps->turn = nf;
   }
-  if (job0 >= njobs) return;
-
-  if (tid < nprod) {
-    // ============================ producer warps ============================
-    const int ptid = tid;
-    int it = 1;
-    long long job = job0;
-    int c = 1;
-    for (;;) {
-      if (c == nch) {                                    // next job, claimed once a stage is free
-        c = 0;
-        mbar_wait(&ps->empty[it & 1], ((it >> 1) & 1) ^ 1);
-        named_bar(2, nprod);
-        if (ptid == 0) ps->prod_job = (long long)(atomicAdd(e.counter, 1ULL) - e.base);
-        named_bar(2, nprod);
-        job = ps->prod_job;
-        if (job >= njobs) {
-          if (ptid == 0) ps->job[it & 1] = -1;
-          mbar_arrive(&ps->full[it & 1]);
-          break;
-        }
-      } else {
-        mbar_wait(&ps->empty[it & 1], ((it >> 1) & 1) ^ 1);
-      }
+  __syncthreads();
+  {
+    constexpr int GW = (kTiledProdWarps + kTiledConsWarps) / 4;   // warps per fill group
+    const int gq = warp_ / GW, gtid = tid - gq * GW * 32;
+    for (int f = gq; f < nf; f += 4) {
+      const long long fj = ps->fjob[f];
+      if (fj < 0) break;
       JobPos jp;
       Blk b;
       const double* gsrc;
       int n_valid;
-      job_block(job, jp, b, gsrc, n_valid);
-      const long long blk_id = jp.sig * g.P + jp.w;
-      if (blk_id != cur_blk) {                          // peak reused across a block's tiles
-        cur_blk = blk_id;
-        c_s = block_cs<PACK>(mp, gsrc, n_valid, ps, ptid, nprod, 2);
-        inv = dequant_scale(c_s, mp.c_k);                // Eq. (16), once per block
+      job_block(fj, jp, b, gsrc, n_valid);
+      const double cs = block_cs<PACK>(mp, gsrc, n_valid, ps->red + 8 * gq, gtid, GW * 32, 1 + gq);
+      pack_window<PACK, T>(g, b, mp, gsrc, n_valid, cs, jp.t * G * T - front * T, rows_s,
+                           stg + (size_t)((f * nch) % NS) * stage_words, gtid, GW * 32);
+      if (gtid == 0) {
+        ps->fcs[f] = cs;
+        ps->finv[f] = dequant_scale(cs, mp.c_k);
       }
-      const int stage = it & 1;
-      pack_window<PACK, T>(g, b, mp, gsrc, n_valid, c_s, jp.t * G * T - front * T + c * KC, rows_s,
-                           stg + stage * stage_words, ptid, nprod);
-      publish(stage, c, job, c_s, inv, ptid);
-      ++c;
-      ++it;
+    }
+  }
+  __syncthreads();
+  if (e.dbg_timing && tid == 0)
+    e.dbg_timing[kTimCyc + 4 * blockIdx.x + 3] = gtimer() - e.dbg_timing[kTimCyc + 4 * blockIdx.x + 2];
+
+  if (tid < nprod) {
+    // ============================ producer warps ============================
+    // Job sequence m (its chunk c is stage sequence n = m * nch + c, slot n % NS) is produced
+    // by producer warp m % 4, so four jobs are companded and packed concurrently.  Claims are
+    // taken in sequence order (a turn counter), so the first failed claim M_end ends the real
+    // jobs; sequences M_end .. M_end + 16/npart - 1 are sentinels (job = -1), one for every
+    // consumer warp.  A slot is refilled only after its previous sequence was published and
+    // then released by the consumers.
+    const int pw = tid >> 5, lane = tid & 31;
+    const int n_sent = 16 / npart;
+    long long cur_blk_w = -1;
+    double c_s_w = 1.0, inv_w = 0.0;
+    int pj = 0;
+    for (long long m = pw;; m += kTiledProdWarps, ++pj) {
+      unsigned long long* prec = (e.dbg_timing && lane == 0 && pj < 16)
+                                     ? e.dbg_timing + kTimP + (((size_t)blockIdx.x * 4 + pw) * 16 + pj) * 4
+                                     : nullptr;
+      if (prec) {
+        prec[0] = (unsigned long long)m;
+        prec[1] = gtimer();
+      }
+      long long job;
+      bool prepacked = false;
+      if (m < nf) {
+        job = ps->fjob[m];
+        prepacked = job >= 0;
+        if (prepacked) {
+          const JobPos jq = job_pos(e, job);
+          cur_blk_w = jq.sig * g.P + jq.w;
+          c_s_w = ps->fcs[m];
+          inv_w = ps->finv[m];
+        }
+      } else {
+        long long j = -1;
+        if (lane == 0) {
+          while (*reinterpret_cast<volatile long long*>(&ps->turn) != m) __nanosleep(256);
+          const long long me = *reinterpret_cast<volatile long long*>(&ps->m_end);
+          j = (me >= 0) ? -1 : 0;
+        }
+        j = __shfl_sync(0xffffffffu, j, 0);
+        if (j == 0) j = claim_job(e, njobs, lane);
+        if (lane == 0) {
+          if (j < 0 && *reinterpret_cast<volatile long long*>(&ps->m_end) < 0)
+            *reinterpret_cast<volatile long long*>(&ps->m_end) = m;
+          __threadfence_block();
+          *reinterpret_cast<volatile long long*>(&ps->turn) = m + 1;
+        }
+        job = j;
+      }
+      if (prec) prec[2] = gtimer();
+      if (job < 0) {
+        long long me = 0;
+        if (lane == 0) me = *reinterpret_cast<volatile long long*>(&ps->m_end);
+        me = __shfl_sync(0xffffffffu, me, 0);
+        if (m >= me + n_sent) break;
+      }
+      JobPos jp;
+      Blk b;
+      const double* gsrc = nullptr;
+      int n_valid = 0;
+      if (job >= 0) {
+        job_block(job, jp, b, gsrc, n_valid);
+        const long long blk_id = jp.sig * g.P + jp.w;
+        if (blk_id != cur_blk_w) {
+          cur_blk_w = blk_id;
+          c_s_w = warp_cs<PACK>(mp, gsrc, n_valid, lane);   // a2/a3 (Eq. (2))
+          inv_w = dequant_scale(c_s_w, mp.c_k);              // Eq. (16), once per block
+        }
+      }
+      for (int c = 0; c < nch; ++c) {
+        const long long n = m * nch + c;
+        const int st = (int)(n % NS);
+        if (n >= NS) {
+          if (lane == 0)
+            while (*reinterpret_cast<volatile long long*>(&ps->seq[st]) != n - NS) __nanosleep(256);
+          __syncwarp();
+          mbar_wait_wd(&ps->empty[st], (uint32_t)(((n / NS) & 1) ^ 1), 1, n, st);
+        }
+        if (job >= 0 && !(prepacked && c == 0))
+          pack_window<PACK, T>(g, b, mp, gsrc, n_valid, c_s_w, jp.t * G * T - front * T + c * KC, rows_s,
+                               stg + (size_t)st * stage_words, lane, 32);
+        __syncwarp();
+        publish(n, st, c, job, inv_w, lane);
+      }
+      if (prec) prec[3] = gtimer();
+    }
+    if (tid == 0) {
+      // every producer warp has finished claiming once the turn passed all of them
+      retire_cta(e);
     }
     return;
   }
 
   // ============================ consumer warps ============================
+  // Warp-job k = (job sequence k / npart, part k % npart) runs on SMSP k % 4: the warps of
+  // SMSP s claim k = 4 c + s in order from their own counter, so every job's parts spread
+  // over the four schedulers and a finished warp takes the next part (no CTA-wide barrier).
   const int ctid = tid - nprod;
-  const int cwarp = ctid >> 5, lane = ctid & 31;
-  mbar_wait(&ps->bar_taps, 0);
-  int it = 0, njob = 0;
+  const int cw = ctid >> 5, lane = tid & 31;
+  const int smsp = (tid >> 5) & 3;
+  double* wbuf = wout + (size_t)cw * 32 * (T + 1);
+  mbar_wait_wd(&ps->bar_taps, 0, 4, 0, 0);
+  // A consumer warp may claim work up to 16 / npart jobs ahead of the producer, i.e. more than
+  // one ring lap: a parity wait could then see the slot's previous lap; the sequence number
+  // stamped by the producer tells the two apart.
+  auto wait_full = [&](long long n, int st) {
+    for (int spin = 0;; ++spin) {
+      mbar_wait_wd(&ps->full[st], (uint32_t)((n / NS) & 1), 2, n, st);
+      if (*reinterpret_cast<volatile long long*>(&ps->seq[st]) == n) return;
+      if (spin > 20000000) mbar_stuck(3, n, st, (uint32_t)*reinterpret_cast<volatile long long*>(&ps->seq[st]));
+      __nanosleep(200);
+    }
+  };
+  int njob = 0;
+#define PC_REC (e.dbg_timing != nullptr && ctid == 0)
+  if (PC_REC) ps->cyc[0] = ps->cyc[1] = ps->cyc[2] = 0;
   for (;; ++njob) {
-    int stage = it & 1;
-    mbar_wait(&ps->full[stage], (it >> 1) & 1);
-    const long long job = ps->job[stage];
-    if (job < 0) break;
-    const double inv = ps->inv[stage];
+    int cl = 0;
+    if (lane == 0) cl = atomicAdd(&ps->smsp_ctr[smsp], 1);
+    cl = __shfl_sync(0xffffffffu, cl, 0);
+    const long long k = 4LL * cl + smsp;
+    const long long mseq = k / npart;
+    const int part = (int)(k % npart);
+    long long n = mseq * nch;
+    int st = (int)(n % NS);
+    if (PC_REC) ps->cyc[3] = clock64();
+    wait_full(n, st);
+    const long long job = ps->job[st];
+    if (PC_REC) {
+      const long long c1 = clock64();
+      ps->cyc[0] += c1 - ps->cyc[3];
+      ps->cyc[3] = c1;
+    }
+    unsigned long long* wrec = (e.dbg_timing && lane == 0 && njob < 16)
+                                   ? e.dbg_timing + kTimW + (((size_t)blockIdx.x * 16 + cw) * 16 + njob) * 4
+                                   : nullptr;
+    if (wrec) {
+      wrec[0] = (unsigned long long)mseq;
+      wrec[1] = gtimer();
+    }
+    if (job < 0) {                                           // sentinel: release its stages, stop
+      for (int c = 0; c < nch; ++c, ++n) {
+        st = (int)(n % NS);
+        if (c > 0) wait_full(n, st);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ps->empty[st]);
+      }
+      break;
+    }
+    const double inv = ps->inv[st];
     const JobPos jp = job_pos(e, job);
     const Blk b = block_info<PACK>(g, mp.K, jp.w);
     const int ngroups = (b.M_out + T - 1) / T;
-    const int gl = ctid;                                     // this thread's group in the tile
+    const int gl = part * 32 + lane;                         // this thread's group in the tile
     const int gi = jp.t * G + gl;                            // group index within the block
-    const bool mine = gl < G && gi < ngroups;
-    const bool extra = (PACK == PACK_SYM) && jp.t > 0 && cwarp == 0;
+    const bool mine = gi < ngroups;
+    const int gi0 = jp.t * G + part * 32;                    // the warp's first group
+    const bool extra = (PACK == PACK_SYM) && gi0 > 0;        // needs B of the word before it
     double acc[T];
 #pragma unroll
     for (int i = 0; i < T; ++i) acc[i] = 0.0;
-    double px = 0.0;                                         // sym extra word partial (warp 0)
-    for (int c = 0; c < nch; ++c, ++it) {
-      stage = it & 1;
-      if (c > 0) mbar_wait(&ps->full[stage], (it >> 1) & 1);
-      const double* xs = stg + stage * stage_words;
+    double px = 0.0;                                         // sym: that word's core output (split)
+    for (int c = 0; c < nch; ++c, ++n) {
+      st = (int)(n % NS);
+      if (c > 0) wait_full(n, st);
+      const double* xs = stg + (size_t)st * stage_words;
       const double* kc = e.taps_resident ? kr_res + (size_t)c * KC : xs + stage_x;
       const int nt = (c == nch - 1) ? mp.K_pad - c * KC : KC;
       if (mine) conv_chunk_padded<T>(smem_u32(xs) + 8u * (T + 1) * (gl + front), smem_u32(kc), nt, acc);   // a5
       if (extra) {
+        const int i0 = part * 32 * T + T - 1;                // local word of core word gi0*T - 1
         for (int j = lane; j < nt; j += 32) {
-          const int i = T - 1 + j;                           // local word of core word m_lo-1+j
+          const int i = i0 + j;
           px = fma(xs[(i / T) * (T + 1) + i % T], kc[j], px);
         }
       }
-      mbar_arrive(&ps->empty[stage]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ps->empty[st]);
     }
-    // ---- a6/a7: unpack, inverse-compand, discard and place (Eqs. (11)-(17))
-    double* __restrict__ r = e.r + jp.sig * e.r_stride;
+    if (wrec) wrec[2] = gtimer();
+    if (PC_REC) {
+      const long long c1 = clock64();
+      ps->cyc[1] += c1 - ps->cyc[3];
+      ps->cyc[3] = c1;
+      if (njob < 16) e.dbg_timing[kTimTr + 16 * blockIdx.x + njob] = gtimer();
+    }
+    // ---- a6/a7: unpack, inverse-compand, discard and place (Eqs. (11)-(17)).  Each warp
+    // decodes into its own staging rows (pitch T+1, conflict-free) and writes them out in
+    // order, 32 consecutive outputs per store; the valid outputs of a run are one contiguous
+    // range, computed once (Eq. (17) placement, the L+N-1 trim, xcorr's valid lags).
     const long long gbase = b.g0 + b.o0;
-    const long long L_conv = g.L + g.N - 1;
-    auto store = [&](int k, double val) {
-      const long long gg = gbase + k;
-      if (g.mode == 0) {
-        if (gg < L_conv) r[gg - e.r_off] = val;
-      } else {
-        const long long j = gg - (g.N - 1);                  // valid lag (C17)
-        if (j >= 0 && j <= g.L - g.N) r[j - e.r_off] = val;
+    const long long goff = (g.mode == 0) ? 0 : (long long)(g.N - 1);     // xcorr: lag = gg - (N-1)
+    const long long g_lo = goff, g_hi = (g.mode == 0) ? g.L + g.N - 1 : g.L;   // valid gg
+    double* __restrict__ rsig = e.r + jp.sig * e.r_stride - e.r_off - goff;    // rsig[gg]
+    const int mw = gi0 * T;                                  // first core output of the warp
+    double* row = wbuf + lane * (T + 1);
+    auto flush = [&](double* dst, int step, long long jlo, long long jhi) {
+      __syncwarp();
+#pragma unroll
+      for (int it = 0; it < T; ++it) {
+        const int j = lane + 32 * it;
+        if (j >= jlo && j < jhi) dst[(long long)step * j] = wbuf[(j / T) * (T + 1) + j % T];
       }
+      __syncwarp();
     };
-    const int moff = (jp.w == 0) ? 0 : 1;
     if (PACK == PACK_SYM) {
-      double* cfirst = fix + (njob & 1) * 2 * (G + 1);
-      double* blast = cfirst + (G + 1) + 1;                   // blast[-1] = B of the extra word
-      if (extra) {
-        for (int o = 16; o > 0; o >>= 1) px += __shfl_xor_sync(0xffffffffu, px, o);
-        if (lane == 0) blast[-1] = decode_sym(px, mp.eps, mp.eps_inv, mp.pow2).B;
-      }
-      if (mine) {
-        double Bprev = 0.0;
-#pragma unroll
-        for (int i = 0; i < T; ++i) {
-          const int m = gi * T + i;
-          const Digits3 d = decode_sym(acc[i], mp.eps, mp.eps_inv, mp.pow2);
-          if (m < b.M_out && m >= moff) {
-            const int k = 2 * (m - moff);
-            store(k + 1, __dmul_rn(d.A, inv));
-            if (i > 0 || m == 0) {
-              store(k, __dmul_rn(d.C + Bprev, inv));
-            } else {
-              cfirst[gl] = d.C;                              // needs B of the previous word
-            }
-          }
-          Bprev = d.B;
-        }
-        blast[gl] = Bprev;
-      }
-      named_bar(1, ncons);
-      if (mine) {
-        const int m = gi * T;
-        if (m < b.M_out && m >= moff && m > 0) store(2 * (m - moff), __dmul_rn(cfirst[gl] + blast[gl - 1], inv));
-      }
-    } else if (PACK == PACK_ASYM2 || PACK == PACK_ASYM3) {
-      if (mine) {
-        constexpr int M = (PACK == PACK_ASYM2) ? 2 : 3;
-#pragma unroll
-        for (int i = 0; i < T; ++i) {
-          const int m = gi * T + i;
-          if (m < b.S) {
-            double v = acc[i];
-#pragma unroll
-            for (int q = 0; q < M; ++q) {                     // balanced digits (C9)
-              const double t = rint_fast(v);
-              if (q < M - 1) v = __dmul_rn(__dsub_rn(v, t), mp.eps_inv);
-              const int k = q * b.S + m;
-              if (k < b.n_out) store(k, __dmul_rn(t, inv));
-            }
-          }
-        }
-      }
-    } else if (mine) {
+      const int moff = (jp.w == 0) ? 0 : 1;
+      for (int o = 16; o > 0; o >>= 1) px += __shfl_xor_sync(0xffffffffu, px, o);
+      const double Bw = extra ? decode_sym(px, mp.eps, mp.eps_inv, mp.pow2).B : 0.0;
+      const double Blast = decode_sym(acc[T - 1], mp.eps, mp.eps_inv, mp.pow2).B;
+      const double Bup = __shfl_up_sync(0xffffffffu, Blast, 1);
+      double Bprev = (lane == 0) ? Bw : Bup;                 // B of the word before the group
 #pragma unroll
       for (int i = 0; i < T; ++i) {
-        const int m = gi * T + i;
-        if (m < b.n_out) store(m, acc[i]);
+        const Digits3 d = decode_sym(acc[i], mp.eps, mp.eps_inv, mp.pow2);
+        row[i] = __dmul_rn(d.C + Bprev, inv);                // r~[2m] = C[m] + B[m-1] (Eqs. (12)-(14))
+        acc[i] = d.A;                                        // r~[2m+1] = A[m] (Eq. (15))
+        Bprev = d.B;
+      }
+      for (int par = 0; par < 2; ++par) {
+        if (par == 1) {
+#pragma unroll
+          for (int i = 0; i < T; ++i) row[i] = __dmul_rn(acc[i], inv);
+        }
+        // output k = 2 (m - moff) + par of core output m = mw + j, gg = gbase + k
+        const long long x0 = (long long)mw - moff;
+        long long jlo = moff - (long long)mw, jhi = (long long)b.M_out - mw;
+        jlo = max(jlo, fdiv_ceil(g_lo - gbase - par, 2) - x0);
+        jhi = min(jhi, fdiv_floor(g_hi - 1 - gbase - par, 2) + 1 - x0);
+        flush(rsig + gbase + par + 2 * x0, 2, max(jlo, 0LL), min(jhi, (long long)(32 * T)));
+      }
+    } else {
+      constexpr int M = (PACK == PACK_ASYM2) ? 2 : (PACK == PACK_ASYM3 ? 3 : 1);
+      const int seg = (PACK == PACK_FULL) ? b.n_out : b.S;   // outputs per digit segment
+#pragma unroll 1
+      for (int q = 0; q < M; ++q) {
+#pragma unroll
+        for (int i = 0; i < T; ++i) {
+          if (PACK == PACK_FULL) {
+            row[i] = acc[i];
+          } else {                                           // balanced digits (C9)
+            const double t = rint_fast(acc[i]);
+            row[i] = __dmul_rn(t, inv);
+            if (q < M - 1) acc[i] = __dmul_rn(__dsub_rn(acc[i], t), mp.eps_inv);
+          }
+        }
+        const long long k0 = (long long)q * seg + mw;          // output k = k0 + j
+        long long jhi = min((long long)seg - mw, (long long)b.n_out - k0);
+        jhi = min(jhi, g_hi - gbase - k0);
+        const long long jlo = max(0LL, g_lo - gbase - k0);
+        flush(rsig + gbase + k0, 1, jlo, min(jhi, (long long)(32 * T)));
       }
     }
+    if (wrec) wrec[3] = gtimer();
+    if (PC_REC) ps->cyc[2] += clock64() - ps->cyc[3];
   }
+  if (PC_REC) {
+    unsigned long long* tim = e.dbg_timing;
+    tim[4 * blockIdx.x + 0] = smid_();
+    tim[4 * blockIdx.x + 1] = tim[kTimCyc + 4 * blockIdx.x + 2];   // t_start (stashed)
+    tim[4 * blockIdx.x + 2] = gtimer();
+    tim[4 * blockIdx.x + 3] = njob;
+    tim[kTimCyc + 4 * blockIdx.x + 0] = ps->cyc[0];
+    tim[kTimCyc + 4 * blockIdx.x + 1] = ps->cyc[1];
+    tim[kTimCyc + 4 * blockIdx.x + 2] = ps->cyc[2];
+  }
+#undef PC_REC
 }
 
 // ------------------------------------------------------------------ launcher
@@ -445,8 +743,10 @@ static cudaError_t launch_tiled_t(const Geo& g, const Exec& e, long long n_jobs,
     c_dev = dev;
     c_grid = c_sms * occ;
   }
-  long long grid = c_grid;
-  if (e.max_ctas_per_sm > 0 && (long long)e.max_ctas_per_sm * c_sms < grid) grid = (long long)e.max_ctas_per_sm * c_sms;
+  if (c_sms > kCtrDone) return cudaErrorInvalidConfiguration;
+  Exec ex = e;
+  ex.nsm = c_sms;
+  long long grid = c_sms;                            // one persistent CTA per SM (smem >= half an SM)
   if (grid > n_jobs) grid = n_jobs;
   *grid_out = (int)grid;
   cudaLaunchConfig_t cfg = {};
@@ -459,7 +759,7 @@ static cudaError_t launch_tiled_t(const Geo& g, const Exec& e, long long n_jobs,
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kfn, g, e);
+  return cudaLaunchKernelEx(&cfg, kfn, g, ex);
 }
 
 template <int T>
