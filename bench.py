@@ -69,6 +69,8 @@ def parse():
     ap.add_argument("--signals", type=int, default=0, help="cfg4: database signals in total (default 1024)")
     ap.add_argument("--force-warps", type=int, default=0, help="diagnostics: consumer warps per CTA")
     ap.add_argument("--opt", action="append", default=[], help="diagnostics: conv_opts.reserved[i]=v as i=v")
+    ap.add_argument("--graph", type=int, default=-1,
+                    help="1: capture the K timed steps in one CUDA graph (default: on for cfg1, launch-bound)")
     return ap.parse_args()
 
 
@@ -294,6 +296,19 @@ def run_ours(args, ws, rank, local):
         torch.cuda.synchronize(dev)
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        use_graph = (args.graph == 1) or (args.graph == -1 and args.workload == "cfg1")
+        graph = None
+        if use_graph:                                # K steps replayed as one graph (no host launch gaps)
+            gs = torch.cuda.Stream(dev)
+            gs.wait_stream(stream)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(gs):
+                with torch.cuda.graph(graph, stream=gs):
+                    for i in range(args.steps):
+                        step(i)
+            stream.wait_stream(gs)
+            graph.replay()
+            torch.cuda.synchronize(dev)
         sampler = ClockSampler(local) if name == head else None
         if sampler:
             sampler.__enter__()
@@ -301,10 +316,13 @@ def run_ours(args, ws, rank, local):
         barrier(ws)
         torch.cuda.synchronize(dev)
         t0.record(stream)
-        for i in range(args.steps):
-            ev[i][0].record(stream)
-            step(i)
-            ev[i][1].record(stream)
+        if graph is not None:
+            graph.replay()
+        else:
+            for i in range(args.steps):
+                ev[i][0].record(stream)
+                step(i)
+                ev[i][1].record(stream)
         t1.record(stream)
         torch.cuda.synchronize(dev)
         barrier(ws)
@@ -324,12 +342,13 @@ def run_ours(args, ws, rank, local):
             sampler.__exit__()
             sampler_summary = sampler.summary()
         ms = max_over_ranks(t0.elapsed_time(t1), ws)
-        kern_ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+        kern_ms = (t0.elapsed_time(t1) / args.steps) if graph is not None else \
+            float(np.mean([a.elapsed_time(b) for a, b in ev]))
         fma = core_fma(info, packing if not adaptive else FULL) * nsig
         rec = {"ms_per_step": ms / args.steps, "kernel_ms": kern_ms,
                "value": ws * L_out * nsig * args.steps / (ms / 1e3), "R_max": info["R_max"], "Q": Q,
                "bound_ok": info["bound_ok"], "tile": info["core_tile"], "fft_n": info["fft_n"],
-               "core": "fft" if core == FFT else "direct"}
+               "core": "fft" if core == FFT else "direct", "cuda_graph": graph is not None}
         if core == DIRECT and not adaptive:
             rec["fp64_tflops"] = 2.0 * fma / (kern_ms / 1e3) / 1e12
             rec["fma_per_output"] = fma / (L_out * nsig)

@@ -60,6 +60,8 @@ struct conv_plan {
   // host end-to-end staging
   double* d_in = nullptr;
   double* d_out = nullptr;
+  cudaStream_t st_h2d = nullptr, st_d2h = nullptr;   // conv_execute_host pipeline (plan-owned)
+  cudaEvent_t ev_in[16] = {}, ev_done[16] = {}, ev_out = nullptr;
   // xcorr scratch
   double* d_xc = nullptr;
   size_t d_xc_bytes = 0;
@@ -576,6 +578,13 @@ void conv_plan_destroy(conv_plan* p) {
   cudaFree(p->d_cand);
   cudaFree(p->d_in);
   cudaFree(p->d_out);
+  for (int i = 0; i < 16; ++i) {
+    if (p->ev_in[i]) cudaEventDestroy(p->ev_in[i]);
+    if (p->ev_done[i]) cudaEventDestroy(p->ev_done[i]);
+  }
+  if (p->ev_out) cudaEventDestroy(p->ev_out);
+  if (p->st_h2d) cudaStreamDestroy(p->st_h2d);
+  if (p->st_d2h) cudaStreamDestroy(p->st_d2h);
   cudaFree(p->d_xc);
   cudaFree(p->d_counter);
   cudaFree(p->d_tw);
@@ -758,12 +767,77 @@ int conv_execute_host(conv_plan* p, const double* s_host, double* r_host, void* 
   const long long L_out = p->mode == PC_MODE_XCORR ? p->L - p->N + 1 : p->L + p->N - 1;
   if (!p->d_in && cudaMalloc(&p->d_in, sizeof(double) * p->L) != cudaSuccess) return PC_E_CUDA;
   if (!p->d_out && cudaMalloc(&p->d_out, sizeof(double) * L_out) != cudaSuccess) return PC_E_CUDA;
-  if (cudaMemcpyAsync(p->d_in, s_host, sizeof(double) * p->L, cudaMemcpyHostToDevice, st) != cudaSuccess)
-    return PC_E_CUDA;
-  int rc = run_exec(p, p->d_in, 0, 0, p->d_out, 0, 0, 0, p->P, 1, nullptr, st);
-  if (rc) return rc;
-  if (cudaMemcpyAsync(r_host, p->d_out, sizeof(double) * L_out, cudaMemcpyDeviceToHost, st) != cudaSuccess)
-    return PC_E_CUDA;
+  // Adaptive plans (decisions belong to one device input) and small plans: one pass.
+  // Chunk weights: small first and last ranges shorten the pipeline ramp (the first H2D and
+  // the last D2H are not overlapped).
+  static const int kW[9] = {1, 2, 4, 4, 4, 4, 4, 2, 1};
+  const int nchunk = (p->packing == PC_PACK_ADAPTIVE || p->P < 128) ? 1 : 9;
+  long long cum[10] = {0};
+  for (int i = 0; i < 9; ++i) cum[i + 1] = cum[i] + kW[i];
+  if (nchunk <= 1) {
+    if (cudaMemcpyAsync(p->d_in, s_host, sizeof(double) * p->L, cudaMemcpyHostToDevice, st) != cudaSuccess)
+      return PC_E_CUDA;
+    int rc = run_exec(p, p->d_in, 0, 0, p->d_out, 0, 0, 0, p->P, 1, nullptr, st);
+    if (rc) return rc;
+    if (cudaMemcpyAsync(r_host, p->d_out, sizeof(double) * L_out, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+      return PC_E_CUDA;
+    return cuda_status(cudaStreamSynchronize(st));
+  }
+  // Pipeline over block ranges: the H2D of chunk c+1, the core of chunk c and the D2H of
+  // chunk c-1 overlap (two copy engines + the SMs).  Each input sample and each output is
+  // copied once; block ranges, halos and output ranges follow Eq. (17) (reading C7).
+  if (!p->st_h2d) {
+    if (cudaStreamCreateWithFlags(&p->st_h2d, cudaStreamNonBlocking) != cudaSuccess) return PC_E_CUDA;
+    if (cudaStreamCreateWithFlags(&p->st_d2h, cudaStreamNonBlocking) != cudaSuccess) return PC_E_CUDA;
+    for (int i = 0; i < 16; ++i) {
+      if (cudaEventCreateWithFlags(&p->ev_in[i], cudaEventDisableTiming) != cudaSuccess) return PC_E_CUDA;
+      if (cudaEventCreateWithFlags(&p->ev_done[i], cudaEventDisableTiming) != cudaSuccess) return PC_E_CUDA;
+    }
+    if (cudaEventCreateWithFlags(&p->ev_out, cudaEventDisableTiming) != cudaSuccess) return PC_E_CUDA;
+  }
+  cudaError_t e = cudaEventRecord(p->ev_out, st);                    // stream order before the call
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(p->st_h2d, p->ev_out, 0);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(p->st_d2h, p->ev_out, 0);
+  if (e != cudaSuccess) return PC_E_CUDA;
+  const long long W = p->W, Wb = p->W_block, Np = p->Np;
+  long long in_done = 0, out_done = 0;
+  for (int c = 0; c < nchunk; ++c) {
+    const long long b0 = p->P * cum[c] / cum[9], b1 = p->P * cum[c + 1] / cum[9];
+    if (b1 <= b0) continue;
+    const long long last = b1 - 1;
+    long long in_end = (last == 0 ? 0 : last * W - 2) + Wb;            // block `last` reads up to here
+    if (in_end > p->L) in_end = p->L;
+    if (c == nchunk - 1) in_end = p->L;
+    long long out_end = (b1 == p->P) ? p->L + p->N - 1 : Np - 1 + b1 * W;   // conv outputs of blocks < b1
+    if (p->mode == PC_MODE_XCORR) {
+      out_end -= p->N - 1;                                              // lags j = gg - (N-1)
+      if (out_end > L_out) out_end = L_out;
+      if (out_end < 0) out_end = 0;
+    } else if (out_end > L_out) {
+      out_end = L_out;
+    }
+    if (in_end > in_done) {
+      e = cudaMemcpyAsync(p->d_in + in_done, s_host + in_done, sizeof(double) * (in_end - in_done),
+                          cudaMemcpyHostToDevice, p->st_h2d);
+      if (e != cudaSuccess) return PC_E_CUDA;
+      in_done = in_end;
+    }
+    if ((e = cudaEventRecord(p->ev_in[c], p->st_h2d)) != cudaSuccess) return PC_E_CUDA;
+    if ((e = cudaStreamWaitEvent(st, p->ev_in[c], 0)) != cudaSuccess) return PC_E_CUDA;
+    const int rc = run_exec(p, p->d_in, 0, 0, p->d_out, 0, 0, b0, b1 - b0, 1, nullptr, st);
+    if (rc) return rc;
+    if ((e = cudaEventRecord(p->ev_done[c], st)) != cudaSuccess) return PC_E_CUDA;
+    if ((e = cudaStreamWaitEvent(p->st_d2h, p->ev_done[c], 0)) != cudaSuccess) return PC_E_CUDA;
+    if (out_end > out_done) {
+      e = cudaMemcpyAsync(r_host + out_done, p->d_out + out_done, sizeof(double) * (out_end - out_done),
+                          cudaMemcpyDeviceToHost, p->st_d2h);
+      if (e != cudaSuccess) return PC_E_CUDA;
+      out_done = out_end;
+    }
+  }
+  if (out_done != L_out) return PC_E_CONFIG;   // geometry bug guard
+  if ((e = cudaEventRecord(p->ev_out, p->st_d2h)) != cudaSuccess) return PC_E_CUDA;
+  if ((e = cudaStreamWaitEvent(st, p->ev_out, 0)) != cudaSuccess) return PC_E_CUDA;
   return cuda_status(cudaStreamSynchronize(st));
 }
 

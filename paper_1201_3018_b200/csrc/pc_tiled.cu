@@ -264,17 +264,19 @@ constexpr int kTimCyc = 4 * 148 * 32, kTimTr = 8 * 148 * 32;
 constexpr int kTimW = 24 * 148 * 32, kTimP = kTimW + 148 * 16 * 16 * 4;
 // total: kTimP + 148 * 4 * 16 * 4 uint64 entries
 
-// Job claim (one full warp).  Per-SM queues balance the FP64 work across SMs: SM s owns jobs
-// [J s / nsm, J (s+1) / nsm) and the CTAs resident on it share that queue; a CTA whose queue
-// is empty steals from the others (warp-parallel scan), so every job runs even if some SM
-// hosts no CTA.  Returns -1 when no job is left anywhere.
+// Job claim (one full warp).  Job queues balance the FP64 work across SMs: with nq queues
+// (nq = nsm when every SM gets >= 8 jobs, fewer for small launches), queue q owns jobs
+// [J q / nq, J (q+1) / nq) and SM s serves queue s % nq; a CTA whose queue is empty steals
+// from the others (warp-parallel scan), so every job runs even if some SM hosts no CTA.
+// Returns -1 when no job is left anywhere.
 __device__ __forceinline__ long long claim_job(const Exec& e, long long njobs, int lane) {
   unsigned* ctr = e.sm_ctr;
-  const int nsm = e.nsm;
-  const int s = (int)(smid_() % (unsigned)nsm);
+  const long long nq_ = njobs / 8;
+  const int nq = (int)(nq_ < 1 ? 1 : (nq_ > e.nsm ? e.nsm : nq_));
+  const int s = (int)(smid_() % (unsigned)nq);
   long long job = -1;
   if (lane == 0) {
-    const long long lo = njobs * s / nsm, hi = njobs * (s + 1) / nsm;
+    const long long lo = njobs * s / nq, hi = njobs * (s + 1) / nq;
     if (lo < hi) {
       const unsigned n = atomicAdd(ctr + s, 1u);
       if (lo + n < hi) job = lo + n;
@@ -282,10 +284,10 @@ __device__ __forceinline__ long long claim_job(const Exec& e, long long njobs, i
   }
   job = __shfl_sync(0xffffffffu, job, 0);
   if (job >= 0) return job;
-  for (int base = 1; base < nsm; base += 32) {
-    const int t = (s + base + lane) % nsm;
-    const long long lo = njobs * t / nsm, hi = njobs * (t + 1) / nsm;
-    const bool has = (base + lane < nsm) && lo + (long long)*(volatile unsigned*)(ctr + t) < hi;
+  for (int base = 1; base < nq; base += 32) {
+    const int t = (s + base + lane) % nq;
+    const long long lo = njobs * t / nq, hi = njobs * (t + 1) / nq;
+    const bool has = (base + lane < nq) && lo + (long long)*(volatile unsigned*)(ctr + t) < hi;
     unsigned mask = __ballot_sync(0xffffffffu, has);
     while (mask) {
       const int l = __ffs(mask) - 1;
@@ -438,9 +440,15 @@ __global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec 
       const double* gsrc;
       int n_valid;
       job_block(fj, jp, b, gsrc, n_valid);
+      unsigned long long* frec = (e.dbg_timing && gtid == 0 && f < 4)
+                                     ? e.dbg_timing + kTimP + (((size_t)blockIdx.x * 4 + f) * 16 + 15) * 4
+                                     : nullptr;
+      if (frec) frec[0] = gtimer();
       const double cs = block_cs<PACK>(mp, gsrc, n_valid, ps->red + 8 * gq, gtid, GW * 32, 1 + gq);
+      if (frec) frec[1] = gtimer();
       pack_window<PACK, T>(g, b, mp, gsrc, n_valid, cs, jp.t * G * T - front * T, rows_s,
                            stg + (size_t)((f * nch) % NS) * stage_words, gtid, GW * 32);
+      if (frec) frec[2] = gtimer();
       if (gtid == 0) {
         ps->fcs[f] = cs;
         ps->finv[f] = dequant_scale(cs, mp.c_k);

@@ -510,3 +510,36 @@ def test_cfg3_full_size_fft_sampled():
     sel = ~np.isnan(ref.out)
     assert rc == pcb.PC_OK and res < 0.25
     assert np.array_equal(got[sel], ref.out[sel])
+
+
+@pytest.mark.parametrize("mode", [O.CONV, O.XCORR])
+@pytest.mark.parametrize("packing", [O.FULL, O.SYM, O.ASYM2])
+def test_execute_host_pipelined(mode, packing):
+    """conv_execute_host over >= 128 blocks pipelines block ranges across copy streams;
+    the result must equal the device-resident conv_execute bit for bit (same kernels,
+    same block geometry, each output written once)."""
+    rng = np.random.default_rng(7)
+    L, N, W_block, Q = 600_001, 65, 1024, 127      # P = 627 blocks, ragged tail
+    s = np.clip(rng.laplace(0.0, 0.2, L), -1.0, 1.0)
+    k = rng.uniform(-1.0, 1.0, N)
+    pk = {O.FULL: pcb.PACK_FULL, O.SYM: pcb.PACK_SYM, O.ASYM2: pcb.PACK_ASYM2}[packing]
+    with pcb.Plan(L, N, W_block, pcb.MODE_XCORR if mode == O.XCORR else pcb.MODE_CONV, pk,
+                  0 if packing == O.FULL else (31 if packing == O.SYM else Q),
+                  rmax_rule=pcb.RMAX_L1) as p:
+        p.set_kernel(dev(k))
+        info = p.info()
+        assert info["P"] >= 512
+        r_dev = torch.empty(info["L_out"], dtype=torch.float64, device=DEV)
+        p.execute(dev(s), r_dev)
+        torch.cuda.synchronize()
+        ref = r_dev.cpu().numpy()
+        sh = torch.from_numpy(s).pin_memory()
+        rh = torch.full((info["L_out"],), float("nan"), dtype=torch.float64).pin_memory()
+        p.execute_host(sh, rh)
+        assert np.array_equal(rh.numpy(), ref)
+        rh2 = torch.full((info["L_out"],), float("nan"), dtype=torch.float64)   # pageable host memory
+        p.execute_host(torch.from_numpy(s.copy()), rh2)
+        assert np.array_equal(rh2.numpy(), ref)
+    if packing == O.FULL and mode == O.CONV:
+        full = O.full_precision(s, k)
+        assert float(np.max(np.abs(ref - full)) / np.max(np.abs(full))) < 1e-12

@@ -83,7 +83,9 @@ for name, (pk, Q, rm) in points.items():
         cons = [[w, int(W[c, w, j, 0]), round((W[c, w, j, 1] - t0) / 1e3, 1), round((W[c, w, j, 2] - t0) / 1e3, 1),
                  round((W[c, w, j, 3] - t0) / 1e3, 1)] for w in range(16) for j in range(16) if W[c, w, j, 1]]
         return {"produced[mseq,t_pub]": sorted(prod), "consumed[warp,mseq,t_ready,t_core,t_stored]": sorted(cons, key=lambda x: x[2])}
-    out[name] = {"smsp_warps_in_core_time_frac": hist_core, "cta0": cta_trace(0), "grid": g, "tile": info["core_tile"], "kernel_us": float(T_end),
+    fill_phases = (Pr[:, :, 15, :3].astype(float) - r[:, 1][:, None, None]) / 1e3   # claimed, peak, packed (us)
+    fill_stats = {k: round(float(np.median(fill_phases[:, :, i])), 2) for i, k in enumerate(["claimed", "peak", "packed"])}
+    out[name] = {"fill_phases_us_median": fill_stats, "smsp_warps_in_core_time_frac": hist_core, "cta0": cta_trace(0), "grid": g, "tile": info["core_tile"], "kernel_us": float(T_end),
                  "start_spread_us": float(st.max()), "sm_end_min_us": float(sm_end.min()),
                  "sm_end_median_us": float(np.median(sm_end)), "sm_end_max_us": float(sm_end.max()),
                  "resident_ctas_per_sm_time_frac": hist,
