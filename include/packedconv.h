@@ -69,8 +69,9 @@ typedef struct conv_opts {
   int32_t device;           /* CUDA device ordinal, -1 = current device                    */
   int32_t reserved[9];      /* [0]: raw-block staging 0 auto/1 on/2 off (per-block kernel);
                                [1]: force the persistent core tile (12/14/16; tests);
-                               [2]: cap persistent CTAs per SM (diagnostics);
-                               [3]: force consumer warps per CTA (2..4; diagnostics); rest 0 */
+                               [2]: unused;
+                               [3]: force consumer warps per job (1, 2, 4; diagnostics);
+                               [4]: force the FFT size N (complex points, 1024..8192); rest 0 */
   double u_sys;             /* P:153; used only by the literal paper unpack form          */
 } conv_opts;
 

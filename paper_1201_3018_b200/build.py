@@ -11,7 +11,8 @@ DEPS = SOURCES + [os.path.join(HERE, "csrc", f) for f in ("pc_device.cuh", "pc_k
     [os.path.join(ROOT, "include", "packedconv.h")]
 OUT = os.path.join(HERE, "libpackedconv.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+EXTRA = os.environ.get("PC_NVCC_EXTRA", "").split()
+FLAGS = EXTRA + ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v", "-cudart", "static"]
 
 

@@ -292,14 +292,28 @@ bool fft_shape(const conv_plan* p, int packing, int N, FShape* f) {
   f->parts1 = parts(m1);
   return true;
 }
-// smallest N (complex points, 1024..8192) whose first part holds a typical block
+// FFT size N (complex points, 1024..8192) minimizing the modelled time of a typical block:
+// parts x (transform work N log2 N + the block's sample loads 3 W_block), divided by the
+// CTAs an SM overlaps (1.4x effective for N <= 4096, two CTAs per SM; measured on cfg3).
 int choose_fft_N(const conv_plan* p, int packing) {
   int mmax, mtyp;
   core_sizes(p, packing, &mmax, &mtyp);
   const int K = core_taps(p, packing);
-  for (int N = 1024; N <= 8192; N *= 2)
-    if (2 * N - K + 1 >= mtyp) return N;
-  return 2 * 8192 - K >= 1 ? 8192 : 0;
+  const int force = p->opts.reserved[4];            // diagnostics: complex points N
+  if (force == 1024 || force == 2048 || force == 4096 || force == 8192) return 2 * force - K >= 1 ? force : 0;
+  int best_N = 0;
+  double best = 0.0;
+  for (int N = 1024, lg = 10; N <= 8192; N *= 2, ++lg) {
+    const int part_out = 2 * N - K;
+    if (part_out < 1) continue;
+    const long long parts = mtyp <= part_out + 1 ? 1 : 1 + (mtyp - (part_out + 1) + part_out - 1) / part_out;
+    const double cost = (double)parts * ((double)N * lg + 3.0 * p->W_block) / (N <= 4096 ? 1.4 : 1.0);
+    if (best_N == 0 || cost < best) {
+      best = cost;
+      best_N = N;
+    }
+  }
+  return best_N;
 }
 
 int cuda_status(cudaError_t e) { return e == cudaSuccess ? PC_OK : PC_E_CUDA; }

@@ -128,16 +128,29 @@ __device__ __forceinline__ void stockham16(double2* s, const double2* __restrict
   const int j = threadIdx.x;
   const int k = j & (LS - 1);
   double2 v[16];
+#ifndef PC_FFT_TW_AFTER
+  double2 w[16];
+  if (LS > 1) {                                 // twiddle loads in flight across the barrier
+    const int step = k * (N / (LS * 16));
+#pragma unroll
+    for (int p = 1; p < 16; ++p) w[p] = __ldg(tw + p * step);
+  }
+#endif
 #pragma unroll
   for (int p = 0; p < 16; ++p) v[p] = s[pidx(j + p * NB)];
   __syncthreads();
   if (LS > 1) {
+#ifdef PC_FFT_TW_AFTER
+    double2 w[16];
     const int step = k * (N / (LS * 16));
 #pragma unroll
+    for (int p = 1; p < 16; ++p) w[p] = __ldg(tw + p * step);
+#endif
+#pragma unroll
     for (int p = 1; p < 16; ++p) {
-      double2 w = __ldg(tw + p * step);
-      if (SIGN > 0) w.y = -w.y;
-      v[p] = cmul(v[p], w);
+      double2 wp = w[p];
+      if (SIGN > 0) wp.y = -wp.y;
+      v[p] = cmul(v[p], wp);
     }
   }
   dft16<SIGN>(v);
@@ -262,7 +275,7 @@ __global__ void __launch_bounds__(N / 16) pc_fft_spectrum(const double* __restri
 
 // ------------------------------------------------------------------ the FFT-core conv kernel
 template <int PACK, int N>
-__global__ void __launch_bounds__(N / 16, 1) pc_fft_conv_kernel(Geo g, Exec e, FftArgs f) {
+__global__ void __launch_bounds__(N / 16, (N <= 4096 ? 2 : 1)) pc_fft_conv_kernel(Geo g, Exec e, FftArgs f) {
   extern __shared__ __align__(16) double2 sm[];
   __shared__ double red[32];
   __shared__ double bx[2];
@@ -289,8 +302,33 @@ __global__ void __launch_bounds__(N / 16, 1) pc_fft_conv_kernel(Geo g, Exec e, F
   // a2/a3: block peak and c_s (Eq. (2))
   double c_s = 1.0;
   if (PACK != PACK_FULL) {
-    double m = 0.0;
-    for (int i = tid; i < n_valid; i += nt) m = fmax(m, fabs(__ldg(gsrc + i)));
+    constexpr int U = 8;                          // 8 loads in flight per thread
+    double mu[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) mu[u] = 0.0;
+    if ((reinterpret_cast<uintptr_t>(gsrc) & 15u) == 0) {
+      const double2* g2 = reinterpret_cast<const double2*>(gsrc);
+      const int n2 = n_valid / 2;
+      for (int i0 = tid; i0 < n2; i0 += U * nt) {
+        double2 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = (i0 + u * nt < n2) ? __ldg(g2 + i0 + u * nt) : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int u = 0; u < U; ++u) mu[u] = fmax(mu[u], fmax(fabs(v[u].x), fabs(v[u].y)));
+      }
+      if ((n_valid & 1) && tid == 0) mu[0] = fmax(mu[0], fabs(gsrc[n_valid - 1]));
+    } else {
+      for (int i0 = tid; i0 < n_valid; i0 += U * nt) {
+        double v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = (i0 + u * nt < n_valid) ? __ldg(gsrc + i0 + u * nt) : 0.0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) mu[u] = fmax(mu[u], fabs(v[u]));
+      }
+    }
+    double m = mu[0];
+#pragma unroll
+    for (int u = 1; u < U; ++u) m = fmax(m, mu[u]);
     for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
     if ((tid & 31) == 0) red[tid >> 5] = m;
     __syncthreads();
@@ -323,9 +361,52 @@ __global__ void __launch_bounds__(N / 16, 1) pc_fft_conv_kernel(Geo g, Exec e, F
   };
   // window of 2N real words (outputs need cw0 .. cw0 + (m_hi-m_lo+front) + K - 2)
   const int wlen = (m_hi - m_lo + front) + mp.K - 1;
-  for (int n = tid; n < N; n += nt) {
-    const int a = 2 * n, c = 2 * n + 1;
-    sm[pidx(n)] = make_double2(a < wlen ? word(cw0 + a) : 0.0, c < wlen ? word(cw0 + c) : 0.0);
+  // a3/a4 with every sample load of UB complex points issued before any use (latency-bound
+  // otherwise); same arithmetic, in the oracle's order, as word().
+  constexpr int MS = (PACK == PACK_ASYM3) ? 3 : 2;   // samples per word (full: 1, sym: 2)
+  constexpr int UB = (PACK == PACK_ASYM3) ? 3 : 4;
+  for (int n0 = tid; n0 < N; n0 += UB * nt) {
+    double xv[UB][2][MS];
+#pragma unroll
+    for (int u = 0; u < UB; ++u)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int cw = cw0 + 2 * (n0 + u * nt) + h;
+        const bool live = (n0 + u * nt < N) && (2 * (n0 + u * nt) + h < wlen) && cw >= 0 && cw < b.xlen;
+#pragma unroll
+        for (int q = 0; q < MS; ++q) {
+          int idx;
+          if (PACK == PACK_SYM) idx = 2 * (cw - b.pre) + q;
+          else if (PACK == PACK_FULL) idx = b.o0 - (g.Np - 1) + cw;
+          else idx = b.o0 - (g.Np - 1) + cw + q * b.S;
+          const bool ok = live && (PACK != PACK_SYM || cw - b.pre >= 0) && (PACK != PACK_FULL || q == 0);
+          xv[u][h][q] = ok ? sample(idx) : 0.0;
+        }
+      }
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {
+      const int n = n0 + u * nt;
+      if (n >= N) break;
+      double wv[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int cw = cw0 + 2 * n + h;
+        const bool live = (2 * n + h < wlen) && cw >= 0 && cw < b.xlen && (PACK != PACK_SYM || cw - b.pre >= 0);
+        double v;
+        if (PACK == PACK_SYM) {
+          v = pack_sym(compand1(c_s, xv[u][h][0]), compand1(c_s, xv[u][h][1]), mp.eps);
+        } else if (PACK == PACK_ASYM2 || PACK == PACK_ASYM3) {
+          constexpr int M = (PACK == PACK_ASYM2) ? 2 : 3;
+          v = compand1(c_s, xv[u][h][M - 1]);
+#pragma unroll
+          for (int q = M - 2; q >= 0; --q) v = __dadd_rn(compand1(c_s, xv[u][h][q]), __dmul_rn(mp.eps, v));
+        } else {
+          v = xv[u][h][0];
+        }
+        wv[h] = live ? v : 0.0;
+      }
+      sm[pidx(n)] = make_double2(wv[0], wv[1]);
+    }
   }
   __syncthreads();
   fft_smem<N, -1>(sm, f.tw);                                        // a5: forward
