@@ -178,9 +178,16 @@ def workload(name, rank, world, args):
     return s, k, W_block, 1, 0
 
 
-def core_fma(info, packing):
-    """Algorithmic FP64 FMAs of the packed core per signal: sum over blocks of M_out * K."""
-    Np, W, P, K = info["Np"], info["W"], info["P"], info["taps"]
+def core_fma(info, packing, blocks=None):
+    """Algorithmic FP64 FMAs of the packed core per signal: sum over blocks of M_out * K
+    (blocks: optional list of block indices, e.g. the blocks an adaptive plan runs packed)."""
+    Np, W, P = info["Np"], info["W"], info["P"]
+    K = (Np + 1) // 2 if packing == SYM else Np
+    if blocks is not None:
+        has0 = 0 in blocks
+        n = len(blocks)
+        m_first, m_rest = _m_out(info, packing)
+        return ((m_first if has0 else 0) + (n - (1 if has0 else 0)) * m_rest) * K
     if packing == FULL:
         m_first, m_rest = W + Np - 1, W
     elif packing == SYM:
@@ -189,6 +196,16 @@ def core_fma(info, packing):
         M = 2 if packing == ASYM2 else 3
         m_first, m_rest = -(-(W + Np - 1) // M), -(-W // M)
     return (m_first + (P - 1) * m_rest) * K
+
+
+def _m_out(info, packing):
+    Np, W = info["Np"], info["W"]
+    if packing == FULL:
+        return W + Np - 1, W
+    if packing == SYM:
+        return (W + Np - 1) // 2, W // 2 + 1
+    M = 2 if packing == ASYM2 else 3
+    return -(-(W + Np - 1) // M), -(-W // M)
 
 
 def cpu_baseline(s, k, W_block, point, target_s=12.0):
@@ -344,14 +361,22 @@ def run_ours(args, ws, rank, local):
         ms = max_over_ranks(t0.elapsed_time(t1), ws)
         kern_ms = (t0.elapsed_time(t1) / args.steps) if graph is not None else \
             float(np.mean([a.elapsed_time(b) for a, b in ev]))
-        fma = core_fma(info, packing if not adaptive else FULL) * nsig
+        if adaptive:                                 # the blocks each packing ran (the decisions of this input)
+            dec = plan.adapt_block(S[(args.steps - 1) % n_buf], Q)
+            fma = sum(core_fma(info, pk, [w for w, d in enumerate(dec) if d[0] == pk]) for pk in (FULL, SYM, ASYM2))
+            rec_modes = {n_: sum(1 for d in dec if d[0] == pk) for n_, pk in (("full", FULL), ("sym", SYM),
+                                                                               ("asym2", ASYM2))}
+        else:
+            fma = core_fma(info, packing) * nsig
         rec = {"ms_per_step": ms / args.steps, "kernel_ms": kern_ms,
                "value": ws * L_out * nsig * args.steps / (ms / 1e3), "R_max": info["R_max"], "Q": Q,
                "bound_ok": info["bound_ok"], "tile": info["core_tile"], "fft_n": info["fft_n"],
                "core": "fft" if core == FFT else "direct", "cuda_graph": graph is not None}
-        if core == DIRECT and not adaptive:
+        if core == DIRECT:
             rec["fp64_tflops"] = 2.0 * fma / (kern_ms / 1e3) / 1e12
             rec["fma_per_output"] = fma / (L_out * nsig)
+        if adaptive:
+            rec["blocks_per_packing"] = rec_modes
         if core == FFT:
             res, rc = plan.residual()
             rec["fft_residual_lsb"] = res
@@ -391,20 +416,22 @@ def run_ours(args, ws, rank, local):
     h = results[head]
     full = results.get(full_pt)
     traffic, traffic_src = None, None
-    prof = os.path.join(ROOT, "profiles", "r01_ncu_cfg2.json")
-    if args.workload == "cfg2" and os.path.exists(prof):
+    prof = os.path.join(ROOT, "profiles", "r01_ncu_cfg2_asym2.json")
+    if args.workload == "cfg2" and head == "asym2_10b" and os.path.exists(prof):
         for recd in json.load(open(prof)).get("ncu_full", []):
             if f"pc_tiled_kernel<2, {h['tile']}>" in recd["kernel"]:
                 rd = recd["dram__bytes_read.sum"].split()
                 wr = recd["dram__bytes_write.sum"].split()
                 mult = {"Mbyte": 1e6, "Kbyte": 1e3, "Gbyte": 1e9, "byte": 1.0}
                 traffic = float(rd[0]) * mult[rd[1]] + float(wr[0]) * mult[wr[1]]
-                traffic_src = "profiles/r01_ncu_cfg2.json (ncu --set full, one launch)"
+                traffic_src = "profiles/r01_ncu_cfg2_asym2.json (ncu --set full, one launch)"
     if "fp64_tflops" in h:
         roof = {"bound": "alu", "achieved": h["fp64_tflops"], "peak": MEASURED_FP64_TFLOPS, "unit": "TFLOP/s",
                 "frac": h["fp64_tflops"] / MEASURED_FP64_TFLOPS, "traffic": traffic, "traffic_unit": "bytes/launch",
                 "traffic_source": traffic_src, "algorithmic_bytes": 8 * (L + L_out) * nsig,
-                "kernel": f"pc_tiled_kernel<{points[head][0]}, {h['tile']}>", "peak_source": FP64_PEAK_SOURCE,
+                "kernel": (f"pc_tiled_kernel<{points[head][0]}, {h['tile']}>" if points[head][0] != 4 else
+                           "pc_tiled_kernel x3 (one launch per packing) + pc_block_stats/pc_adapt_decide/pc_adapt_lists"),
+                "peak_source": FP64_PEAK_SOURCE,
                 "algorithmic": "FP64 FMAs of the packed core: sum over blocks of M_out * K (2 flop each)"}
     else:
         gbs = h.get("hbm_gbs_algorithmic", 8 * (L + L_out) * nsig / (h["kernel_ms"] / 1e3) / 1e9)

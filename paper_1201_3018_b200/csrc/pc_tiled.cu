@@ -266,14 +266,14 @@ constexpr int kTimW = 24 * 148 * 32, kTimP = kTimW + 148 * 16 * 16 * 4;
 
 // Job claim (one full warp).  Job queues balance the FP64 work across SMs: with nq queues
 // (nq = nsm when every SM gets >= 8 jobs, fewer for small launches), queue q owns jobs
-// [J q / nq, J (q+1) / nq) and SM s serves queue s % nq; a CTA whose queue is empty steals
-// from the others (warp-parallel scan), so every job runs even if some SM hosts no CTA.
-// Returns -1 when no job is left anywhere.
+// [J q / nq, J (q+1) / nq) and CTA c serves queue c % nq (one CTA per SM, so per CTA is per
+// SM; %smid is not dense on every part); a CTA whose queue is empty steals from the others
+// (warp-parallel scan), so every job runs.  Returns -1 when no job is left anywhere.
 __device__ __forceinline__ long long claim_job(const Exec& e, long long njobs, int lane) {
   unsigned* ctr = e.sm_ctr;
   const long long nq_ = njobs / 8;
   const int nq = (int)(nq_ < 1 ? 1 : (nq_ > e.nsm ? e.nsm : nq_));
-  const int s = (int)(smid_() % (unsigned)nq);
+  const int s = (int)(blockIdx.x % (unsigned)nq);
   long long job = -1;
   if (lane == 0) {
     const long long lo = njobs * s / nq, hi = njobs * (s + 1) / nq;

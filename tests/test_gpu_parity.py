@@ -30,9 +30,10 @@ def dev(x):
 
 
 def gpu_run(s, k, W_block, packing, Q, mode=O.CONV, eps_rule=O.EPS_POW2, rmax_rule=O.RMAX_PAPER, debug=True,
-            tile=0):
+            tile=0, npart=0):
     opts = pcb.opts_default(eps_rule=EPS[eps_rule], rmax_rule=rmax_rule, bound_policy=pcb.BOUND_WARN)
     opts.reserved[1] = tile
+    opts.reserved[3] = npart
     with pcb.Plan(len(s), len(k), W_block, mode, PK[packing], Q, opts=opts) as p:
         p.set_kernel(dev(k))
         info = p.info()
@@ -111,6 +112,54 @@ def test_every_core_tile(tile, packing, case):
     ref = O.conv_pipeline(s, k, W_block, packing, Q)
     g = gpu_run(s, k, W_block, packing, Q, debug=False, tile=tile)
     assert np.array_equal(g["r"], ref.out)
+
+
+@pytest.mark.parametrize("npart", [1, 2, 4])
+@pytest.mark.parametrize("packing", [O.FULL, O.SYM, O.ASYM2, O.ASYM3])
+@pytest.mark.parametrize("mode", [O.CONV, O.XCORR])
+def test_every_parts_per_job(npart, packing, mode):
+    """The tiled kernel splits a job into npart warp parts (G = 32 npart groups), each claimed
+    by a consumer warp of one SM sub-partition; force each split (ring depth, sentinel count
+    16/npart and the per-warp symmetric B hand-over all change with it)."""
+    L, N, W_block, Q = 150_000, 201, 2048, 31
+    rng = np.random.default_rng(npart * 10 + packing)
+    s, k = np.clip(rng.laplace(0, 0.3, L), -1, 1), rng.uniform(-1, 1, N)
+    if packing == O.FULL:
+        g = gpu_run(s, k, W_block, O.FULL, 0, mode=mode, debug=False, npart=npart)
+        want = O.full_precision(s, k, mode=mode)
+        assert np.max(np.abs(g["r"] - want)) / np.max(np.abs(want)) < 1e-12
+        return
+    Q = min(Q, O.max_q_under_bound(None, N | 1, packing, O.EPS_POW2, O.RMAX_PAPER))
+    ref = O.conv_pipeline(s, k, W_block, packing, Q, mode=mode)
+    g = gpu_run(s, k, W_block, packing, Q, mode=mode, debug=False, npart=npart)
+    assert np.array_equal(g["r"], ref.out)
+
+
+def test_graph_replay_bit_exact():
+    """Job queues are reset by the last CTA of every launch, so a captured CUDA graph of
+    several executions replays with identical results (no host-side counter state)."""
+    L, N, W_block, Q = 300_000, 513, 4096, 511
+    s, k = WL.cfg2(seed=3, L=L, N=N)
+    ref = O.conv_pipeline(s, k, W_block, O.ASYM2, Q, rmax_rule=O.RMAX_L1).out
+    with pcb.Plan(L, N, W_block, pcb.MODE_CONV, pcb.PACK_ASYM2, Q, rmax_rule=pcb.RMAX_L1) as p:
+        p.set_kernel(dev(k))
+        S = dev(s)
+        R = [torch.full((L + N - 1,), float("nan"), dtype=torch.float64, device=DEV) for _ in range(3)]
+        p.execute(S, R[0])
+        torch.cuda.synchronize()
+        gs = torch.cuda.Stream(DEV)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(gs):
+            with torch.cuda.graph(graph, stream=gs):
+                for r in R:
+                    p.execute(S, r)
+        for _ in range(3):
+            for r in R:
+                r.fill_(float("nan"))
+            graph.replay()
+            torch.cuda.synchronize()
+            for r in R:
+                assert np.array_equal(r.cpu().numpy(), ref)
 
 
 @pytest.mark.parametrize("packing", [O.SYM, O.ASYM2, O.ASYM3])
