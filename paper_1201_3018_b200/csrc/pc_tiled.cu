@@ -377,6 +377,24 @@ __global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec 
   }
   // programmatic dependent launch: only plan-owned, read-only taps are touched above
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (!e.blk_list) {
+    // While the previous launch drains: L2 prefetch of the input of the (likely) first four
+    // jobs of this CTA's queue.  A hint only -- L2 is coherent, so even if the preceding
+    // kernel writes the input, the loads after griddepcontrol.wait see its data.
+    const long long nj = e.jobs_per_sig * e.nsig;
+    const long long nq_ = nj / 8;
+    const long long nq = nq_ < 1 ? 1 : (nq_ > (long long)gridDim.x ? (long long)gridDim.x : nq_);
+    const long long q = blockIdx.x % nq, lo = nj * q / nq, hi = nj * (q + 1) / nq;
+    for (long long jb = lo; jb < hi && jb < lo + kTiledProdWarps; ++jb) {
+      const JobPos jp = job_pos(e, jb);
+      const Blk b = block_info<PACK>(g, mp.K, jp.w);
+      const long long avail = g.L - b.g0;
+      const int nv = (int)(avail < 0 ? 0 : (avail > g.W_block ? g.W_block : avail));
+      const double* src = e.s + jp.sig * e.s_stride + (b.g0 - e.s_off);
+      for (int i = threadIdx.x * 16; i < nv; i += blockDim.x * 16)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(src + i));
+    }
+  }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   __syncthreads();
   if (e.dbg_timing && tid == 0) e.dbg_timing[kTimCyc + 4 * blockIdx.x + 2] = gtimer();   // t_start (stash)
@@ -444,10 +462,10 @@ __global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec 
                                      ? e.dbg_timing + kTimP + (((size_t)blockIdx.x * 4 + f) * 16 + 15) * 4
                                      : nullptr;
       if (frec) frec[0] = gtimer();
+      double* xs_f = stg + (size_t)((f * nch) % NS) * stage_words;
       const double cs = block_cs<PACK>(mp, gsrc, n_valid, ps->red + 8 * gq, gtid, GW * 32, 1 + gq);
       if (frec) frec[1] = gtimer();
-      pack_window<PACK, T>(g, b, mp, gsrc, n_valid, cs, jp.t * G * T - front * T, rows_s,
-                           stg + (size_t)((f * nch) % NS) * stage_words, gtid, GW * 32);
+      pack_window<PACK, T>(g, b, mp, gsrc, n_valid, cs, jp.t * G * T - front * T, rows_s, xs_f, gtid, GW * 32);
       if (frec) frec[2] = gtimer();
       if (gtid == 0) {
         ps->fcs[f] = cs;
