@@ -12,8 +12,16 @@ constexpr int kTPChoices[3] = {16, 14, 12};   // tiled-kernel tiles instantiated
 constexpr int kSmemHeader = 512;
 constexpr int kTiledHeader = 2048;      // tiled kernel: mbarriers, stage metadata, counters
 constexpr int kTiledMaxStages = 24;     // tiled kernel: stage ring slots (>= 16 / npart jobs in flight)
-constexpr int kTiledProdWarps = 4;      // tiled kernel: producer warps (peak, companding, packing)
-constexpr int kTiledConsWarps = 16;     // tiled kernel: consumer warps (core + unpack), 4 per SMSP
+#ifndef PC_PROD_WARPS
+#define PC_PROD_WARPS 4
+#endif
+constexpr int kTiledProdWarps = PC_PROD_WARPS;   // tiled kernel: producer warps (peak, companding, packing)
+constexpr int kTiledFillJobs = 4;       // tiled kernel: jobs packed by all warps before the consumers start
+#ifndef PC_CONS_WARPS
+#define PC_CONS_WARPS 12
+#endif
+constexpr int kTiledConsWarps = PC_CONS_WARPS;   // tiled kernel: consumer warps (core + unpack); 12 = 3 per SMSP,
+                                                 // 16 warps per CTA so the core gets 128 registers
 constexpr int kTiledThreads = 32 * (kTiledProdWarps + kTiledConsWarps);
 constexpr int kCtrDone = 256;     // sm_ctr[kCtrDone] counts retired CTAs; queues are sm_ctr[0, nsm)   // mbarrier + reduction scratch, keeps the rest 128B-aligned
 

@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec 
     const long long nq_ = nj / 8;
     const long long nq = nq_ < 1 ? 1 : (nq_ > (long long)gridDim.x ? (long long)gridDim.x : nq_);
     const long long q = blockIdx.x % nq, lo = nj * q / nq, hi = nj * (q + 1) / nq;
-    for (long long jb = lo; jb < hi && jb < lo + kTiledProdWarps; ++jb) {
+    for (long long jb = lo; jb < hi && jb < lo + kTiledFillJobs; ++jb) {
       const JobPos jp = job_pos(e, jb);
       const Blk b = block_info<PACK>(g, mp.K, jp.w);
       const long long avail = g.L - b.g0;
@@ -431,7 +431,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec 
 
   // Pipeline fill: the first nf jobs (one per producer warp when a job is one stage) are
   // claimed in parallel, then companded and packed by all warps, five warps per job.
-  const int nf = (nch == 1) ? min(kTiledProdWarps, NS) : 1;
+  const int nf = (nch == 1) ? min(kTiledFillJobs, NS) : 1;
   const int lane_ = tid & 31, warp_ = tid >> 5;
   if (warp_ < nf) {
     const long long j = claim_job(e, njobs, lane_);
@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec 
   }
   __syncthreads();
   {
-    constexpr int GW = (kTiledProdWarps + kTiledConsWarps) / 4;   // warps per fill group
+    constexpr int GW = (kTiledProdWarps + kTiledConsWarps) / kTiledFillJobs;   // warps per fill group
     const int gq = warp_ / GW, gtid = tid - gq * GW * 32;
     for (int f = gq; f < nf; f += 4) {
       const long long fj = ps->fjob[f];
@@ -486,7 +486,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec 
     // consumer warp.  A slot is refilled only after its previous sequence was published and
     // then released by the consumers.
     const int pw = tid >> 5, lane = tid & 31;
-    const int n_sent = 16 / npart;
+    const int n_sent = kTiledConsWarps / npart;
     long long cur_blk_w = -1;
     double c_s_w = 1.0, inv_w = 0.0;
     int pj = 0;
@@ -579,7 +579,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec 
   const int smsp = (tid >> 5) & 3;
   double* wbuf = wout + (size_t)cw * 32 * (T + 1);
   mbar_wait_wd(&ps->bar_taps, 0, 4, 0, 0);
-  // A consumer warp may claim work up to 16 / npart jobs ahead of the producer, i.e. more than
+  // A consumer warp may claim work up to kTiledConsWarps / npart jobs ahead of the producer, i.e. more than
   // one ring lap: a parity wait could then see the slot's previous lap; the sequence number
   // stamped by the producer tells the two apart.
   auto wait_full = [&](long long n, int st) {
@@ -733,11 +733,11 @@ __global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec 
     if (wrec) wrec[3] = gtimer();
     if (PC_REC) ps->cyc[2] += clock64() - ps->cyc[3];
   }
+  if (e.dbg_timing && lane == 0) atomicMax(e.dbg_timing + 4 * blockIdx.x + 2, gtimer());   // CTA end = last warp
   if (PC_REC) {
     unsigned long long* tim = e.dbg_timing;
     tim[4 * blockIdx.x + 0] = smid_();
     tim[4 * blockIdx.x + 1] = tim[kTimCyc + 4 * blockIdx.x + 2];   // t_start (stashed)
-    tim[4 * blockIdx.x + 2] = gtimer();
     tim[4 * blockIdx.x + 3] = njob;
     tim[kTimCyc + 4 * blockIdx.x + 0] = ps->cyc[0];
     tim[kTimCyc + 4 * blockIdx.x + 1] = ps->cyc[1];
