@@ -689,24 +689,40 @@ __global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec 
       const double Blast = decode_sym(acc[T - 1], mp.eps, mp.eps_inv, mp.pow2).B;
       const double Bup = __shfl_up_sync(0xffffffffu, Blast, 1);
       double Bprev = (lane == 0) ? Bw : Bup;                 // B of the word before the group
+      double cb[T];
 #pragma unroll
       for (int i = 0; i < T; ++i) {
         const Digits3 d = decode_sym(acc[i], mp.eps, mp.eps_inv, mp.pow2);
-        row[i] = __dmul_rn(d.C + Bprev, inv);                // r~[2m] = C[m] + B[m-1] (Eqs. (12)-(14))
-        acc[i] = d.A;                                        // r~[2m+1] = A[m] (Eq. (15))
+        cb[i] = __dmul_rn(d.C + Bprev, inv);                 // r~[2m] = C[m] + B[m-1] (Eqs. (12)-(14))
+        acc[i] = __dmul_rn(d.A, inv);                        // r~[2m+1] = A[m] (Eq. (15))
         Bprev = d.B;
       }
-      for (int par = 0; par < 2; ++par) {
-        if (par == 1) {
+      // two rounds of 16 groups: rows (r~[2m], r~[2m+1], ...) of pitch 2T+1, one contiguous run
+      constexpr int V2 = 2 * T;
+      for (int h = 0; h < 2; ++h) {
+        if ((lane >> 4) == h) {
+          double* row2 = wbuf + (lane & 15) * (V2 + 1);
 #pragma unroll
-          for (int i = 0; i < T; ++i) row[i] = __dmul_rn(acc[i], inv);
+          for (int i = 0; i < T; ++i) {
+            row2[2 * i] = cb[i];
+            row2[2 * i + 1] = acc[i];
+          }
         }
-        // output k = 2 (m - moff) + par of core output m = mw + j, gg = gbase + k
-        const long long x0 = (long long)mw - moff;
-        long long jlo = moff - (long long)mw, jhi = (long long)b.M_out - mw;
-        jlo = max(jlo, fdiv_ceil(g_lo - gbase - par, 2) - x0);
-        jhi = min(jhi, fdiv_floor(g_hi - 1 - gbase - par, 2) + 1 - x0);
-        flush(rsig + gbase + par + 2 * x0, 2, max(jlo, 0LL), min(jhi, (long long)(32 * T)));
+        __syncwarp();
+        // output k = 2 (m - moff) + parity = k0 + j for j < 16 * 2T, gg = gbase + k
+        const long long k0 = 2LL * ((long long)mw + 16 * h * T - moff);
+        long long jlo = -k0, jhi = 2LL * b.M_out - 2LL * moff - k0;   // moff <= m < M_out
+        jlo = max(jlo, g_lo - gbase - k0);
+        jhi = min(jhi, g_hi - gbase - k0);
+        jlo = max(jlo, 0LL);
+        jhi = min(jhi, (long long)(16 * V2));
+        double* dst = rsig + gbase + k0;
+#pragma unroll
+        for (int it = 0; it < T; ++it) {
+          const int j = lane + 32 * it;
+          if (j >= jlo && j < jhi) dst[j] = wbuf[(j / V2) * (V2 + 1) + j % V2];
+        }
+        __syncwarp();
       }
     } else {
       constexpr int M = (PACK == PACK_ASYM2) ? 2 : (PACK == PACK_ASYM3 ? 3 : 1);
