@@ -383,6 +383,8 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
     f.parts0 = fs.parts0;
     f.parts1 = fs.parts1;
     e.jobs_per_sig = (b0 == 0) ? fs.parts0 + (nblk - 1) * fs.parts1 : nblk * fs.parts1;
+    e.dbg_timing = timing;
+    if (grid_out) *grid_out = (int)(e.jobs_per_sig * n_sig);
     return cuda_status(pc::launch_fft_conv(p->packing, p->fft_N, make_geo(p), e, f, e.jobs_per_sig * n_sig, st));
   }
   TShape ts;

@@ -17,6 +17,10 @@
 #include "pc_device.cuh"
 #include "pc_kernels.h"
 
+#ifndef PC_FFT_PREFETCH
+#define PC_FFT_PREFETCH 0   // L2 prefetch one wave ahead: measured slower on cfg3 (HBM bursts)
+#endif
+
 namespace pc {
 
 namespace {
@@ -215,39 +219,57 @@ __device__ void fft_smem(double2* s, const double2* __restrict__ tw) {
 template <int N>
 __device__ void spectrum_product(double2* s, const double2* __restrict__ H, const double2* __restrict__ tw2) {
   const double sc = 1.0 / (double)N;   // exact (power of two)
-  for (int k = threadIdx.x; k <= N / 2; k += blockDim.x) {
-    if (k == 0) {
-      const double2 z0 = s[pidx(0)];
-      const double X0 = z0.x + z0.y, XN = z0.x - z0.y;   // X[0], X[N] (real)
-      const double2 P0 = make_double2(X0 * H[0].x, X0 * H[0].y);
-      const double2 PN = make_double2(XN * H[N].x, XN * H[N].y);
-      // Z'[0] = (P0 + conj PN)/2 + i (P0 - conj PN)/2
-      const double2 e = make_double2(0.5 * (P0.x + PN.x), 0.5 * (P0.y - PN.y));
-      const double2 o = make_double2(0.5 * (P0.x - PN.x), 0.5 * (P0.y + PN.y));
-      s[pidx(0)] = make_double2((e.x - o.y) * sc, (e.y + o.x) * sc);
-      continue;
+  if (threadIdx.x == 0) {
+    const double2 z0 = s[pidx(0)];
+    const double X0 = z0.x + z0.y, XN = z0.x - z0.y;   // X[0], X[N] (real)
+    const double2 P0 = make_double2(X0 * H[0].x, X0 * H[0].y);
+    const double2 PN = make_double2(XN * H[N].x, XN * H[N].y);
+    // Z'[0] = (P0 + conj PN)/2 + i (P0 - conj PN)/2
+    const double2 e = make_double2(0.5 * (P0.x + PN.x), 0.5 * (P0.y - PN.y));
+    const double2 o = make_double2(0.5 * (P0.x - PN.x), 0.5 * (P0.y + PN.y));
+    s[pidx(0)] = make_double2((e.x - o.y) * sc, (e.y + o.x) * sc);
+  }
+  // k = 1 .. N/2 in rounds of UK per thread, every table and shared load of a round issued
+  // before any use (the loop is latency-bound otherwise)
+  constexpr int UK = 4;
+  for (int k0 = 1 + threadIdx.x; k0 <= N / 2; k0 += UK * blockDim.x) {
+    double2 Zk[UK], Zkp[UK], Wk[UK], Wkp[UK], Hk[UK], Hkp[UK];
+#pragma unroll
+    for (int u = 0; u < UK; ++u) {
+      const int k = k0 + u * blockDim.x;
+      const int kk = (k <= N / 2) ? k : N / 2;       // clamp (results of clamped lanes unused)
+      const int kp = N - kk;
+      Zk[u] = s[pidx(kk)];
+      Zkp[u] = s[pidx(kp)];
+      Wk[u] = __ldg(tw2 + kk);                        // exp(-2 pi i k / 2N)
+      Wkp[u] = __ldg(tw2 + kp);
+      Hk[u] = __ldg(H + kk);
+      Hkp[u] = __ldg(H + kp);
     }
-    const int kp = N - k;
-    const double2 Zk = s[pidx(k)], Zkp = s[pidx(kp)];
-    const double2 Wk = __ldg(tw2 + k), Wkp = __ldg(tw2 + kp);          // exp(-2 pi i k / 2N)
-    // E[k] = (Z[k] + conj Z[k'])/2,  O[k] = -i/2 (Z[k] - conj Z[k'])
-    const double2 Ek = make_double2(0.5 * (Zk.x + Zkp.x), 0.5 * (Zk.y - Zkp.y));
-    const double2 Ok = make_double2(0.5 * (Zk.y + Zkp.y), -0.5 * (Zk.x - Zkp.x));
-    const double2 Ekp = cconj(Ek), Okp = cconj(Ok);
-    const double2 Xk = cadd(Ek, cmul(Wk, Ok));
-    const double2 Xkp = cadd(Ekp, cmul(Wkp, Okp));
-    const double2 Pk = cmul(Xk, __ldg(H + k)), Pkp = cmul(Xkp, __ldg(H + kp));
-    // Z'[k] = (P[k] + conj P[k'])/2 + i conj(W_k) (P[k] - conj P[k'])/2
-    auto merge = [&](double2 a, double2 b, double2 W) {
-      const double2 e = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
-      const double2 d = make_double2(0.5 * (a.x - b.x), 0.5 * (a.y + b.y));
-      const double2 o = cmul(d, cconj(W));
-      return make_double2((e.x - o.y) * sc, (e.y + o.x) * sc);
-    };
-    const double2 Zpk = merge(Pk, Pkp, Wk);
-    const double2 Zpkp = merge(Pkp, Pk, Wkp);
-    s[pidx(k)] = Zpk;
-    if (kp != k) s[pidx(kp)] = Zpkp;
+#pragma unroll
+    for (int u = 0; u < UK; ++u) {
+      const int k = k0 + u * blockDim.x;
+      if (k > N / 2) break;
+      const int kp = N - k;
+      // E[k] = (Z[k] + conj Z[k'])/2,  O[k] = -i/2 (Z[k] - conj Z[k'])
+      const double2 Ek = make_double2(0.5 * (Zk[u].x + Zkp[u].x), 0.5 * (Zk[u].y - Zkp[u].y));
+      const double2 Ok = make_double2(0.5 * (Zk[u].y + Zkp[u].y), -0.5 * (Zk[u].x - Zkp[u].x));
+      const double2 Ekp = cconj(Ek), Okp = cconj(Ok);
+      const double2 Xk = cadd(Ek, cmul(Wk[u], Ok));
+      const double2 Xkp = cadd(Ekp, cmul(Wkp[u], Okp));
+      const double2 Pk = cmul(Xk, Hk[u]), Pkp = cmul(Xkp, Hkp[u]);
+      // Z'[k] = (P[k] + conj P[k'])/2 + i conj(W_k) (P[k] - conj P[k'])/2
+      auto merge = [&](double2 a, double2 b, double2 W) {
+        const double2 e = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
+        const double2 d = make_double2(0.5 * (a.x - b.x), 0.5 * (a.y + b.y));
+        const double2 o = cmul(d, cconj(W));
+        return make_double2((e.x - o.y) * sc, (e.y + o.x) * sc);
+      };
+      const double2 Zpk = merge(Pk, Pkp, Wk[u]);
+      const double2 Zpkp = merge(Pkp, Pk, Wkp[u]);
+      s[pidx(k)] = Zpk;
+      if (kp != k) s[pidx(kp)] = Zpkp;
+    }
   }
   __syncthreads();
 }
@@ -299,6 +321,41 @@ __global__ void __launch_bounds__(N / 16, (N <= 4096 ? 2 : 1)) pc_fft_conv_kerne
   const long long avail = g.L - b.g0;
   const int n_valid = (int)(avail < 0 ? 0 : (avail > g.W_block ? g.W_block : avail));
 
+  // diagnostics (conv_execute_profile): per job {smid, t0, t_peak, t_packed, t_fwd, t_prod, t_inv, t_end}
+  unsigned long long* ft = (e.dbg_timing && tid == 0 && blockIdx.x < 4096) ? e.dbg_timing + 8 * blockIdx.x : nullptr;
+  auto stamp = [&](int i) {
+    if (ft) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      ft[i] = t;
+    }
+  };
+  if (ft) {
+    unsigned sm_;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_));
+    ft[0] = sm_;
+  }
+  stamp(1);
+  {
+    // L2 prefetch of the input of the job one wave ahead (grid-stride by the resident CTAs),
+    // so that job's peak and packing loads hit L2.  A hint only.
+    const long long nj = e.jobs_per_sig * e.nsig, jn = job + f.wave;
+    if (PC_FFT_PREFETCH && f.wave > 0 && jn < nj) {
+      const long long sig2 = jn / e.jobs_per_sig;
+      long long r2 = jn % e.jobs_per_sig, w2;
+      if (e.b0 == 0 && r2 < f.parts0) {
+        w2 = 0;
+      } else {
+        if (e.b0 == 0) r2 -= f.parts0;
+        w2 = e.b0 + (e.b0 == 0 ? 1 : 0) + r2 / f.parts1;
+      }
+      const long long g2 = (w2 == 0) ? 0 : w2 * (long long)g.W - 2;
+      const long long av = g.L - g2;
+      const int nv2 = (int)(av < 0 ? 0 : (av > g.W_block ? g.W_block : av));
+      const double* src2 = e.s + sig2 * e.s_stride + (g2 - e.s_off);
+      for (int i = tid * 16; i < nv2; i += nt * 16) asm volatile("prefetch.global.L2 [%0];" ::"l"(src2 + i));
+    }
+  }
   // a2/a3: block peak and c_s (Eq. (2))
   double c_s = 1.0;
   if (PACK != PACK_FULL) {
@@ -337,6 +394,7 @@ __global__ void __launch_bounds__(N / 16, (N <= 4096 ? 2 : 1)) pc_fft_conv_kerne
     c_s = (peak == 0.0) ? 1.0 : mp.Q / peak;
   }
   const double inv = dequant_scale(c_s, mp.c_k);
+  stamp(2);
   // part window: core outputs [m_lo, m_hi); sym parts after the first also need word m_lo-1
   const int front = (PACK == PACK_SYM && part > 0) ? 1 : 0;
   const int m_lo = (part == 0) ? 0 : f.part0_out + (part - 1) * f.part_out;
@@ -409,9 +467,13 @@ __global__ void __launch_bounds__(N / 16, (N <= 4096 ? 2 : 1)) pc_fft_conv_kerne
     }
   }
   __syncthreads();
+  stamp(3);
   fft_smem<N, -1>(sm, f.tw);                                        // a5: forward
+  stamp(4);
   spectrum_product<N>(sm, f.H, f.tw2);
+  stamp(5);
   fft_smem<N, +1>(sm, f.tw);                                        // a5: inverse
+  stamp(6);
   // p[q] = Re/Im of sm[q/2]; core output m (window-relative mw = m - cw0) = p[mw + K - 1]
   auto pval = [&](int q) -> double {
     const double2 z = sm[pidx(q >> 1)];
@@ -466,6 +528,7 @@ __global__ void __launch_bounds__(N / 16, (N <= 4096 ? 2 : 1)) pc_fft_conv_kerne
     if ((tid & 31) == 0 && resid > 0.0)
       atomicMax(reinterpret_cast<unsigned long long*>(f.resid), (unsigned long long)__double_as_longlong(resid));
   }
+  stamp(7);
   (void)bx;
 }
 
@@ -479,13 +542,19 @@ static cudaError_t launch_fft_N(int packing, const Geo& g, const Exec& e, const 
 #define PC_FFT_CASE(PK)                                                                                  \
   case PK: {                                                                                             \
     auto kfn = pc_fft_conv_kernel<PK, N>;                                                               \
-    static bool set = false;                                                                             \
-    if (!set) {                                                                                          \
+    static int wave = -1;                                                                                \
+    if (wave < 0) {                                                                                      \
       err = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);          \
       if (err != cudaSuccess) return err;                                                                \
-      set = true;                                                                                        \
+      int occ = 0, dev = 0, sms = 0;                                                                     \
+      cudaGetDevice(&dev);                                                                               \
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);                                 \
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, N / 16, smem) != cudaSuccess) occ = 0; \
+      wave = occ * sms;                                                                                  \
     }                                                                                                    \
-    kfn<<<(unsigned)n_jobs, N / 16, smem, st>>>(g, e, f);                                               \
+    FftArgs fw = f;                                                                                      \
+    fw.wave = wave;                                                                                      \
+    kfn<<<(unsigned)n_jobs, N / 16, smem, st>>>(g, e, fw);                                              \
     break;                                                                                               \
   }
     PC_FFT_CASE(PACK_FULL)
