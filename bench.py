@@ -69,6 +69,8 @@ def parse():
     ap.add_argument("--signals", type=int, default=0, help="cfg4: database signals in total (default 1024)")
     ap.add_argument("--force-warps", type=int, default=0, help="diagnostics: consumer warps per CTA")
     ap.add_argument("--opt", action="append", default=[], help="diagnostics: conv_opts.reserved[i]=v as i=v")
+    ap.add_argument("--N", type=int, default=0, help="diagnostics: override the kernel length (cfg1/cfg2)")
+    ap.add_argument("--exec", default="fused", choices=["fused", "perblock"], help="diagnostics: execution form")
     ap.add_argument("--graph", type=int, default=-1,
                     help="1: capture the K timed steps in one CUDA graph (default: on for cfg1, launch-bound)")
     return ap.parse_args()
@@ -160,9 +162,9 @@ def workload(name, rank, world, args):
     from paper_1201_3018_b200 import workloads as WL
     W_block = WORKLOADS[name][0]
     if name == "cfg1":
-        s, k = WL.cfg1(seed=rank, L=args.L or 65536)
+        s, k = WL.cfg1(seed=rank, L=args.L or 65536, N=args.N or 64)
     elif name == "cfg2":
-        s, k = WL.cfg2(seed=rank, L=args.L or (1 << 22))
+        s, k = WL.cfg2(seed=rank, L=args.L or (1 << 22), N=args.N or 512)
     elif name == "cfg3":
         s, k = WL.cfg3(seed=rank, L=args.L or (1 << 24))
     elif name == "cfg5":
@@ -286,7 +288,7 @@ def run_ours(args, ws, rank, local):
     for name in sel:
         packing, Q, rmax, core = points[name]
         adaptive = packing == 4
-        opts = pcb.opts_default(rmax_rule=rmax, core=core)
+        opts = pcb.opts_default(rmax_rule=rmax, core=core, exec=0 if args.exec == "fused" else 1)
         opts.reserved[3] = args.force_warps
         for kv in args.opt:
             i, v = kv.split("=")

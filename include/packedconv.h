@@ -52,10 +52,12 @@ enum { PC_EPS_PAPER = 0, PC_EPS_RADIX = 1, PC_EPS_POW2 = 2 };   /* Eq.(6); C2; C
 enum { PC_RMAX_PAPER = 0, PC_RMAX_L1 = 1 };                /* Eq.(3); C3                  */
 enum { PC_BOUND_STRICT = 0, PC_BOUND_WARN = 1 };
 enum { PC_CORE_DIRECT = 0, PC_CORE_FFT = 1 };              /* Tier-2 core          */
-/* Execution form: FUSED = persistent warp-specialized kernel (producer warps compand and
- * pack block n+1 while consumer warps run the core on block n); PERBLOCK = one CTA per
+/* Execution form: FUSED = automatic (the tiled kernel, or the per-block kernel when a
+ * block's core is below 1e5 FMAs, where the tiled pipeline's per-job latency dominates);
+ * TILED = always the persistent warp-specialized tiled kernel (producer warps compand and
+ * pack jobs n+1.. while consumer warps run the core on job n); PERBLOCK = one CTA per
  * block, phases separated by barriers (also the form that serves conv_execute_debug). */
-enum { PC_EXEC_FUSED = 0, PC_EXEC_PERBLOCK = 1 };
+enum { PC_EXEC_FUSED = 0, PC_EXEC_PERBLOCK = 1, PC_EXEC_TILED = 2 };
 
 /* Plan options.  conv_opts_default() fills: eps_rule POW2, rmax_rule PAPER, bound_policy
  * STRICT, core DIRECT, exec FUSED, K_q 0 (= Q), device -1 (current), u_sys 3.1193e-11. */

@@ -21,7 +21,7 @@ EPS_PAPER, EPS_RADIX, EPS_POW2 = 0, 1, 2
 RMAX_PAPER, RMAX_L1 = 0, 1
 BOUND_STRICT, BOUND_WARN = 0, 1
 CORE_DIRECT, CORE_FFT = 0, 1
-EXEC_FUSED, EXEC_PERBLOCK = 0, 1
+EXEC_FUSED, EXEC_PERBLOCK, EXEC_TILED = 0, 1, 2
 
 PACK_NAMES = {PACK_FULL: "full", PACK_SYM: "sym", PACK_ASYM2: "asym2", PACK_ASYM3: "asym3",
               PACK_ADAPTIVE: "adaptive"}

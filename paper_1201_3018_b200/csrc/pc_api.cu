@@ -18,6 +18,7 @@ using pc::ModeP;
 namespace {
 
 constexpr size_t kMaxSmem = 232448;      // 227 KB dynamic shared memory per CTA (sm_100)
+constexpr long long kSmallCoreFma = 100000;   // per-block core FMAs below which the per-block kernel runs
 constexpr size_t kSmemPerSM = 233472;    // 228 KB shared memory per SM
 
 struct ModeState {
@@ -388,7 +389,20 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
     return cuda_status(pc::launch_fft_conv(p->packing, p->fft_N, make_geo(p), e, f, e.jobs_per_sig * n_sig, st));
   }
   TShape ts;
-  if (!dbg && p->packing == PC_PACK_ADAPTIVE && p->opts.exec == PC_EXEC_FUSED && n_sig == 1 && b0 == 0 &&
+  // Small cores (cfg1: 1024-sample blocks, 65 taps): a job's core is shorter than the tiled
+  // kernel's per-job pipeline latency, so one CTA per block (phases in sequence) is faster
+  // (measured 2x at N = 64 for 65k..1M samples; the tiled kernel wins from N = 128 at 4096).
+  bool small_core = true;
+  for (int i = 0; i < np; ++i) {
+    int mmax, mtyp;
+    core_sizes(p, packs[i], &mmax, &mtyp);
+    if ((long long)mtyp * core_taps(p, packs[i]) >= kSmallCoreFma) small_core = false;
+  }
+  const bool forced = p->opts.reserved[1] != 0 || p->opts.reserved[3] != 0;   // tile / parts forced: tiled
+  if (!dbg && small_core && !forced && per_block_ok && p->opts.exec == PC_EXEC_FUSED)
+    return cuda_status(pc::launch_fused(launch_pack, make_geo(p), e, nblk * n_sig, sh.threads, sh.smem, st));
+  const bool tiled_ok = p->opts.exec == PC_EXEC_FUSED || p->opts.exec == PC_EXEC_TILED;
+  if (!dbg && p->packing == PC_PACK_ADAPTIVE && tiled_ok && n_sig == 1 && b0 == 0 &&
       nblk == p->P && p->d_lists) {
     // a8 -> a2..a7: one tiled launch per packing over its block list (pc_adapt_lists)
     TShape sh3[3];
@@ -423,7 +437,7 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
       return PC_OK;
     }
   }
-  if (!dbg && p->packing != PC_PACK_ADAPTIVE && p->opts.exec == PC_EXEC_FUSED && tiled_shape(p, p->packing, &ts)) {
+  if (!dbg && p->packing != PC_PACK_ADAPTIVE && tiled_ok && tiled_shape(p, p->packing, &ts)) {
     e.sm_ctr = p->d_counter;
     e.dbg_timing = timing;
     e.G = ts.G;

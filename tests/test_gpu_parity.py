@@ -30,8 +30,8 @@ def dev(x):
 
 
 def gpu_run(s, k, W_block, packing, Q, mode=O.CONV, eps_rule=O.EPS_POW2, rmax_rule=O.RMAX_PAPER, debug=True,
-            tile=0, npart=0):
-    opts = pcb.opts_default(eps_rule=EPS[eps_rule], rmax_rule=rmax_rule, bound_policy=pcb.BOUND_WARN)
+            tile=0, npart=0, exec_=0):
+    opts = pcb.opts_default(eps_rule=EPS[eps_rule], rmax_rule=rmax_rule, bound_policy=pcb.BOUND_WARN, exec=exec_)
     opts.reserved[1] = tile
     opts.reserved[3] = npart
     with pcb.Plan(len(s), len(k), W_block, mode, PK[packing], Q, opts=opts) as p:
@@ -77,9 +77,10 @@ SMALL_CASES = [  # (L, N, W_block, Q): several tiles, ragged tails, P = 1, N = 1
 ]
 
 
+@pytest.mark.parametrize("exec_", [0, 2, 1])      # auto, tiled, per-block
 @pytest.mark.parametrize("packing", [O.SYM, O.ASYM2, O.ASYM3])
 @pytest.mark.parametrize("case", SMALL_CASES)
-def test_packed_bit_exact_pow2(packing, case):
+def test_packed_bit_exact_pow2(packing, case, exec_):
     L, N, W_block, Q = case
     rng = np.random.default_rng(L * 7 + N)
     s, k = rng.laplace(0, 0.3, L), rng.uniform(-1, 1, N)
@@ -87,7 +88,7 @@ def test_packed_bit_exact_pow2(packing, case):
     Q = min(Q, O.max_q_under_bound(None, Np, packing, O.EPS_POW2, O.RMAX_PAPER))   # Eq. (3) within bound
     ref = O.conv_pipeline(s, k, W_block, packing, Q, keep_blocks=True)
     assert ref.kernel.bound_ok and ref.mismatches == 0
-    g = gpu_run(s, k, W_block, packing, Q)
+    g = gpu_run(s, k, W_block, packing, Q, exec_=exec_)
     assert g["info"]["c_k"] == ref.kernel.c_k and g["info"]["R_max"] == ref.kernel.R
     assert g["info"]["eps_inv"] == ref.kernel.eps.eps_inv
     check_blocks(g, ref, packing)
