@@ -36,6 +36,7 @@ MEASURED_FP64_TFLOPS = 34.0   # profiles/r01_fp64_peak.log: sustained DFMA, 148 
 FP64_PEAK_SOURCE = "measured (tools/fp64_peak.cu, profiles/r01_fp64_peak.log); not in MEASURED_PEAKS.json"
 HBM_GBS = 6540.2              # MEASURED_PEAKS.json hbm_gbs (copy)
 
+METRIC = "output samples/s, packed vs full-precision conv, 1/2/4/8 B200; % FP64/HBM peak"   # BASELINE.json
 FULL, SYM, ASYM2, ASYM3 = 0, 1, 2, 3
 DIRECT, FFT = 0, 1
 # workload -> (W_block, points {name: (packing, Q, rmax_rule, core)}, headline, full-precision point)
@@ -251,7 +252,7 @@ def run_reference(args, ws, rank):
             O.process_block(s, 1 + (i * blocks_per_step + j) % (geom.P - 1), geom, ks, Q)
     dt = time.perf_counter() - t0
     v = args.steps * blocks_per_step * geom.W / dt
-    line = {"metric": "output samples/s, packed vs full-precision conv", "value": v, "unit": "output samples/s",
+    line = {"metric": METRIC, "value": v, "unit": "output samples/s",
             "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -437,7 +438,7 @@ def run_ours(args, ws, rank, local):
                 "traffic": None, "kernel": "pc_fft_conv_kernel" if h["core"] == "fft" else "pc_fused_kernel",
                 "algorithmic": "8 B read + 8 B written per sample"}
     line = {
-        "metric": "output samples/s, packed vs full-precision conv, 1/2/4/8 B200; % FP64/HBM peak",
+        "metric": METRIC,
         "value": h["value"], "unit": "output samples/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": h["ms_per_step"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
