@@ -77,6 +77,17 @@ for name, (pk, Q, rm) in points.items():
     cta_end = {cc: (r[cc, 2] - t0) / 1e3 for cc in range(g)}
     live = np.array([[tb < cta_end[cc]] * 4 for cc in range(g)]).reshape(g, 4, len(tb))
     hist_core = {int(v): round(float(np.sum((act == v) & live) / np.sum(live)), 4) for v in range(5)}
+    # where the zero-warps-in-core SMSP time sits: before the first core, between cores, after the last
+    zero = (act == 0) & live
+    any_core = act > 0
+    first = np.argmax(any_core, axis=2)
+    last = act.shape[2] - 1 - np.argmax(any_core[:, :, ::-1], axis=2)
+    idx = np.arange(act.shape[2])[None, None, :]
+    zsplit = {"before_first_core": float(np.sum(zero & (idx < first[:, :, None]))),
+              "between_cores": float(np.sum(zero & (idx >= first[:, :, None]) & (idx <= last[:, :, None]))),
+              "after_last_core": float(np.sum(zero & (idx > last[:, :, None])))}
+    ztot = max(1.0, float(np.sum(live)))
+    zsplit = {k: round(v / ztot, 4) for k, v in zsplit.items()}
     def cta_trace(c):
         prod = [[int(Pr[c, w, j, 0]), round((Pr[c, w, j, 3] - t0) / 1e3, 1)] for w in range(4) for j in range(16)
                 if Pr[c, w, j, 3]]
@@ -85,7 +96,7 @@ for name, (pk, Q, rm) in points.items():
         return {"produced[mseq,t_pub]": sorted(prod), "consumed[warp,mseq,t_ready,t_core,t_stored]": sorted(cons, key=lambda x: x[2])}
     fill_phases = (Pr[:, :, 15, :3].astype(float) - r[:, 1][:, None, None]) / 1e3   # claimed, peak, packed (us)
     fill_stats = {k: round(float(np.median(fill_phases[:, :, i])), 2) for i, k in enumerate(["claimed", "peak", "packed"])}
-    out[name] = {"fill_phases_us_median": fill_stats, "smsp_warps_in_core_time_frac": hist_core, "cta0": cta_trace(0), "grid": g, "tile": info["core_tile"], "kernel_us": float(T_end),
+    out[name] = {"zero_core_time_split": zsplit, "fill_phases_us_median": fill_stats, "smsp_warps_in_core_time_frac": hist_core, "cta0": cta_trace(0), "grid": g, "tile": info["core_tile"], "kernel_us": float(T_end),
                  "start_spread_us": float(st.max()), "sm_end_min_us": float(sm_end.min()),
                  "sm_end_median_us": float(np.median(sm_end)), "sm_end_max_us": float(sm_end.max()),
                  "resident_ctas_per_sm_time_frac": hist,
