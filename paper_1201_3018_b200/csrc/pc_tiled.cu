@@ -83,11 +83,11 @@ __device__ __forceinline__ JobPos job_pos(const Exec& e, long long job) {
 // a4 for one stage: core words [cw0, cw0 + rows_s*T) of block b into the padded row-major
 // window xs[(i / T) * (T + 1) + i % T].  Word-major over the producer threads (coalesced
 // loads), UW words per thread with every sample load issued before any use.
-template <int PACK, int T>
+template <int PACK, int T, int UWF = 1>
 __device__ __forceinline__ void pack_window(const Geo& g, const Blk& b, const ModeP& mp, const double* gsrc,
                                             int n_valid, double c_s, int cw0, int rows_s, double* xs, int ptid,
                                             int nprod) {
-  constexpr int UW = (PACK == PACK_ASYM3) ? 4 : 8;
+  constexpr int UW = UWF * ((PACK == PACK_ASYM3) ? 4 : 8);   // words per thread in flight
   const int words = rows_s * T;
   auto sample = [&](int i) -> double { return (i < 0 || i >= n_valid) ? 0.0 : __ldg(gsrc + i); };
   for (int i0 = ptid; i0 < words; i0 += UW * nprod) {
@@ -556,7 +556,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec 
           mbar_wait_wd(&ps->empty[st], (uint32_t)(((n / NS) & 1) ^ 1), 1, n, st);
         }
         if (job >= 0 && !(prepacked && c == 0))
-          pack_window<PACK, T>(g, b, mp, gsrc, n_valid, c_s_w, jp.t * G * T - front * T + c * KC, rows_s,
+          pack_window<PACK, T, 2>(g, b, mp, gsrc, n_valid, c_s_w, jp.t * G * T - front * T + c * KC, rows_s,
                                stg + (size_t)st * stage_words, lane, 32);
         __syncwarp();
         publish(n, st, c, job, inv_w, lane);
