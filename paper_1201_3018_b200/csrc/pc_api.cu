@@ -329,6 +329,9 @@ void fill_modep(const ModeState& m, ModeP* mp) {
   mp->K = m.K;
   mp->K_pad = m.K_pad;
   mp->rows = m.rows;
+  mp->paper_unpack = 0;
+  mp->R = (double)m.R;
+  mp->R_safe = 0.0;
 }
 
 // The packings a plan's launches may use.
@@ -367,6 +370,11 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
   e.stage_raw = per_block_ok ? sh.stage_raw : 0;
   e.reg_path = per_block_ok ? sh.reg_path : 0;
   for (int i = 0; i < np; ++i) fill_modep(p->ms[packs[i]], &e.mp[packs[i]]);
+  if (p->opts.reserved[5] == 1) {                    // literal Eqs. (11)-(15) (SYM, tiled kernel)
+    pc::ModeP& ms = e.mp[PC_PACK_SYM];
+    ms.paper_unpack = 1;
+    ms.R_safe = ms.R * (ms.eps + 1.0 + ms.eps_inv) + p->opts.u_sys * ms.eps_inv;   // P:103, oracle order
+  }
   e.dec_pack = p->packing == PC_PACK_ADAPTIVE ? p->d_dec_pack : nullptr;
   e.nsig = n_sig;
   const int launch_pack = p->packing == PC_PACK_ADAPTIVE ? -1 : p->packing;
@@ -398,7 +406,8 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
     core_sizes(p, packs[i], &mmax, &mtyp);
     if ((long long)mtyp * core_taps(p, packs[i]) >= kSmallCoreFma) small_core = false;
   }
-  const bool forced = p->opts.reserved[1] != 0 || p->opts.reserved[3] != 0;   // tile / parts forced: tiled
+  const bool forced = p->opts.reserved[1] != 0 || p->opts.reserved[3] != 0 ||   // tile / parts forced,
+                      p->opts.reserved[5] == 1;                                  // literal unpack: tiled
   if (!dbg && small_core && !forced && per_block_ok && p->opts.exec == PC_EXEC_FUSED)
     return cuda_status(pc::launch_fused(launch_pack, make_geo(p), e, nblk * n_sig, sh.threads, sh.smem, st));
   const bool tiled_ok = p->opts.exec == PC_EXEC_FUSED || p->opts.exec == PC_EXEC_TILED;

@@ -34,6 +34,8 @@ struct ModeP {
   int pow2;             // eps = 2^-b (reading C4)
   int K, K_pad;         // core taps and taps padded to a multiple of the kernel's tile T
   int rows;             // rows of the column layout of the core's input words
+  int paper_unpack;     // SYM: literal Eqs. (11)-(15) with the u_sys guard instead of balanced digits
+  double R, R_safe;     // R_max and R_safe = R (eps + 1 + eps^-1) + u_sys eps^-1
 };
 
 struct Exec {

@@ -685,17 +685,42 @@ __global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec 
     if (PACK == PACK_SYM) {
       const int moff = (jp.w == 0) ? 0 : 1;
       for (int o = 16; o > 0; o >>= 1) px += __shfl_xor_sync(0xffffffffu, px, o);
-      const double Bw = extra ? decode_sym(px, mp.eps, mp.eps_inv, mp.pow2).B : 0.0;
-      const double Blast = decode_sym(acc[T - 1], mp.eps, mp.eps_inv, mp.pow2).B;
-      const double Bup = __shfl_up_sync(0xffffffffu, Blast, 1);
-      double Bprev = (lane == 0) ? Bw : Bup;                 // B of the word before the group
       double cb[T];
+      if (!mp.paper_unpack) {
+        const double Bw = extra ? decode_sym(px, mp.eps, mp.eps_inv, mp.pow2).B : 0.0;
+        const double Blast = decode_sym(acc[T - 1], mp.eps, mp.eps_inv, mp.pow2).B;
+        const double Bup = __shfl_up_sync(0xffffffffu, Blast, 1);
+        double Bprev = (lane == 0) ? Bw : Bup;               // B of the word before the group
 #pragma unroll
-      for (int i = 0; i < T; ++i) {
-        const Digits3 d = decode_sym(acc[i], mp.eps, mp.eps_inv, mp.pow2);
-        cb[i] = __dmul_rn(d.C + Bprev, inv);                 // r~[2m] = C[m] + B[m-1] (Eqs. (12)-(14))
-        acc[i] = __dmul_rn(d.A, inv);                        // r~[2m+1] = A[m] (Eq. (15))
-        Bprev = d.B;
+        for (int i = 0; i < T; ++i) {
+          const Digits3 d = decode_sym(acc[i], mp.eps, mp.eps_inv, mp.pow2);
+          cb[i] = __dmul_rn(d.C + Bprev, inv);               // r~[2m] = C[m] + B[m-1] (Eqs. (12)-(14))
+          acc[i] = __dmul_rn(d.A, inv);                      // r~[2m+1] = A[m] (Eq. (15))
+          Bprev = d.B;
+        }
+      } else {
+        // Literal Eqs. (11)-(15) (reading C6), the oracle's operation order:
+        // u = r_bar + R_safe (11); side_eps[m] = eps^-1 (u[m-1] - floor u[m-1]) (12), R at the
+        // block's first word; side_eps^-1 = floor(eps u) (13); even = floor(side_eps^-1 +
+        // side_eps - 2R) (14); odd = floor(floor u - eps^-1 side_eps^-1 - R) (15).
+        auto frac_side = [&](double r) {
+          const double u = __dadd_rn(r, mp.R_safe);
+          return __dmul_rn(mp.eps_inv, __dsub_rn(u, floor(u)));
+        };
+        const double se_w = extra ? frac_side(px) : mp.R;
+        const double se_last = frac_side(acc[T - 1]);
+        const double se_up = __shfl_up_sync(0xffffffffu, se_last, 1);
+        double se = (lane == 0) ? se_w : se_up;
+        const double twoR = __dmul_rn(2.0, mp.R);
+#pragma unroll
+        for (int i = 0; i < T; ++i) {
+          const double u = __dadd_rn(acc[i], mp.R_safe);
+          const double fu = floor(u);
+          const double sei = floor(__dmul_rn(mp.eps, u));
+          cb[i] = __dmul_rn(floor(__dsub_rn(__dadd_rn(sei, se), twoR)), inv);
+          acc[i] = __dmul_rn(floor(__dsub_rn(__dsub_rn(fu, __dmul_rn(mp.eps_inv, sei)), mp.R)), inv);
+          se = __dmul_rn(mp.eps_inv, __dsub_rn(u, fu));
+        }
       }
       // two rounds of 16 groups: rows (r~[2m], r~[2m+1], ...) of pitch 2T+1, one contiguous run
       constexpr int V2 = 2 * T;

@@ -593,3 +593,31 @@ def test_execute_host_pipelined(mode, packing):
     if packing == O.FULL and mode == O.CONV:
         full = O.full_precision(s, k)
         assert float(np.max(np.abs(ref - full)) / np.max(np.abs(full))) < 1e-12
+
+
+@pytest.mark.parametrize("mode", [O.CONV, O.XCORR])
+@pytest.mark.parametrize("case", [(50_000, 65, 1024, 20), (120_000, 129, 2048, 20), (60_000, 33, 512, 35)])
+def test_literal_paper_unpack(mode, case):
+    """conv_opts.reserved[5] = 1: the symmetric unpack follows the literal Eqs. (11)-(15) with
+    the u_sys guard (PAPER eps, reading C6: exact for R_max < 89,524).  Its integers equal the
+    exact integer convolution, so the output equals the oracle's literal-form pipeline and the
+    balanced-digit output bit for bit."""
+    L, N, W_block, Q = case
+    rng = np.random.default_rng(L + N)
+    s, k = np.clip(rng.laplace(0, 0.3, L), -1, 1), rng.uniform(-1, 1, N)
+    Np = N | 1
+    assert Np * Q * Q <= 52_000      # the u_sys guard is reliable well below 89,524 (SURVEY §0.3: none at 51k)
+    ref = O.conv_pipeline(s, k, W_block, O.SYM, Q, mode=mode, eps_rule=O.EPS_PAPER, unpack_form="paper")
+    assert ref.mismatches == 0
+    opts = pcb.opts_default(eps_rule=EPS[O.EPS_PAPER], rmax_rule=O.RMAX_PAPER, bound_policy=pcb.BOUND_WARN)
+    opts.reserved[5] = 1
+    with pcb.Plan(L, N, W_block, pcb.MODE_XCORR if mode == O.XCORR else pcb.MODE_CONV, pcb.PACK_SYM, Q,
+                  opts=opts) as p:
+        p.set_kernel(dev(k))
+        r = torch.full((p.info()["L_out"],), float("nan"), dtype=torch.float64, device=DEV)
+        p.execute(dev(s), r)
+        torch.cuda.synchronize()
+        got = r.cpu().numpy()
+    assert np.array_equal(got, ref.out)
+    bal = O.conv_pipeline(s, k, W_block, O.SYM, Q, mode=mode, eps_rule=O.EPS_PAPER)
+    assert np.array_equal(got, bal.out)
