@@ -21,6 +21,10 @@
 #define PC_FFT_PREFETCH 0   // L2 prefetch one wave ahead: measured slower on cfg3 (HBM bursts)
 #endif
 
+#ifndef PC_FFT_CARVEOUT
+#define PC_FFT_CARVEOUT 60   // % of the unified L1/shared array as shared memory
+#endif
+
 namespace pc {
 
 namespace {
@@ -121,13 +125,28 @@ __device__ __forceinline__ void dft_small(double2* v) {
   }
 }
 
+// Twiddle sources: a correctly rounded global table, or (conv kernel) a two-level table in
+// shared memory: w^m = hi[m >> 6] * lo[m & 63] with lo[b] = w^b, hi[a] = w^(64a) copied from
+// the correctly rounded table (hi[0] = lo[0] = 1 exactly, so m < 64 or 64 | m are exact; else
+// one complex product, <= ~1.5 ulp).  Shared-memory reads replace L1/L2 table loads, which
+// were half of a pass's time.
+struct TwGlobal {
+  const double2* tw;
+  __device__ __forceinline__ double2 operator()(int m) const { return __ldg(tw + m); }
+};
+struct TwSmem2 {
+  const double2* lo;
+  const double2* hi;
+  __device__ __forceinline__ double2 operator()(int m) const { return cmul(hi[m >> 6], lo[m & 63]); }
+};
+
 }  // namespace
 
 __host__ __device__ constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n / 2); }
 
 // One radix-16 Stockham pass (sub-transform length LS before the pass).
-template <int N, int SIGN, int LS>
-__device__ __forceinline__ void stockham16(double2* s, const double2* __restrict__ tw) {
+template <int N, int SIGN, int LS, class TW>
+__device__ __forceinline__ void stockham16(double2* s, const TW& tw) {
   constexpr int NB = N / 16;
   const int j = threadIdx.x;
   const int k = j & (LS - 1);
@@ -137,7 +156,7 @@ __device__ __forceinline__ void stockham16(double2* s, const double2* __restrict
   if (LS > 1) {                                 // twiddle loads in flight across the barrier
     const int step = k * (N / (LS * 16));
 #pragma unroll
-    for (int p = 1; p < 16; ++p) w[p] = __ldg(tw + p * step);
+    for (int p = 1; p < 16; ++p) w[p] = tw(p * step);
   }
 #endif
 #pragma unroll
@@ -148,7 +167,7 @@ __device__ __forceinline__ void stockham16(double2* s, const double2* __restrict
     double2 w[16];
     const int step = k * (N / (LS * 16));
 #pragma unroll
-    for (int p = 1; p < 16; ++p) w[p] = __ldg(tw + p * step);
+    for (int p = 1; p < 16; ++p) w[p] = tw(p * step);
 #endif
 #pragma unroll
     for (int p = 1; p < 16; ++p) {
@@ -165,8 +184,8 @@ __device__ __forceinline__ void stockham16(double2* s, const double2* __restrict
 }
 
 // Final Stockham pass of radix R in {2, 4, 8} (16/R butterflies per thread).
-template <int N, int SIGN, int LS, int R>
-__device__ __forceinline__ void stockham_last(double2* s, const double2* __restrict__ tw) {
+template <int N, int SIGN, int LS, int R, class TW>
+__device__ __forceinline__ void stockham_last(double2* s, const TW& tw) {
   constexpr int NB = N / 16, NBT = 16 / R;
   double2 v[16];
 #pragma unroll
@@ -181,7 +200,7 @@ __device__ __forceinline__ void stockham_last(double2* s, const double2* __restr
     const int step = k * (N / (LS * R));
 #pragma unroll
     for (int p = 1; p < R; ++p) {
-      double2 w = __ldg(tw + p * step);
+      double2 w = tw(p * step);
       if (SIGN > 0) w.y = -w.y;
       v[bb * R + p] = cmul(v[bb * R + p], w);
     }
@@ -201,23 +220,23 @@ __device__ __forceinline__ void stockham_last(double2* s, const double2* __restr
 // In-place N-point complex DFT of s (padded layout) with blockDim.x == N/16 threads.
 // SIGN = -1 forward, +1 inverse (unscaled).  tw[m] = exp(-2 pi i m / N), m < N.
 // N = 16^P * R, R in {1, 2, 4, 8}: P radix-16 passes then one radix-R pass.
-template <int N, int SIGN>
-__device__ void fft_smem(double2* s, const double2* __restrict__ tw) {
+template <int N, int SIGN, class TW>
+__device__ void fft_smem(double2* s, const TW& tw) {
   constexpr int LG = ilog2(N);
   constexpr int P = LG / 4, R = 1 << (LG % 4);
   static_assert(P >= 1 && P <= 3, "N in 2^10 .. 2^13");
-  stockham16<N, SIGN, 1>(s, tw);
-  if (P >= 2) stockham16<N, SIGN, (P >= 2 ? 16 : 1)>(s, tw);
-  if (P >= 3) stockham16<N, SIGN, (P >= 3 ? 256 : 1)>(s, tw);
+  stockham16<N, SIGN, 1, TW>(s, tw);
+  if (P >= 2) stockham16<N, SIGN, (P >= 2 ? 16 : 1), TW>(s, tw);
+  if (P >= 3) stockham16<N, SIGN, (P >= 3 ? 256 : 1), TW>(s, tw);
   constexpr int LSF = (P == 1) ? 16 : (P == 2 ? 256 : 4096);
-  if (R > 1) stockham_last<N, SIGN, LSF, (R > 1 ? R : 2)>(s, tw);
+  if (R > 1) stockham_last<N, SIGN, LSF, (R > 1 ? R : 2), TW>(s, tw);
 }
 
 // Real-FFT split + product by H + merge for the inverse (see header comment):
 // on entry s = Z = FFT_N(z); on exit s = Z' such that IFFT_N(Z') (unscaled) gives
 // N * p packed as p[2n] + i p[2n+1]; the 1/N is folded in here.
-template <int N>
-__device__ void spectrum_product(double2* s, const double2* __restrict__ H, const double2* __restrict__ tw2) {
+template <int N, class TW2>
+__device__ void spectrum_product(double2* s, const double2* __restrict__ H, const TW2& tw2) {
   const double sc = 1.0 / (double)N;   // exact (power of two)
   if (threadIdx.x == 0) {
     const double2 z0 = s[pidx(0)];
@@ -241,8 +260,8 @@ __device__ void spectrum_product(double2* s, const double2* __restrict__ H, cons
       const int kp = N - kk;
       Zk[u] = s[pidx(kk)];
       Zkp[u] = s[pidx(kp)];
-      Wk[u] = __ldg(tw2 + kk);                        // exp(-2 pi i k / 2N)
-      Wkp[u] = __ldg(tw2 + kp);
+      Wk[u] = tw2(kk);                                // exp(-2 pi i k / 2N)
+      Wkp[u] = tw2(kp);
       Hk[u] = __ldg(H + kk);
       Hkp[u] = __ldg(H + kp);
     }
@@ -286,7 +305,7 @@ __global__ void __launch_bounds__(N / 16) pc_fft_spectrum(const double* __restri
     sm[pidx(n)] = make_double2(a < K ? kr[K - 1 - a] : 0.0, b < K ? kr[K - 1 - b] : 0.0);
   }
   __syncthreads();
-  fft_smem<N, -1>(sm, tw);
+  fft_smem<N, -1>(sm, TwGlobal{tw});
   for (int k = threadIdx.x; k <= N; k += blockDim.x) {
     const double2 Zk = sm[pidx(k % N)], Zkp = sm[pidx((N - k) % N)];
     const double2 E = make_double2(0.5 * (Zk.x + Zkp.x), 0.5 * (Zk.y - Zkp.y));
@@ -304,6 +323,9 @@ __global__ void __launch_bounds__(N / 16, (N <= 4096 ? 2 : 1)) pc_fft_conv_kerne
   const ModeP& mp = e.mp[PACK];
   const int tid = threadIdx.x, nt = blockDim.x;
   const long long job = blockIdx.x;
+  double2* tw_lo = sm + (N + N / 16);                               // w^b, b < 64
+  double2* tw_hi = tw_lo + 64;                                      // w^(64 a), a < N / 64
+  for (int i = tid; i < 64 + N / 64; i += nt) tw_lo[i] = (i < 64) ? __ldg(f.tw + i) : __ldg(f.tw + 64 * (i - 64));
   const long long sig = job / e.jobs_per_sig;
   long long r0 = job % e.jobs_per_sig;
   long long w;
@@ -468,11 +490,12 @@ __global__ void __launch_bounds__(N / 16, (N <= 4096 ? 2 : 1)) pc_fft_conv_kerne
   }
   __syncthreads();
   stamp(3);
-  fft_smem<N, -1>(sm, f.tw);                                        // a5: forward
+  const TwSmem2 tws{tw_lo, tw_hi};
+  fft_smem<N, -1>(sm, tws);                                         // a5: forward
   stamp(4);
-  spectrum_product<N>(sm, f.H, f.tw2);
+  spectrum_product<N>(sm, f.H, TwGlobal{f.tw2});
   stamp(5);
-  fft_smem<N, +1>(sm, f.tw);                                        // a5: inverse
+  fft_smem<N, +1>(sm, tws);                                         // a5: inverse
   stamp(6);
   // p[q] = Re/Im of sm[q/2]; core output m (window-relative mw = m - cw0) = p[mw + K - 1]
   auto pval = [&](int q) -> double {
@@ -536,7 +559,7 @@ __global__ void __launch_bounds__(N / 16, (N <= 4096 ? 2 : 1)) pc_fft_conv_kerne
 template <int N>
 static cudaError_t launch_fft_N(int packing, const Geo& g, const Exec& e, const FftArgs& f, long long n_jobs,
                                 cudaStream_t st) {
-  const size_t smem = (size_t)(N + N / 16) * sizeof(double2);
+  const size_t smem = (size_t)(N + N / 16 + 64 + N / 64) * sizeof(double2);   // + two-level twiddles
   cudaError_t err = cudaSuccess;
   switch (packing) {
 #define PC_FFT_CASE(PK)                                                                                  \
@@ -545,6 +568,9 @@ static cudaError_t launch_fft_N(int packing, const Geo& g, const Exec& e, const 
     static int wave = -1;                                                                                \
     if (wave < 0) {                                                                                      \
       err = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);          \
+      if (err != cudaSuccess) return err;                                                                \
+      /* leave the rest of the 256 KB unified array to L1: the twiddle/spectrum tables stay cached */   \
+      err = cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, PC_FFT_CARVEOUT);  \
       if (err != cudaSuccess) return err;                                                                \
       int occ = 0, dev = 0, sms = 0;                                                                     \
       cudaGetDevice(&dev);                                                                               \
