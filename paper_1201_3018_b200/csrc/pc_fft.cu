@@ -21,6 +21,12 @@
 #define PC_FFT_PREFETCH 0   // L2 prefetch one wave ahead: measured slower on cfg3 (HBM bursts)
 #endif
 
+#ifndef PC_FFT_PEAK_U
+#define PC_FFT_PEAK_U 8
+#endif
+#ifndef PC_FFT_PACK_UB
+#define PC_FFT_PACK_UB 8
+#endif
 #ifndef PC_FFT_CARVEOUT
 #define PC_FFT_CARVEOUT 60   // % of the unified L1/shared array as shared memory
 #endif
@@ -381,7 +387,7 @@ __global__ void __launch_bounds__(N / 16, (N <= 4096 ? 2 : 1)) pc_fft_conv_kerne
   // a2/a3: block peak and c_s (Eq. (2))
   double c_s = 1.0;
   if (PACK != PACK_FULL) {
-    constexpr int U = 8;                          // 8 loads in flight per thread
+    constexpr int U = PC_FFT_PEAK_U;              // loads in flight per thread
     double mu[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) mu[u] = 0.0;
@@ -444,7 +450,7 @@ __global__ void __launch_bounds__(N / 16, (N <= 4096 ? 2 : 1)) pc_fft_conv_kerne
   // a3/a4 with every sample load of UB complex points issued before any use (latency-bound
   // otherwise); same arithmetic, in the oracle's order, as word().
   constexpr int MS = (PACK == PACK_ASYM3) ? 3 : 2;   // samples per word (full: 1, sym: 2)
-  constexpr int UB = (PACK == PACK_ASYM3) ? 3 : 4;
+  constexpr int UB = (PACK == PACK_ASYM3) ? 3 : PC_FFT_PACK_UB;
   for (int n0 = tid; n0 < N; n0 += UB * nt) {
     double xv[UB][2][MS];
 #pragma unroll
