@@ -17,9 +17,6 @@
 #include "pc_device.cuh"
 #include "pc_kernels.h"
 
-#ifndef PC_FFT_PREFETCH
-#define PC_FFT_PREFETCH 0   // L2 prefetch one wave ahead: measured slower on cfg3 (HBM bursts)
-#endif
 
 #ifndef PC_FFT_PEAK_U
 #define PC_FFT_PEAK_U 8
@@ -364,26 +361,6 @@ __global__ void __launch_bounds__(N / 16, (N <= 4096 ? 2 : 1)) pc_fft_conv_kerne
     ft[0] = sm_;
   }
   stamp(1);
-  {
-    // L2 prefetch of the input of the job one wave ahead (grid-stride by the resident CTAs),
-    // so that job's peak and packing loads hit L2.  A hint only.
-    const long long nj = e.jobs_per_sig * e.nsig, jn = job + f.wave;
-    if (PC_FFT_PREFETCH && f.wave > 0 && jn < nj) {
-      const long long sig2 = jn / e.jobs_per_sig;
-      long long r2 = jn % e.jobs_per_sig, w2;
-      if (e.b0 == 0 && r2 < f.parts0) {
-        w2 = 0;
-      } else {
-        if (e.b0 == 0) r2 -= f.parts0;
-        w2 = e.b0 + (e.b0 == 0 ? 1 : 0) + r2 / f.parts1;
-      }
-      const long long g2 = (w2 == 0) ? 0 : w2 * (long long)g.W - 2;
-      const long long av = g.L - g2;
-      const int nv2 = (int)(av < 0 ? 0 : (av > g.W_block ? g.W_block : av));
-      const double* src2 = e.s + sig2 * e.s_stride + (g2 - e.s_off);
-      for (int i = tid * 16; i < nv2; i += nt * 16) asm volatile("prefetch.global.L2 [%0];" ::"l"(src2 + i));
-    }
-  }
   // a2/a3: block peak and c_s (Eq. (2))
   double c_s = 1.0;
   if (PACK != PACK_FULL) {
