@@ -548,22 +548,16 @@ static cudaError_t launch_fft_N(int packing, const Geo& g, const Exec& e, const 
 #define PC_FFT_CASE(PK)                                                                                  \
   case PK: {                                                                                             \
     auto kfn = pc_fft_conv_kernel<PK, N>;                                                               \
-    static int wave = -1;                                                                                \
-    if (wave < 0) {                                                                                      \
+    static bool set = false;                                                                             \
+    if (!set) {                                                                                          \
       err = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);          \
       if (err != cudaSuccess) return err;                                                                \
-      /* leave the rest of the 256 KB unified array to L1: the twiddle/spectrum tables stay cached */   \
+      /* leave the rest of the 256 KB unified array to L1: the spectrum tables stay cached */           \
       err = cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, PC_FFT_CARVEOUT);  \
       if (err != cudaSuccess) return err;                                                                \
-      int occ = 0, dev = 0, sms = 0;                                                                     \
-      cudaGetDevice(&dev);                                                                               \
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);                                 \
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, N / 16, smem) != cudaSuccess) occ = 0; \
-      wave = occ * sms;                                                                                  \
+      set = true;                                                                                        \
     }                                                                                                    \
-    FftArgs fw = f;                                                                                      \
-    fw.wave = wave;                                                                                      \
-    kfn<<<(unsigned)n_jobs, N / 16, smem, st>>>(g, e, fw);                                              \
+    kfn<<<(unsigned)n_jobs, N / 16, smem, st>>>(g, e, f);                                              \
     break;                                                                                               \
   }
     PC_FFT_CASE(PACK_FULL)

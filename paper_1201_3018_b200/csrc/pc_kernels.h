@@ -82,7 +82,6 @@ struct FftArgs {
   double* resid;         // plan-owned max last-digit residual (LSB), atomicMax on the bits
   int part0_out, part_out;   // core outputs of a block's first / later parts
   long long parts0, parts1;  // parts of block 0 / of every other block
-  long long wave;            // resident CTAs of the launch (L2 prefetch distance, jobs), 0 = none
 };
 cudaError_t launch_fft_conv(int packing, int N, const Geo& g, const Exec& e, const FftArgs& f, long long n_jobs,
                             cudaStream_t st);
