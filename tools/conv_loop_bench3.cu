@@ -40,6 +40,39 @@ __device__ __forceinline__ void core(uint32_t xs_row, uint32_t kr_addr, int n_ta
   }
 }
 
+
+// V2: the T new words of iteration j0+T are loaded at the start of iteration j0 (a full
+// iteration of latency cover), taps one pair ahead; registers: acc T + window T + next T.
+template <int T>
+__device__ __forceinline__ void core_v2(uint32_t xs_row, uint32_t kr_addr, int n_taps, double (&acc)[T]) {
+  double win[T], nxt[T];
+#pragma unroll
+  for (int c = 0; c < T - 1; ++c) win[c] = lds64(xs_row + 8u * c);
+  // new words of iteration 0: x[T-1+u]
+#pragma unroll
+  for (int u = 0; u < T; ++u) nxt[u] = lds64(xs_row + 8u * (((T - 1 + u) / T) * (T + 1) + (T - 1 + u) % T));
+  uint32_t xa = xs_row, ka = kr_addr;
+  double2 kp = lds128(ka);
+  for (int j0 = 0; j0 < n_taps; j0 += T, xa += 8u * (T + 1), ka += 8u * T) {
+    double cur[T];
+#pragma unroll
+    for (int u = 0; u < T; ++u) cur[u] = nxt[u];
+    if (j0 + T < n_taps) {
+#pragma unroll
+      for (int u = 0; u < T; ++u)
+        nxt[u] = lds64(xa + 8u * (T + 1) + 8u * (((T - 1 + u) / T) * (T + 1) + (T - 1 + u) % T));
+    }
+#pragma unroll
+    for (int u = 0; u < T; ++u) {
+      const double k = (u & 1) ? kp.y : kp.x;
+      if (u & 1) kp = lds128(ka + 8u * (u + 1));     // next pair (the last one reads the next iteration's)
+      win[(T - 1 + u) % T] = cur[u];
+#pragma unroll
+      for (int i = 0; i < T; ++i) acc[i] = fma(win[(i + u) % T], k, acc[i]);
+    }
+  }
+}
+
 template <int T, int V, int NREG>
 __global__ void __maxnreg__(NREG) loop_kernel(int K_pad, int rows, int groups, int reps, double* out) {
   extern __shared__ double sm[];
@@ -54,7 +87,8 @@ __global__ void __maxnreg__(NREG) loop_kernel(int K_pad, int rows, int groups, i
       double acc[T];
 #pragma unroll
       for (int i = 0; i < T; ++i) acc[i] = 0.0;
-      core<T, V>(smem_u32(xs) + 8u * (T + 1) * g, smem_u32(kr), K_pad, acc);
+      if (V == 2) core_v2<T>(smem_u32(xs) + 8u * (T + 1) * g, smem_u32(kr), K_pad, acc);
+      else core<T, V>(smem_u32(xs) + 8u * (T + 1) * g, smem_u32(kr), K_pad, acc);
 #pragma unroll
       for (int i = 0; i < T; ++i) tot += acc[i];
     }
@@ -90,18 +124,11 @@ int main() {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   double* dout;
   cudaMalloc(&dout, 8192 * 8);
-  for (int th : {128, 256, 512}) {
-    run<14, 0, 96>(th, 513, dout, sms);
-    run<14, 1, 96>(th, 513, dout, sms);
-    run<16, 0, 96>(th, 513, dout, sms);
-    run<16, 1, 96>(th, 513, dout, sms);
-    run<12, 0, 96>(th, 513, dout, sms);
-    run<12, 1, 96>(th, 513, dout, sms);
-  }
-  for (int th : {128, 256, 512}) {
-    run<16, 1, 128>(th, 513, dout, sms);
-    run<20, 1, 128>(th, 513, dout, sms);
-    run<24, 1, 128>(th, 513, dout, sms);
+  for (int th : {128, 256, 384, 512}) {
+    run<14, 0, 128>(th, 513, dout, sms);
+    run<14, 2, 128>(th, 513, dout, sms);
+    run<16, 0, 128>(th, 513, dout, sms);
+    run<16, 2, 128>(th, 513, dout, sms);
   }
   return 0;
 }
