@@ -322,7 +322,6 @@ template <int PACK, int N>
 __global__ void __launch_bounds__(N / 16, (N <= 4096 ? 2 : 1)) pc_fft_conv_kernel(Geo g, Exec e, FftArgs f) {
   extern __shared__ __align__(16) double2 sm[];
   __shared__ double red[32];
-  __shared__ double bx[2];
   const ModeP& mp = e.mp[PACK];
   const int tid = threadIdx.x, nt = blockDim.x;
   const long long job = blockIdx.x;
@@ -535,7 +534,6 @@ __global__ void __launch_bounds__(N / 16, (N <= 4096 ? 2 : 1)) pc_fft_conv_kerne
       atomicMax(reinterpret_cast<unsigned long long*>(f.resid), (unsigned long long)__double_as_longlong(resid));
   }
   stamp(7);
-  (void)bx;
 }
 
 // ------------------------------------------------------------------ launchers

@@ -1,22 +1,26 @@
 // pc_tiled.cu -- the production kernel of the packed overlap-save path (arXiv 1201.3018):
-// persistent, warp-specialized, (block, output-tile) jobs, tap-chunked shared-memory stages.
+// one persistent CTA per SM, warp-specialized, (block, output-tile) jobs in per-SM queues.
 //
 // Job = (signal, overlap-save block w, tile t).  Tile t covers core outputs
-// [t*G*T, (t+1)*G*T) of block w (G consumer threads, T outputs each).  The core taps are
-// processed in chunks of KC (one chunk, taps resident in shared memory, whenever they fit),
-// so any kernel length runs: cfg2's 513 taps in one chunk, cfg3/cfg4's 4097/8193 in several.
+// [t*G*T, (t+1)*G*T) of block w (G = 32 npart groups of T outputs; npart warp parts).  The
+// core taps are processed in chunks of KC (one chunk, taps resident in shared memory, when
+// they fit), so any kernel length runs: cfg2's 513 taps in one chunk, cfg3/cfg4's 4097/8193
+// in several.
 //
-//   producer warps  a2-a4: block peak (coalesced loads + shuffles; reused across the tiles
-//                   of one block), companding (Eq. (2)), packing (Eq. (4) / Eq. (7)) of the
-//                   words one (tile, chunk) needs into a shared-memory stage; non-resident
-//                   tap chunks arrive by TMA bulk copy on the same mbarrier
-//   consumer warps  a5: the FP64 core (conv_chunk_padded, accumulators live across chunks);
-//                   a6-a7: unpacking, inverse companding and placement from registers
+//   producer warps  a2-a4: job m is produced by warp m mod 4 -- block peak (coalesced loads
+//                   + shuffles; reused across the tiles of one block), companding (Eq. (2)),
+//                   packing (Eq. (4) / Eq. (7)) of the words one (tile, chunk) needs into a
+//                   stage of the ring; non-resident tap chunks arrive by TMA bulk copy on the
+//                   stage's mbarrier
+//   consumer warps  a5: the FP64 core (conv_chunk_padded, accumulators live across chunks)
+//                   on one 32-group part of a job; a6-a7: unpacking, inverse companding and
+//                   placement through per-warp staging rows, coalesced stores
 //
-// Stages (2) are handed over with mbarriers: full (producers -> consumers, + TMA bytes) and
-// empty (consumers -> producers).  Symmetric packing needs B of the word before the tile for
-// the tile's first even output: consumer warp 0 computes that one extra core output by a
-// warp-split dot product (exact under the dyadic eps, reading C4).
+// Stages are handed over with mbarriers (full: producer -> consumers, + TMA bytes; empty:
+// the job's part warps -> producers) and stamped with their sequence number.  Warp parts are
+// bound to SM sub-partitions (part k of the job sequence runs on SMSP k mod 4).  Symmetric
+// packing needs B of the word before each warp's first group: that warp computes the one
+// extra core output by a warp-split dot product (exact under the dyadic eps, reading C4).
 #include <cstdio>
 
 #include "pc_device.cuh"
@@ -32,7 +36,6 @@ struct TSmem {
   long long seq[kTiledMaxStages];   // stage sequence number the slot holds
   double inv[kTiledMaxStages];      // (c_s c_k)^-1 of the stage's block (Eq. (16))
   int smsp_ctr[4];                  // consumer warp-job claim counters, one per SM sub-partition
-  long long prod_job;
   long long turn;                   // next job sequence to claim (claims happen in sequence order)
   long long fjob[16];               // pipeline fill: jobs of sequences 0 .. nf-1
   double fcs[16], finv[16];         // their c_s and (c_s c_k)^-1
