@@ -46,10 +46,13 @@ WORKLOADS = {
     "cfg2": (4096, {"asym2_10b": (ASYM2, 511, 1, DIRECT), "asym2_8b": (ASYM2, 127, 1, DIRECT),
                     "asym3_8b": (ASYM3, 127, 1, DIRECT), "sym_8b": (SYM, 127, 1, DIRECT),
                     "sym_6b": (SYM, 31, 1, DIRECT), "full": (FULL, 0, 0, DIRECT)}, "asym2_10b", "full"),
+    # cfg3's full-precision reference as configured (BASELINE.json: the block's 32768-point
+    # transform) is full_fft32k; full_fft is the fair circular n = 16384 overlap-save
     "cfg3": (16384, {"asym2_9b_fft": (ASYM2, 255, 1, FFT), "asym2_8b_fft": (ASYM2, 127, 1, FFT),
-                     "sym_q12_fft": (SYM, 12, 1, FFT), "full_fft": (FULL, 0, 0, FFT),
+                     "sym_q12_fft": (SYM, 12, 1, FFT), "full_fft32k": (FULL, 0, 0, FFT, {4: 16384}),
+                     "full_fft": (FULL, 0, 0, FFT),
                      "asym2_9b_direct": (ASYM2, 255, 1, DIRECT), "full_direct": (FULL, 0, 0, DIRECT)},
-             "asym2_9b_fft", "full_fft"),
+             "asym2_9b_fft", "full_fft32k"),
     "cfg4": (32768, {"asym2_8b": (ASYM2, 127, 1, DIRECT), "sym_q7": (SYM, 7, 1, DIRECT),
                      "full": (FULL, 0, 0, DIRECT)}, "asym2_8b", "full"),
     "cfg5": (4096, {"adapt_40db": (4, 40.0, 1, DIRECT), "adapt_50db": (4, 50.0, 1, DIRECT),
@@ -215,7 +218,7 @@ def cpu_baseline(s, k, W_block, point, target_s=12.0):
     """The oracle as it stands, on a bounded sample of the same workload: consecutive
     blocks from block 1 until ~target_s seconds of CPU work; value = output samples/s."""
     import oracle as O
-    packing, Q, rmax, _ = point
+    packing, Q, rmax = point[:3]
     if packing not in (FULL, SYM, ASYM2, ASYM3):
         packing, Q, rmax = FULL, 0, 0
     geom = O.Geometry(len(s), len(k), W_block)
@@ -238,7 +241,7 @@ def run_reference(args, ws, rank):
     W_block, points, head, _ = WORKLOADS[args.workload]
     s, k, _, nsig, _ = workload(args.workload if args.workload != "cfg4" else "cfg2", 0, 1, args)
     import oracle as O
-    packing, Q, rmax, _ = points[head]
+    packing, Q, rmax = points[head][:3]
     if packing not in (FULL, SYM, ASYM2, ASYM3):
         packing, Q, rmax = ASYM2, 535, 1
     geom = O.Geometry(len(s), len(k), W_block if args.workload != "cfg4" else 4096)
@@ -287,10 +290,13 @@ def run_ours(args, ws, rank, local):
     results, outputs = {}, {}
     sampler_summary = None
     for name in sel:
-        packing, Q, rmax, core = points[name]
+        packing, Q, rmax, core = points[name][:4]
+        extra_opts = points[name][4] if len(points[name]) > 4 else {}
         adaptive = packing == 4
         opts = pcb.opts_default(rmax_rule=rmax, core=core, exec=0 if args.exec == "fused" else 1)
         opts.reserved[3] = args.force_warps
+        for i, v in extra_opts.items():
+            opts.reserved[i] = v
         for kv in args.opt:
             i, v = kv.split("=")
             opts.reserved[int(i)] = int(v)
@@ -460,6 +466,8 @@ def run_ours(args, ws, rank, local):
         "roofline": roof,
         "e2e": h.get("e2e"),
         "packed_vs_full": (h["value"] / full["value"]) if full else None,
+        "packed_vs_full_fair": (h["value"] / results["full_fft"]["value"]) if args.workload == "cfg3" and
+        "full_fft" in results else None,
         "full_precision": full,
         "points": results,
         "clocks": sampler_summary,

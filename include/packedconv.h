@@ -73,7 +73,9 @@ typedef struct conv_opts {
                                [1]: force the persistent core tile (12/14/16; tests);
                                [2]: unused;
                                [3]: force consumer warps per job (1, 2, 4; diagnostics);
-                               [4]: force the FFT size N (complex points, 1024..8192);
+                               [4]: force the FFT size N (complex points, 1024..8192; 16384 =
+                                    the 32768-point real transform of the whole block, full
+                                    precision, W_block <= 16386, 2-CTA clusters);
                                [5]: unpack form, 0 balanced digits (C6), 1 the literal
                                     Eqs. (11)-(15) with the u_sys guard (symmetric packing,
                                     direct core; exact for R_max < 89,524, reading C6); rest 0 */

@@ -302,6 +302,9 @@ int choose_fft_N(const conv_plan* p, int packing) {
   const int K = core_taps(p, packing);
   const int force = p->opts.reserved[4];            // diagnostics: complex points N
   if (force == 1024 || force == 2048 || force == 4096 || force == 8192) return 2 * force - K >= 1 ? force : 0;
+  // 32768-point real transform of the whole block (cfg3's configured full-precision core):
+  // full precision, windows of at most 16384 real words (2-CTA cluster kernel)
+  if (force == 16384) return (packing == PC_PACK_FULL && p->W_block <= 16386) ? 16384 : 0;
   int best_N = 0;
   double best = 0.0;
   for (int N = 1024, lg = 10; N <= 8192; N *= 2, ++lg) {

@@ -14,8 +14,12 @@
 //
 // Twiddles come from tables rounded once from long-double values on the host (recurrences
 // break exactness at cfg3 sizes).
+#include <cooperative_groups.h>
+
 #include "pc_device.cuh"
 #include "pc_kernels.h"
+
+namespace cg = cooperative_groups;
 
 
 #ifndef PC_FFT_PEAK_U
@@ -536,6 +540,160 @@ __global__ void __launch_bounds__(N / 16, (N <= 4096 ? 2 : 1)) pc_fft_conv_kerne
   stamp(7);
 }
 
+// ------------------------------------------------------------------ n = 32768 (full precision)
+// The configured full-precision core of cfg3 (BASELINE.json configs[2]: the block's linear
+// convolution through a 32768-point real transform, SURVEY §8(d) "G6").  Its 16384 complex
+// points (256 KB) exceed one CTA's shared memory, so a 2-CTA cluster shares the work: the
+// window's data occupy only the first 8192 complex points (16384 real words; the rest is zero
+// padding), so Z[2k'+r] = FFT_8192(z[n] W^{nr})[k'] (W = exp(-2 pi i/16384)) -- CTA r computes
+// parity class r with no exchange; the real-transform split pairs k with 16384-k, which has
+// the same parity, so the spectrum product is local too; the inverse gives q_r = IFFT_8192 of
+// each class and p[n] = q_0[n] + W^{-n} q_1[n], formed by CTA 0 reading CTA 1's shared memory
+// (DSMEM).  Twiddles: tw[m] = W^m (m < 16384); the 8192-point passes use W^{2m}.
+namespace {
+constexpr int kN32 = 8192;                 // complex points per CTA
+constexpr int kN32Full = 2 * kN32;         // complex points of the transform (real length 32768)
+
+struct TwStride2 {                         // w_8192^m = W^{2m} from the 16384-entry table, two-level in smem
+  const double2* lo;                       // lo[b] = W^{2b}, b < 64
+  const double2* hi;                       // hi[a] = W^{128 a}, a < 128
+  __device__ __forceinline__ double2 operator()(int m) const { return cmul(hi[m >> 6], lo[m & 63]); }
+};
+
+// Parity-class partner of local index k' (global k = 2k'+r): 16384 - k is 2k''+r.
+__device__ __forceinline__ int partner32(int kl, int r) { return r == 0 ? ((kN32 - kl) & (kN32 - 1)) : (kN32 - 1 - kl); }
+}  // namespace
+
+__global__ void __launch_bounds__(kN32 / 16) pc_fft32k_spectrum(const double* __restrict__ kr, int K,
+                                                              const double2* __restrict__ tw,
+                                                              const double2* __restrict__ tw2,
+                                                              double2* __restrict__ H) {
+  extern __shared__ __align__(16) double2 sm[];
+  const int r = blockIdx.x;                 // parity class
+  double2* lo = sm + (kN32 + kN32 / 16);
+  double2* hi = lo + 64;
+  for (int i = threadIdx.x; i < 64 + kN32 / 64; i += blockDim.x)
+    lo[i] = (i < 64) ? __ldg(tw + 2 * i) : __ldg(tw + 128 * (i - 64));
+  for (int n = threadIdx.x; n < kN32; n += blockDim.x) {   // h[n] = kr[K-1-n]; z[n] W^{nr}
+    const int a = 2 * n, b = 2 * n + 1;
+    double2 z = make_double2(a < K ? kr[K - 1 - a] : 0.0, b < K ? kr[K - 1 - b] : 0.0);
+    if (r) z = cmul(z, __ldg(tw + n));
+    sm[pidx(n)] = z;
+  }
+  __syncthreads();
+  fft_smem<kN32, -1>(sm, TwStride2{lo, hi});
+  // X[k] = E[k] + W2^k O[k] for k = 2k'+r (k = 0 .. 16384; k = 16384 is class 0, k' = 8192 = 0)
+  for (int kl = threadIdx.x; kl <= (r == 0 ? kN32 : kN32 - 1); kl += blockDim.x) {
+    const int k = 2 * kl + r;
+    const double2 Zk = sm[pidx(kl & (kN32 - 1))], Zkp = sm[pidx(partner32(kl & (kN32 - 1), r))];
+    const double2 E = make_double2(0.5 * (Zk.x + Zkp.x), 0.5 * (Zk.y - Zkp.y));
+    const double2 O = make_double2(0.5 * (Zk.y + Zkp.y), -0.5 * (Zk.x - Zkp.x));
+    H[k] = cadd(E, cmul(__ldg(tw2 + k), O));
+  }
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kN32 / 16, 1)
+    pc_fft32k_full_kernel(Geo g, Exec e, FftArgs f) {
+  extern __shared__ __align__(16) double2 sm[];
+  const ModeP& mp = e.mp[PACK_FULL];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const unsigned r = cg::this_cluster().block_rank();
+  const long long job = blockIdx.x >> 1;
+  const long long sig = job / e.jobs_per_sig;
+  const long long w = e.b0 + job % e.jobs_per_sig;
+  double2* lo = sm + (kN32 + kN32 / 16);
+  double2* hi = lo + 64;
+  for (int i = tid; i < 64 + kN32 / 64; i += nt) lo[i] = (i < 64) ? __ldg(f.tw + 2 * i) : __ldg(f.tw + 128 * (i - 64));
+  const Blk b = block_info<PACK_FULL>(g, mp.K, w);
+  const double* gsrc = e.s + sig * e.s_stride + (b.g0 - e.s_off);
+  const long long avail = g.L - b.g0;
+  const int n_valid = (int)(avail < 0 ? 0 : (avail > g.W_block ? g.W_block : avail));
+  // window = core words [cw0, xlen): block 0 skips its N'-1 zero prefix, so every window holds
+  // at most W_block = 16384 real words (the first 8192 complex points)
+  const int cw0 = (w == 0) ? g.Np - 1 : 0;
+  const int wlen = b.xlen - cw0;
+  auto word = [&](int i) -> double {
+    const int idx = b.o0 - (g.Np - 1) + cw0 + i;
+    return (i < wlen && idx >= 0 && idx < n_valid) ? __ldg(gsrc + idx) : 0.0;
+  };
+  constexpr int UB = 8;
+  for (int n0 = tid; n0 < kN32; n0 += UB * nt) {
+    double2 z[UB];
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {
+      const int n = n0 + u * nt;
+      z[u] = (n < kN32) ? make_double2(word(2 * n), word(2 * n + 1)) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {
+      const int n = n0 + u * nt;
+      if (n < kN32) sm[pidx(n)] = r ? cmul(z[u], __ldg(f.tw + n)) : z[u];
+    }
+  }
+  __syncthreads();
+  const TwStride2 tws{lo, hi};
+  fft_smem<kN32, -1>(sm, tws);                                      // a5: Z[2k'+r]
+  // spectrum product by H (real-transform split/merge), pairs (k, 16384-k) of this class
+  const double sc = 1.0 / (double)kN32Full;
+  if (r == 0 && tid == 0) {
+    const double2 z0 = sm[pidx(0)];
+    const double X0 = z0.x + z0.y, XN = z0.x - z0.y;
+    const double2 H0 = __ldg(f.H), HN = __ldg(f.H + kN32Full);
+    const double2 P0 = make_double2(X0 * H0.x, X0 * H0.y);
+    const double2 PN = make_double2(XN * HN.x, XN * HN.y);
+    const double2 ee = make_double2(0.5 * (P0.x + PN.x), 0.5 * (P0.y - PN.y));
+    const double2 oo = make_double2(0.5 * (P0.x - PN.x), 0.5 * (P0.y + PN.y));
+    sm[pidx(0)] = make_double2((ee.x - oo.y) * sc, (ee.y + oo.x) * sc);
+  }
+  const int klo = (r == 0) ? 1 : 0, khi = (r == 0) ? kN32 / 2 : kN32 / 2 - 1;   // k' <= partner
+  for (int kl = klo + tid; kl <= khi; kl += nt) {
+    const int kp_l = partner32(kl, r);
+    const int k = 2 * kl + (int)r, kp = kN32Full - k;
+    const double2 Zk = sm[pidx(kl)], Zkp = sm[pidx(kp_l)];
+    const double2 Wk = __ldg(f.tw2 + k), Wkp = __ldg(f.tw2 + kp);
+    const double2 Ek = make_double2(0.5 * (Zk.x + Zkp.x), 0.5 * (Zk.y - Zkp.y));
+    const double2 Ok = make_double2(0.5 * (Zk.y + Zkp.y), -0.5 * (Zk.x - Zkp.x));
+    const double2 Xk = cadd(Ek, cmul(Wk, Ok));
+    const double2 Xkp = cadd(cconj(Ek), cmul(Wkp, cconj(Ok)));
+    const double2 Pk = cmul(Xk, __ldg(f.H + k)), Pkp = cmul(Xkp, __ldg(f.H + kp));
+    auto merge = [&](double2 a, double2 bb, double2 W) {
+      const double2 ee = make_double2(0.5 * (a.x + bb.x), 0.5 * (a.y - bb.y));
+      const double2 d = make_double2(0.5 * (a.x - bb.x), 0.5 * (a.y + bb.y));
+      const double2 o = cmul(d, cconj(W));
+      return make_double2((ee.x - o.y) * sc, (ee.y + o.x) * sc);
+    };
+    const double2 Zpk = merge(Pk, Pkp, Wk);
+    const double2 Zpkp = merge(Pkp, Pk, Wkp);
+    sm[pidx(kl)] = Zpk;
+    if (kp_l != kl) sm[pidx(kp_l)] = Zpkp;
+  }
+  __syncthreads();
+  fft_smem<kN32, +1>(sm, tws);                                      // q_r = IFFT_8192 (unscaled)
+  cg::this_cluster().sync();                                        // both classes ready
+  if (r == 0) {
+    const double2* q1 = cg::this_cluster().map_shared_rank(sm, 1);   // CTA 1's q_1 (DSMEM)
+    double* __restrict__ out = e.r + sig * e.r_stride;
+    const long long gbase = b.g0 + b.o0;
+    const long long L_conv = g.L + g.N - 1;
+    const int K1 = mp.K - 1;
+    for (int m = tid; m < b.M_out; m += nt) {
+      const int q = m - cw0 + K1;                                   // p index of core output m
+      const int n = q >> 1;
+      const double2 a = sm[pidx(n)], c = q1[pidx(n)];
+      const double2 p = cadd(a, cmul(c, cconj(__ldg(f.tw + n))));  // q_0 + W^{-n} q_1
+      const double v = (q & 1) ? p.y : p.x;
+      const long long gg = gbase + m;
+      if (g.mode == 0) {
+        if (m < b.n_out && gg < L_conv) out[gg - e.r_off] = v;
+      } else {
+        const long long j = gg - (g.N - 1);                         // valid lag (C17)
+        if (m < b.n_out && j >= 0 && j <= g.L - g.N) out[j - e.r_off] = v;
+      }
+    }
+  }
+  cg::this_cluster().sync();                                        // CTA 1's shared memory stays valid
+}
+
 // ------------------------------------------------------------------ launchers
 template <int N>
 static cudaError_t launch_fft_N(int packing, const Geo& g, const Exec& e, const FftArgs& f, long long n_jobs,
@@ -576,6 +734,19 @@ cudaError_t launch_fft_conv(int packing, int N, const Geo& g, const Exec& e, con
     case 2048: return launch_fft_N<2048>(packing, g, e, f, n_jobs, st);
     case 4096: return launch_fft_N<4096>(packing, g, e, f, n_jobs, st);
     case 8192: return launch_fft_N<8192>(packing, g, e, f, n_jobs, st);
+    case 16384: {                                         // full precision only (2-CTA clusters)
+      if (packing != PACK_FULL) return cudaErrorInvalidValue;
+      const size_t smem = (size_t)(kN32 + kN32 / 16 + 64 + kN32 / 64) * sizeof(double2);
+      static bool set = false;
+      if (!set) {
+        cudaError_t err = cudaFuncSetAttribute(pc_fft32k_full_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)smem);
+        if (err != cudaSuccess) return err;
+        set = true;
+      }
+      pc_fft32k_full_kernel<<<(unsigned)(2 * n_jobs), kN32 / 16, smem, st>>>(g, e, f);
+      return cudaGetLastError();
+    }
   }
   return cudaErrorInvalidValue;
 }
@@ -598,6 +769,13 @@ cudaError_t launch_fft_spectrum(int N, const double* kr, int K, const double2* t
     case 2048: return launch_spec_N<2048>(kr, K, tw, tw2, H, st);
     case 4096: return launch_spec_N<4096>(kr, K, tw, tw2, H, st);
     case 8192: return launch_spec_N<8192>(kr, K, tw, tw2, H, st);
+    case 16384: {
+      const size_t smem = (size_t)(kN32 + kN32 / 16 + 64 + kN32 / 64) * sizeof(double2);
+      cudaError_t err = cudaFuncSetAttribute(pc_fft32k_spectrum, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (err != cudaSuccess) return err;
+      pc_fft32k_spectrum<<<2, kN32 / 16, smem, st>>>(kr, K, tw, tw2, H);
+      return cudaGetLastError();
+    }
   }
   return cudaErrorInvalidValue;
 }

@@ -511,6 +511,33 @@ def test_fft_full_precision(case):
     assert np.max(np.abs(got - want)) / np.max(np.abs(want)) < 1e-12
 
 
+@pytest.mark.parametrize("mode", [O.CONV, O.XCORR])
+@pytest.mark.parametrize("case", [(1 << 18, 4096, 16384), (100_000, 1000, 8192), (40_000, 3000, 16384),
+                                  (20_000, 4096, 16384)])
+def test_fft32k_configured_full_precision(case, mode):
+    """cfg3's configured full-precision core: the block's linear convolution through a
+    32768-point real transform (conv_opts.reserved[4] = 16384), computed by 2-CTA clusters
+    (parity classes, DSMEM combine).  Within 1e-12 normalized of the direct FP64 result,
+    including block 0 (zero prefix skipped), ragged tails and xcorr placement."""
+    L, N, W_block = case
+    rng = np.random.default_rng(N + L)
+    s, k = rng.laplace(0, 0.2, L), rng.normal(0, 1 / np.sqrt(N), N)
+    opts = pcb.opts_default(core=1)
+    opts.reserved[4] = 16384
+    with pcb.Plan(L, N, W_block, pcb.MODE_XCORR if mode == O.XCORR else pcb.MODE_CONV, pcb.PACK_FULL, 0,
+                  opts=opts) as p:
+        p.set_kernel(dev(k))
+        info = p.info()
+        assert info["fft_n"] == 16384
+        r = torch.full((info["L_out"],), float("nan"), dtype=torch.float64, device=DEV)
+        p.execute(dev(s), r)
+        torch.cuda.synchronize()
+        got = r.cpu().numpy()
+    want = O.full_precision(s, k, mode=mode)
+    assert not np.isnan(got).any()
+    assert np.max(np.abs(got - want)) / np.max(np.abs(want)) < 1e-12
+
+
 @pytest.mark.parametrize("packing,Q", [(O.ASYM2, 127), (O.ASYM2, 255), (O.ASYM3, 7), (O.SYM, 7), (O.SYM, 12)])
 def test_fft_packed_exact_cfg3_geometry(packing, Q):
     """Config 3 geometry (N = 4096, W_block = 16384) on a 2^18-sample slice: the FFT core's
