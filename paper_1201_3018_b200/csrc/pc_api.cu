@@ -813,9 +813,16 @@ int conv_execute_host(conv_plan* p, const double* s_host, double* r_host, void* 
   // Chunk weights: small first and last ranges shorten the pipeline ramp (the first H2D and
   // the last D2H are not overlapped).
   static const int kW[9] = {1, 2, 4, 4, 4, 4, 4, 2, 1};
-  const int nchunk = (p->packing == PC_PACK_ADAPTIVE || p->P < 128) ? 1 : 9;
-  long long cum[10] = {0};
+  int nchunk = (p->packing == PC_PACK_ADAPTIVE || p->P < 128) ? 1 : 9;
+  long long cum[33] = {0};
   for (int i = 0; i < 9; ++i) cum[i + 1] = cum[i] + kW[i];
+  if (const char* ev = std::getenv("PC_HOST_CHUNKS")) {         // diagnostics: n equal ranges
+    const int n = std::atoi(ev);
+    if (n >= 1 && n <= 16 && nchunk > 1) {            // (16 event pairs)
+      nchunk = n;
+      for (int i = 0; i <= n; ++i) cum[i] = i;
+    }
+  }
   if (nchunk <= 1) {
     if (cudaMemcpyAsync(p->d_in, s_host, sizeof(double) * p->L, cudaMemcpyHostToDevice, st) != cudaSuccess)
       return PC_E_CUDA;
@@ -844,7 +851,7 @@ int conv_execute_host(conv_plan* p, const double* s_host, double* r_host, void* 
   const long long W = p->W, Wb = p->W_block, Np = p->Np;
   long long in_done = 0, out_done = 0;
   for (int c = 0; c < nchunk; ++c) {
-    const long long b0 = p->P * cum[c] / cum[9], b1 = p->P * cum[c + 1] / cum[9];
+    const long long b0 = p->P * cum[c] / cum[nchunk], b1 = p->P * cum[c + 1] / cum[nchunk];
     if (b1 <= b0) continue;
     const long long last = b1 - 1;
     long long in_end = (last == 0 ? 0 : last * W - 2) + Wb;            // block `last` reads up to here

@@ -434,7 +434,9 @@ __global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec 
 
   // Pipeline fill: the first nf jobs (one per producer warp when a job is one stage) are
   // claimed in parallel, then companded and packed by all warps, five warps per job.
-  const int nf = (nch == 1) ? min(kTiledFillJobs, NS) : 1;
+  // (never more than a CTA's share of the launch: small launches spread over all CTAs)
+  const long long share = (njobs + gridDim.x - 1) / gridDim.x;
+  const int nf = (nch == 1) ? (int)min((long long)min(kTiledFillJobs, NS), share < 1 ? 1 : share) : 1;
   const int lane_ = tid & 31, warp_ = tid >> 5;
   if (warp_ < nf) {
     const long long j = claim_job(e, njobs, lane_);

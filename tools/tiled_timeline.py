@@ -96,7 +96,8 @@ for name, (pk, Q, rm) in points.items():
         return {"produced[mseq,t_pub]": sorted(prod), "consumed[warp,mseq,t_ready,t_core,t_stored]": sorted(cons, key=lambda x: x[2])}
     fill_phases = (Pr[:, :, 15, :3].astype(float) - r[:, 1][:, None, None]) / 1e3   # claimed, peak, packed (us)
     fill_stats = {k: round(float(np.median(fill_phases[:, :, i])), 2) for i, k in enumerate(["claimed", "peak", "packed"])}
-    out[name] = {"zero_core_time_split": zsplit, "fill_phases_us_median": fill_stats, "smsp_warps_in_core_time_frac": hist_core, "cta0": cta_trace(0), "grid": g, "tile": info["core_tile"], "kernel_us": float(T_end),
+    crit = int(np.argmax(r[:, 2]))                  # the CTA that ends last
+    out[name] = {"cta_last": crit, "cta_last_trace": cta_trace(crit), "zero_core_time_split": zsplit, "fill_phases_us_median": fill_stats, "smsp_warps_in_core_time_frac": hist_core, "cta0": cta_trace(0), "grid": g, "tile": info["core_tile"], "kernel_us": float(T_end),
                  "start_spread_us": float(st.max()), "sm_end_min_us": float(sm_end.min()),
                  "sm_end_median_us": float(np.median(sm_end)), "sm_end_max_us": float(sm_end.max()),
                  "resident_ctas_per_sm_time_frac": hist,
