@@ -484,12 +484,11 @@ def run_ours(args, ws, rank, local):
                 "traffic": None, "kernel": "pc_fft_conv_kernel" if h["core"] == "fft" else "pc_fused_kernel",
                 "algorithmic": "8 B read + 8 B written per sample"}
     # our kernels per step: adaptive = block stats + decide + lists + one tiled launch per packing;
-    # xcorr = (tiled core + score) per chunk of <= 2^28 lag outputs; otherwise one fused launch
+    # xcorr = the tiled core with the fused score epilogue + the per-signal reduction; else one
     if points[head][0] == 4:
         launches_per_step = 6
     elif xcorr:
-        per_chunk = max(1, (1 << 28) // (L - N + 1))
-        launches_per_step = 2 * (-(-nsig // per_chunk))
+        launches_per_step = 2
     else:
         launches_per_step = 1
     line = {

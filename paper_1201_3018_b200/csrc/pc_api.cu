@@ -62,6 +62,9 @@ struct conv_plan {
   double* d_in = nullptr;
   double* d_out = nullptr;
   cudaStream_t st_h2d = nullptr, st_d2h = nullptr;   // conv_execute_host pipeline (plan-owned)
+  double* d_xc_pval = nullptr;         // conv_xcorr_max fused: per warp-part partial max and its lag
+  long long* d_xc_plag = nullptr;
+  size_t xc_part_n = 0;
   cudaEvent_t ev_in[16] = {}, ev_done[16] = {}, ev_out = nullptr;
   // xcorr scratch
   double* d_xc = nullptr;
@@ -349,9 +352,35 @@ int plan_packs(const conv_plan* p, int* packs) {
   return 1;
 }
 
+// Does a (non-debug) direct-core execute of this non-adaptive plan run the tiled kernel?
+// (The per-block kernel serves small cores unless the tiled kernel is forced; see run_exec.)
+bool small_core_plan(const conv_plan* p, const int* packs, int np) {
+  for (int i = 0; i < np; ++i) {
+    int mmax, mtyp;
+    core_sizes(p, packs[i], &mmax, &mtyp);
+    if ((long long)mtyp * core_taps(p, packs[i]) >= kSmallCoreFma) return false;
+  }
+  return true;
+}
+bool forced_tiled(const conv_plan* p) {
+  return p->opts.reserved[1] != 0 || p->opts.reserved[3] != 0 || p->opts.reserved[5] == 1;
+}
+bool uses_tiled(const conv_plan* p) {
+  if (p->opts.core != PC_CORE_DIRECT || p->packing == PC_PACK_ADAPTIVE) return false;
+  if (p->opts.exec != PC_EXEC_FUSED && p->opts.exec != PC_EXEC_TILED) return false;
+  TShape ts;
+  if (!tiled_shape(p, p->packing, &ts)) return false;
+  if (p->opts.exec == PC_EXEC_TILED || forced_tiled(p)) return true;
+  int packs[4];
+  const int np = plan_packs(p, packs);
+  Shape sh;
+  return !(small_core_plan(p, packs, np) && launch_shape(p, packs, np, &sh));
+}
+
 int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride, double* r, long long r_off,
               long long r_stride, long long b0, long long nblk, long long n_sig, Exec* dbg, cudaStream_t st,
-              unsigned long long* timing = nullptr, int* grid_out = nullptr) {
+              unsigned long long* timing = nullptr, int* grid_out = nullptr, double* xc_val = nullptr,
+              long long* xc_lag = nullptr) {
   if (!p->kernel_set) return PC_E_STATE;
   if (p->packing == PC_PACK_ADAPTIVE && !p->adapt_ready) return PC_E_STATE;
   if (nblk <= 0 || n_sig <= 0) return PC_OK;
@@ -403,15 +432,9 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
   // Small cores (cfg1: 1024-sample blocks, 65 taps): a job's core is shorter than the tiled
   // kernel's per-job pipeline latency, so one CTA per block (phases in sequence) is faster
   // (measured 2x at N = 64 for 65k..1M samples; the tiled kernel wins from N = 128 at 4096).
-  bool small_core = true;
-  for (int i = 0; i < np; ++i) {
-    int mmax, mtyp;
-    core_sizes(p, packs[i], &mmax, &mtyp);
-    if ((long long)mtyp * core_taps(p, packs[i]) >= kSmallCoreFma) small_core = false;
-  }
-  const bool forced = p->opts.reserved[1] != 0 || p->opts.reserved[3] != 0 ||   // tile / parts forced,
-                      p->opts.reserved[5] == 1;                                  // literal unpack: tiled
-  if (!dbg && small_core && !forced && per_block_ok && p->opts.exec == PC_EXEC_FUSED)
+  const bool small_core = small_core_plan(p, packs, np);
+  const bool forced = forced_tiled(p);                 // tile / parts forced, literal unpack: tiled
+  if (!dbg && !xc_val && small_core && !forced && per_block_ok && p->opts.exec == PC_EXEC_FUSED)
     return cuda_status(pc::launch_fused(launch_pack, make_geo(p), e, nblk * n_sig, sh.threads, sh.smem, st));
   const bool tiled_ok = p->opts.exec == PC_EXEC_FUSED || p->opts.exec == PC_EXEC_TILED;
   if (!dbg && p->packing == PC_PACK_ADAPTIVE && tiled_ok && n_sig == 1 && b0 == 0 &&
@@ -452,6 +475,8 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
   if (!dbg && p->packing != PC_PACK_ADAPTIVE && tiled_ok && tiled_shape(p, p->packing, &ts)) {
     e.sm_ctr = p->d_counter;
     e.dbg_timing = timing;
+    e.xc_val = xc_val;
+    e.xc_lag = xc_lag;
     e.G = ts.G;
     e.nstages = ts.nstages;
     e.KC = ts.KC;
@@ -620,6 +645,8 @@ void conv_plan_destroy(conv_plan* p) {
   cudaFree(p->d_cand);
   cudaFree(p->d_in);
   cudaFree(p->d_out);
+  cudaFree(p->d_xc_pval);
+  cudaFree(p->d_xc_plag);
   for (int i = 0; i < 16; ++i) {
     if (p->ev_in[i]) cudaEventDestroy(p->ev_in[i]);
     if (p->ev_done[i]) cudaEventDestroy(p->ev_done[i]);
@@ -915,6 +942,32 @@ int conv_xcorr_max(conv_plan* p, const double* db, int64_t n_signals, int64_t s_
   if (cudaSetDevice(p->device) != cudaSuccess) return PC_E_CUDA;
   cudaStream_t st = (cudaStream_t)stream;
   const long long n_lags = p->L - p->N + 1;
+  if (uses_tiled(p) && n_signals > 0) {
+    // a9 fused: the tiled kernel's epilogue keeps each warp part's max over its
+    // valid lags (lowest lag on ties) instead of storing the lags; one launch over all
+    // signals, then a per-signal reduction of the partials.  No lag scratch.
+    TShape ts;
+    tiled_shape(p, p->packing, &ts);
+    const long long jobs_per_sig = ts.tiles0 + (p->P - 1) * ts.tiles1;
+    const long long n_part = jobs_per_sig * (ts.G / 32);
+    const size_t need = (size_t)n_signals * (size_t)n_part;
+    if (need > p->xc_part_n) {
+      cudaFree(p->d_xc_pval);
+      cudaFree(p->d_xc_plag);
+      p->d_xc_pval = nullptr;
+      p->d_xc_plag = nullptr;
+      p->xc_part_n = 0;
+      if (cudaMalloc(&p->d_xc_pval, sizeof(double) * need) != cudaSuccess) return PC_E_CUDA;
+      if (cudaMalloc(&p->d_xc_plag, sizeof(long long) * need) != cudaSuccess) return PC_E_CUDA;
+      p->xc_part_n = need;
+    }
+    int rc = run_exec(p, db, 0, s_stride, p->d_xc_pval, 0, n_lags, 0, p->P, n_signals, nullptr, st, nullptr,
+                      nullptr, p->d_xc_pval, p->d_xc_plag);
+    if (rc) return rc;
+    cudaError_t e = pc::launch_xcorr_reduce(p->d_xc_pval, p->d_xc_plag, n_signals, n_part, score,
+                                            reinterpret_cast<long long*>(lag), st);
+    return cuda_status(e);
+  }
   long long chunk = (1LL << 28) / n_lags;    // <= 2 GiB of lag scratch
   if (chunk < 1) chunk = 1;
   if (chunk > n_signals) chunk = n_signals;

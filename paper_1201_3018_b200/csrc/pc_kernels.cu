@@ -506,6 +506,53 @@ cudaError_t launch_adapt_lists(long long P, const int* dec_pack, int* lists, int
   return cudaGetLastError();
 }
 
+// Per signal: the maximum of the warp partials of the fused xcorr epilogue, lowest lag on ties.
+__global__ void pc_xcorr_reduce(const double* __restrict__ val, const long long* __restrict__ lag, long long n_part,
+                                double* __restrict__ score, long long* __restrict__ best) {
+  __shared__ double sv[32];
+  __shared__ long long sj[32];
+  const long long sig = blockIdx.x;
+  double v = -__longlong_as_double(0x7ff0000000000000LL);
+  long long j = -1;
+  for (long long i = threadIdx.x; i < n_part; i += blockDim.x) {
+    const double a = val[sig * n_part + i];
+    const long long b = lag[sig * n_part + i];
+    if (b >= 0 && (j < 0 || a > v || (a == v && b < j))) {
+      v = a;
+      j = b;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+    const long long oj = __shfl_xor_sync(0xffffffffu, j, o);
+    if (oj >= 0 && (j < 0 || ov > v || (ov == v && oj < j))) {
+      v = ov;
+      j = oj;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sv[threadIdx.x >> 5] = v;
+    sj[threadIdx.x >> 5] = j;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+      if (sj[w] >= 0 && (j < 0 || sv[w] > v || (sv[w] == v && sj[w] < j))) {
+        v = sv[w];
+        j = sj[w];
+      }
+    score[sig] = v;
+    best[sig] = j;
+  }
+}
+
+cudaError_t launch_xcorr_reduce(const double* val, const long long* lag, long long n_signals, long long n_part,
+                                double* score, long long* best, cudaStream_t st) {
+  if (n_signals <= 0) return cudaSuccess;
+  pc_xcorr_reduce<<<(unsigned)n_signals, 256, 0, st>>>(val, lag, n_part, score, best);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_xcorr_max(const double* c, long long n_signals, long long n_lags, long long stride,
                              double* score, long long* lag, cudaStream_t st) {
   pc_xcorr_max<<<(unsigned)n_signals, 1024, 0, st>>>(c, n_lags, stride, score, lag);

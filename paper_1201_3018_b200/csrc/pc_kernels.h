@@ -72,6 +72,10 @@ struct Exec {
   long long dbg_rint_stride;
   double* dbg_cs;
   unsigned long long* dbg_timing;   // persistent kernel: per CTA {smid, t_start, t_end, jobs}
+  // xcorr with fused score (tiled kernel): instead of storing the lags, every warp part writes
+  // the max over its valid lags and the lowest lag attaining it to [sig][job * npart + part]
+  double* xc_val;                    // nullptr: store the lags
+  long long* xc_lag;
 };
 
 // FFT overlap-save core (pc_fft.cu).
@@ -102,6 +106,8 @@ cudaError_t launch_adapt_decide(long long P, const double* sigma, const double* 
                                 const int* cand, const int* qmode, int ncand, double thr, int* dp, int* dq, double* ds,
                                 cudaStream_t st);
 cudaError_t launch_adapt_lists(long long P, const int* dec_pack, int* lists, int* counts, cudaStream_t st);
+cudaError_t launch_xcorr_reduce(const double* val, const long long* lag, long long n_signals, long long n_part,
+                                double* score, long long* best, cudaStream_t st);
 cudaError_t launch_xcorr_max(const double* c, long long n_signals, long long n_lags, long long stride,
                              double* score, long long* lag, cudaStream_t st);
 

@@ -678,12 +678,27 @@ __global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec 
     double* __restrict__ rsig = e.r + jp.sig * e.r_stride - e.r_off - goff;    // rsig[gg]
     const int mw = gi0 * T;                                  // first core output of the warp
     double* row = wbuf + lane * (T + 1);
+    // fused xcorr score (a9): running max over this lane's valid lags, lowest lag on ties (C17)
+    double sc_v = -__longlong_as_double(0x7ff0000000000000LL);   // -inf
+    long long sc_j = -1;
+    auto score_or_store = [&](double* dst, long long j, double v) {
+      if (e.xc_val) {
+        // dst + j is this signal's output slot r[lag - r_off] (placement of C17)
+        const long long lagj = (long long)((dst + j) - (e.r + jp.sig * e.r_stride)) + e.r_off;
+        if (v > sc_v) {
+          sc_v = v;
+          sc_j = lagj;
+        }
+      } else {
+        *(dst + j) = v;
+      }
+    };
     auto flush = [&](double* dst, int step, long long jlo, long long jhi) {
       __syncwarp();
 #pragma unroll
       for (int it = 0; it < T; ++it) {
         const int j = lane + 32 * it;
-        if (j >= jlo && j < jhi) dst[(long long)step * j] = wbuf[(j / T) * (T + 1) + j % T];
+        if (j >= jlo && j < jhi) score_or_store(dst, (long long)step * j, wbuf[(j / T) * (T + 1) + j % T]);
       }
       __syncwarp();
     };
@@ -750,7 +765,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec 
 #pragma unroll
         for (int it = 0; it < T; ++it) {
           const int j = lane + 32 * it;
-          if (j >= jlo && j < jhi) dst[j] = wbuf[(j / V2) * (V2 + 1) + j % V2];
+          if (j >= jlo && j < jhi) score_or_store(dst, j, wbuf[(j / V2) * (V2 + 1) + j % V2]);
         }
         __syncwarp();
       }
@@ -774,6 +789,21 @@ __global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec 
         jhi = min(jhi, g_hi - gbase - k0);
         const long long jlo = max(0LL, g_lo - gbase - k0);
         flush(rsig + gbase + k0, 1, jlo, min(jhi, (long long)(32 * T)));
+      }
+    }
+    if (e.xc_val) {                                          // warp max, lowest lag on ties
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, sc_v, o);
+        const long long oj = __shfl_xor_sync(0xffffffffu, sc_j, o);
+        if (oj >= 0 && (sc_j < 0 || ov > sc_v || (ov == sc_v && oj < sc_j))) {
+          sc_v = ov;
+          sc_j = oj;
+        }
+      }
+      if (lane == 0) {
+        const long long slot = jp.sig * e.jobs_per_sig * npart + (job % e.jobs_per_sig) * npart + part;
+        e.xc_val[slot] = sc_v;
+        e.xc_lag[slot] = sc_j;
       }
     }
     if (wrec) wrec[3] = gtimer();

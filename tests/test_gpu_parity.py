@@ -325,13 +325,17 @@ def test_adaptive_decisions_and_output(floor):
             assert np.array_equal(got[lo:hi], y_ref[lo:hi]), w
 
 
-def test_xcorr_max_scores():
+@pytest.mark.parametrize("exec_", [0, 1])    # auto (tiled kernel, fused score epilogue), per-block + lag scan
+def test_xcorr_max_scores(exec_):
+    """conv_xcorr_max: per-signal max over valid lags and its lowest argmax (C17).  The tiled
+    kernel fuses the score into its epilogue (warp partials + a per-signal reduction, no lag
+    buffer); the per-block kernel stores the lags and scans them.  Both equal the oracle."""
     rng = np.random.default_rng(4)
     n_sig, L, N = 6, 1 << 14, 256
     db = np.stack([WL.cfg4_signal(i, L) for i in range(n_sig)])
     q = db[3, 5000:5000 + N] + rng.normal(0, 0.01, N)
     for packing, Q in ((O.FULL, 0), (O.SYM, 7), (O.ASYM2, 127)):
-        with pcb.Plan(L, N, 2048, pcb.MODE_XCORR, PK[packing], Q, rmax_rule=pcb.RMAX_L1) as p:
+        with pcb.Plan(L, N, 2048, pcb.MODE_XCORR, PK[packing], Q, rmax_rule=pcb.RMAX_L1, exec=exec_) as p:
             p.set_kernel(dev(q))
             sc = torch.empty(n_sig, dtype=torch.float64, device=DEV)
             lag = torch.empty(n_sig, dtype=torch.int64, device=DEV)
@@ -648,3 +652,29 @@ def test_literal_paper_unpack(mode, case):
     assert np.array_equal(got, ref.out)
     bal = O.conv_pipeline(s, k, W_block, O.SYM, Q, mode=mode, eps_rule=O.EPS_PAPER)
     assert np.array_equal(got, bal.out)
+
+
+@pytest.mark.parametrize("packing,Q", [(O.FULL, 0), (O.SYM, 5), (O.ASYM2, 63)])
+def test_xcorr_max_ties_lowest_lag(packing, Q):
+    """Equal maxima at many lags (a periodic database signal and a query of whole periods):
+    the score's lag is the lowest one (C17), across warp parts, jobs and blocks."""
+    n_sig, L, N, per = 3, 50_000, 300, 100
+    base = np.sin(2 * np.pi * np.arange(L) / per) * 0.5
+    db = np.stack([base * (1 + 0.1 * i) for i in range(n_sig)])
+    q = base[:N].copy()
+    with pcb.Plan(L, N, 2048, pcb.MODE_XCORR, PK[packing], Q, rmax_rule=pcb.RMAX_L1) as p:
+        p.set_kernel(dev(q))
+        sc = torch.empty(n_sig, dtype=torch.float64, device=DEV)
+        lag = torch.empty(n_sig, dtype=torch.int64, device=DEV)
+        p.xcorr_max(dev(db), n_sig, L, sc, lag)
+        torch.cuda.synchronize()
+        sc, lag = sc.cpu().numpy(), lag.cpu().numpy()
+    for i in range(n_sig):
+        if packing == O.FULL:
+            c = O.full_precision(db[i], q, O.XCORR)
+            best = np.max(c)
+            assert abs(sc[i] - best) <= 1e-12 * best and c[lag[i]] >= best * (1 - 1e-12)
+        else:
+            c = O.conv_pipeline(db[i], q, 2048, packing, Q, mode=O.XCORR, rmax_rule=O.RMAX_L1).out
+            assert (sc[i], lag[i]) == O.xcorr_score(c)
+            assert np.sum(c == sc[i]) > 1            # a real tie was resolved
