@@ -510,6 +510,13 @@ def run_ours(args, ws, rank, local):
         "full_precision": full,
         "points": results,
         "clocks": sampler_summary,
+        # the paper's own numbers: context only, another machine and workload
+        "paper_context": {"hardware": "Intel Core i5 540M 2.5 GHz, single-threaded, Intel IPP 7.0 ippsConv_64f "
+                                      "(P:153, P:164)",
+                          "packed_vs_full": {"synthetic_IV_A_sym": "+52%..+158% (Table 2, P:176-181)",
+                                             "music_matching_xcorr_sym": "+112.5% (Table 3, P:195-199)",
+                                             "mpeg7_xcorr_sym": "+174% (Table 4, P:207-212)"},
+                          "best_msamples_per_s": 15.57},
     }
     if ws == 1 and not args.no_cpu_baseline and not xcorr:
         line["cpu_baseline"] = cpu_baseline(x, k, W_block, points[head])
