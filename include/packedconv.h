@@ -166,6 +166,25 @@ int conv_execute_batch(conv_plan* plan, const double* s_dev, int64_t n_signals, 
  * the copies to overlap.  Results are identical to conv_execute. */
 int conv_execute_host(conv_plan* plan, const double* s_host, double* r_host, void* stream);
 
+/* Many (signal, kernel) pairs, one kernel each -- the MPEG-7 stereo-descriptor regime of §IV.C
+ * (SURVEY NEXT-3): block b of one channel cross-correlated with block b of the other.
+ * conv_plan_set_kernels companding each of the n kernels (q_dev: n rows of N doubles, row
+ * stride q_stride; device) on its own (reading C5): per-kernel c_k, k~ and core taps,
+ * with one R_max = N' S_q K_q for all (PAPER rule required for packed modes, so eps is
+ * common; CONFIG otherwise).  It also performs conv_plan_set_kernel with row 0.  The plan's
+ * mode, packing, Q and geometry apply to every pair.  Plan-owned memory: about
+ * n (2 N' + K + 35) doubles.  Returns BOUND (STRICT) as conv_plan_set_kernel. */
+int conv_plan_set_kernels(conv_plan* plan, const double* q_dev, int64_t n, int64_t q_stride, void* stream);
+
+/* xcorr plans after conv_plan_set_kernels(n' >= n): pair i = signal row i of x_dev (L
+ * doubles at x_dev + i*x_stride; device) with kernel i: score[i] = max over valid lags j of
+ * c_i[j] = sum_n x_i[j+n] q_i[n], lag[i] = the lowest j attaining it (C17) (device arrays).
+ * Always the tiled kernel with the fused score epilogue (tap chunks per stage).  Callers wanting
+ * all 2N-1 lags of equal-length blocks pad x with N-1 zeros on each side.  STATE if n exceeds
+ * the kernels set. */
+int conv_xcorr_pairs(conv_plan* plan, const double* x_dev, int64_t n, int64_t x_stride, double* score,
+                     int64_t* lag, void* stream);
+
 /* xcorr plans only: per signal, the maximum of c[j] over valid lags and its argmax
  * (lowest j on ties; C17) -- the music-matching score. */
 int conv_xcorr_max(conv_plan* plan, const double* db_dev, int64_t n_signals, int64_t s_stride,

@@ -79,6 +79,8 @@ def load():
             "conv_execute_batch": (C.c_int, [P, VP, I64, I64, VP, I64, VP]),
             "conv_execute_host": (C.c_int, [P, VP, VP, VP]),
             "conv_xcorr_max": (C.c_int, [P, VP, I64, I64, VP, VP, VP]),
+            "conv_plan_set_kernels": (C.c_int, [P, VP, I64, I64, VP]),
+            "conv_xcorr_pairs": (C.c_int, [P, VP, I64, I64, VP, VP, VP]),
             "conv_execute_debug": (C.c_int, [P, VP, VP, VP, VP, VP, VP, VP]),
             "conv_adapt_block": (C.c_int, [P, VP, D, D, C.POINTER(conv_block_decision), VP]),
             "conv_plan_query": (C.c_int, [P, C.POINTER(conv_plan_info)]),
@@ -175,6 +177,18 @@ def xcorr_max(plan, db_dev, n_signals, s_stride, score_dev, lag_dev, stream=None
                                  _ptr(lag_dev), _stream(stream)), "conv_xcorr_max")
 
 
+def set_kernels(plan, q_dev, n, q_stride, stream=None):
+    """One kernel per pair (NEXT-3): n rows of N doubles, row stride q_stride (device)."""
+    _check(load().conv_plan_set_kernels(plan, _ptr(q_dev), int(n), int(q_stride), _stream(stream)),
+           "conv_plan_set_kernels")
+
+
+def xcorr_pairs(plan, x_dev, n, x_stride, score_dev, lag_dev, stream=None):
+    """score/lag of pair i = (row i of x, kernel i); see include/packedconv.h."""
+    _check(load().conv_xcorr_pairs(plan, _ptr(x_dev), int(n), int(x_stride), _ptr(score_dev), _ptr(lag_dev),
+                                   _stream(stream)), "conv_xcorr_pairs")
+
+
 def execute_debug(plan, s_dev, r_dev=None, packed=None, rbar=None, rint=None, c_s=None, stream=None):
     _check(load().conv_execute_debug(plan, _ptr(s_dev), _ptr(r_dev), _ptr(packed), _ptr(rbar), _ptr(rint),
                                      _ptr(c_s), _stream(stream)), "conv_execute_debug")
@@ -256,6 +270,12 @@ class Plan:
 
     def xcorr_max(self, *a, **k):
         xcorr_max(self.h, *a, **k)
+
+    def set_kernels(self, *a, **k):
+        set_kernels(self.h, *a, **k)
+
+    def xcorr_pairs(self, *a, **k):
+        xcorr_pairs(self.h, *a, **k)
 
     def adapt_block(self, s_dev, floor_db, calib_offset_db=0.0, stream=None):
         return adapt_block(self.h, s_dev, floor_db, calib_offset_db, self.info()["P"], stream)

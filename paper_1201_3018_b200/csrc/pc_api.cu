@@ -62,6 +62,12 @@ struct conv_plan {
   double* d_in = nullptr;
   double* d_out = nullptr;
   cudaStream_t st_h2d = nullptr, st_d2h = nullptr;   // conv_execute_host pipeline (plan-owned)
+  // conv_plan_set_kernels / conv_xcorr_pairs (NEXT-3): one kernel per pair
+  long long n_kernels = 0;
+  double* d_pk_pad = nullptr;          // [n][N'] padded (reversed) kernels, then k~
+  double* d_pk_int = nullptr;
+  double* d_pk_scal = nullptr;         // [n][3] {peak, c_k, l1}
+  double* d_pk_taps = nullptr;         // [n][K + 32] core taps, reversed
   double* d_xc_pval = nullptr;         // conv_xcorr_max fused: per warp-part partial max and its lag
   long long* d_xc_plag = nullptr;
   size_t xc_part_n = 0;
@@ -210,7 +216,7 @@ struct TShape {
   long long tiles0, tiles1;
   size_t smem;
 };
-bool tiled_shape(const conv_plan* p, int packing, TShape* sh) {
+bool tiled_shape(const conv_plan* p, int packing, TShape* sh, bool taps_per_signal = false) {
   int mmax, mtyp;
   core_sizes(p, packing, &mmax, &mtyp);
   const int K = core_taps(p, packing);
@@ -237,8 +243,8 @@ bool tiled_shape(const conv_plan* p, int packing, TShape* sh) {
   const int T = sh->T;
   sh->K_pad = (K + T - 1) / T * T;
   sh->threads = pc::kTiledThreads;
-  const int KCmax = 4096;
-  if (sh->K_pad <= KCmax) {
+  const int KCmax = taps_per_signal ? 1024 : 4096;   // per-signal taps travel with every stage
+  if (sh->K_pad <= KCmax && !taps_per_signal) {
     sh->taps_resident = 1;
     sh->nchunks = 1;
     sh->KC = sh->K_pad;
@@ -380,7 +386,7 @@ bool uses_tiled(const conv_plan* p) {
 int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride, double* r, long long r_off,
               long long r_stride, long long b0, long long nblk, long long n_sig, Exec* dbg, cudaStream_t st,
               unsigned long long* timing = nullptr, int* grid_out = nullptr, double* xc_val = nullptr,
-              long long* xc_lag = nullptr) {
+              long long* xc_lag = nullptr, bool pairs = false) {
   if (!p->kernel_set) return PC_E_STATE;
   if (p->packing == PC_PACK_ADAPTIVE && !p->adapt_ready) return PC_E_STATE;
   if (nblk <= 0 || n_sig <= 0) return PC_OK;
@@ -434,7 +440,7 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
   // (measured 2x at N = 64 for 65k..1M samples; the tiled kernel wins from N = 128 at 4096).
   const bool small_core = small_core_plan(p, packs, np);
   const bool forced = forced_tiled(p);                 // tile / parts forced, literal unpack: tiled
-  if (!dbg && !xc_val && small_core && !forced && per_block_ok && p->opts.exec == PC_EXEC_FUSED)
+  if (!dbg && !xc_val && !pairs && small_core && !forced && per_block_ok && p->opts.exec == PC_EXEC_FUSED)
     return cuda_status(pc::launch_fused(launch_pack, make_geo(p), e, nblk * n_sig, sh.threads, sh.smem, st));
   const bool tiled_ok = p->opts.exec == PC_EXEC_FUSED || p->opts.exec == PC_EXEC_TILED;
   if (!dbg && p->packing == PC_PACK_ADAPTIVE && tiled_ok && n_sig == 1 && b0 == 0 &&
@@ -472,7 +478,12 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
       return PC_OK;
     }
   }
-  if (!dbg && p->packing != PC_PACK_ADAPTIVE && tiled_ok && tiled_shape(p, p->packing, &ts)) {
+  if (!dbg && p->packing != PC_PACK_ADAPTIVE && (tiled_ok || pairs) && tiled_shape(p, p->packing, &ts, pairs)) {
+    if (pairs) {
+      e.kr_sig = p->d_pk_taps;
+      e.kr_stride = ((long long)p->ms[p->packing].K + 33) & ~1LL;   // as conv_plan_set_kernels
+      e.scal_sig = p->d_pk_scal;
+    }
     e.sm_ctr = p->d_counter;
     e.dbg_timing = timing;
     e.xc_val = xc_val;
@@ -647,6 +658,10 @@ void conv_plan_destroy(conv_plan* p) {
   cudaFree(p->d_out);
   cudaFree(p->d_xc_pval);
   cudaFree(p->d_xc_plag);
+  cudaFree(p->d_pk_pad);
+  cudaFree(p->d_pk_int);
+  cudaFree(p->d_pk_scal);
+  cudaFree(p->d_pk_taps);
   for (int i = 0; i < 16; ++i) {
     if (p->ev_in[i]) cudaEventDestroy(p->ev_in[i]);
     if (p->ev_done[i]) cudaEventDestroy(p->ev_done[i]);
@@ -933,6 +948,69 @@ int conv_execute_debug(conv_plan* p, const double* s, double* r, double* packed,
   d.dbg_rint_stride = info.rint_stride;
   d.dbg_cs = c_s;
   return run_exec(p, s, 0, 0, r, 0, 0, 0, p->P, 1, &d, (cudaStream_t)stream);
+}
+
+int conv_plan_set_kernels(conv_plan* p, const double* q_dev, int64_t n, int64_t q_stride, void* stream) {
+  if (!p || !q_dev || n < 1 || q_stride < p->N) return PC_E_CONFIG;
+  if (p->packing == PC_PACK_ADAPTIVE || p->opts.core != PC_CORE_DIRECT) return PC_E_CONFIG;
+  if (p->packing != PC_PACK_FULL && p->opts.rmax_rule != PC_RMAX_PAPER) return PC_E_CONFIG;   // pair-independent eps
+  if (cudaSetDevice(p->device) != cudaSuccess) return PC_E_CUDA;
+  cudaStream_t st = (cudaStream_t)stream;
+  // the packing state (R_max = N' S_q K_q, eps, bound, taps layout) from the first kernel
+  int rc = conv_plan_set_kernel(p, q_dev, stream);
+  if (rc) return rc;
+  const ModeState& m = p->ms[p->packing];
+  const long long Np = p->Np, kr_len = ((long long)m.K + 33) & ~1LL;   // rows 16-byte aligned (TMA)
+  if (n > p->n_kernels) {
+    cudaFree(p->d_pk_pad);
+    cudaFree(p->d_pk_int);
+    cudaFree(p->d_pk_scal);
+    cudaFree(p->d_pk_taps);
+    p->d_pk_pad = p->d_pk_int = p->d_pk_scal = p->d_pk_taps = nullptr;
+    p->n_kernels = 0;
+    cudaError_t e = cudaMalloc(&p->d_pk_pad, sizeof(double) * n * Np);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_pk_int, sizeof(double) * n * Np);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_pk_scal, sizeof(double) * 3 * n);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_pk_taps, sizeof(double) * n * kr_len);
+    if (e != cudaSuccess) return PC_E_CUDA;
+  }
+  p->n_kernels = n;
+  cudaError_t e = pc::launch_kernel_prep_batch(q_dev, q_stride, n, p->N, p->Np, p->mode == PC_MODE_XCORR,
+                                               (double)m.K_q, p->d_pk_pad, p->d_pk_int, Np, p->d_pk_scal, st);
+  if (e == cudaSuccess)
+    e = pc::launch_build_taps_batch(p->d_pk_pad, p->d_pk_int, Np, p->Np, p->packing, m.eps_inv, m.K, (int)kr_len,
+                                    p->d_pk_taps, kr_len, n, st);
+  return cuda_status(e);
+}
+
+int conv_xcorr_pairs(conv_plan* p, const double* x_dev, int64_t n, int64_t x_stride, double* score, int64_t* lag,
+                     void* stream) {
+  if (!p || !x_dev || !score || !lag || n < 0 || x_stride < p->L) return PC_E_CONFIG;
+  if (p->mode != PC_MODE_XCORR || n > p->n_kernels) return n > p->n_kernels ? PC_E_STATE : PC_E_CONFIG;
+  if (n == 0) return PC_OK;
+  if (cudaSetDevice(p->device) != cudaSuccess) return PC_E_CUDA;
+  cudaStream_t st = (cudaStream_t)stream;
+  TShape ts;
+  if (!tiled_shape(p, p->packing, &ts, true)) return PC_E_CONFIG;
+  const long long jobs_per_sig = ts.tiles0 + (p->P - 1) * ts.tiles1;
+  const long long n_part = jobs_per_sig * (ts.G / 32);
+  const size_t need = (size_t)n * (size_t)n_part;
+  if (need > p->xc_part_n) {
+    cudaFree(p->d_xc_pval);
+    cudaFree(p->d_xc_plag);
+    p->d_xc_pval = nullptr;
+    p->d_xc_plag = nullptr;
+    p->xc_part_n = 0;
+    if (cudaMalloc(&p->d_xc_pval, sizeof(double) * need) != cudaSuccess) return PC_E_CUDA;
+    if (cudaMalloc(&p->d_xc_plag, sizeof(long long) * need) != cudaSuccess) return PC_E_CUDA;
+    p->xc_part_n = need;
+  }
+  const long long n_lags = p->L - p->N + 1;
+  int rc = run_exec(p, x_dev, 0, x_stride, p->d_xc_pval, 0, n_lags, 0, p->P, n, nullptr, st, nullptr, nullptr,
+                    p->d_xc_pval, p->d_xc_plag, true);
+  if (rc) return rc;
+  return cuda_status(pc::launch_xcorr_reduce(p->d_xc_pval, p->d_xc_plag, n, n_part, score,
+                                             reinterpret_cast<long long*>(lag), st));
 }
 
 int conv_xcorr_max(conv_plan* p, const double* db, int64_t n_signals, int64_t s_stride, double* score,

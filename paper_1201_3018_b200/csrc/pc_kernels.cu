@@ -21,10 +21,11 @@
 namespace pc {
 
 // ------------------------------------------------------------------ a1: kernel preparation
-__global__ void pc_kernel_prep(const double* __restrict__ k_in, int N, int Np, int reverse, double K_q,
-                               double* __restrict__ k_pad, double* __restrict__ k_int,
-                               double* __restrict__ scal /* [peak, c_k, l1] */) {
-  __shared__ double red[32];
+// One kernel (query) per CTA: pad to N' (C13), reverse for xcorr (a9), ||k||_inf, c_k = K_q /
+// ||k||_inf (all-zero -> 1), k~ = [[c_k k]] (Eq. (2)) and ||k~||_1.
+__device__ __forceinline__ void kernel_prep_one(const double* __restrict__ k_in, int N, int Np, int reverse,
+                                                double K_q, double* __restrict__ k_pad, double* __restrict__ k_int,
+                                                double* __restrict__ scal /* [peak, c_k, l1] */, double* red) {
   const int tid = threadIdx.x, nt = blockDim.x;
   double m = 0.0;
   for (int i = tid; i < Np; i += nt) {
@@ -63,25 +64,49 @@ __global__ void pc_kernel_prep(const double* __restrict__ k_in, int N, int Np, i
   }
 }
 
+__global__ void pc_kernel_prep(const double* __restrict__ k_in, int N, int Np, int reverse, double K_q,
+                               double* __restrict__ k_pad, double* __restrict__ k_int,
+                               double* __restrict__ scal /* [peak, c_k, l1] */) {
+  __shared__ double red[32];
+  kernel_prep_one(k_in, N, Np, reverse, K_q, k_pad, k_int, scal, red);
+}
+
+// Many kernels at once (conv_plan_set_kernels, NEXT-3): problem i = blockIdx.x.
+__global__ void pc_kernel_prep_batch(const double* __restrict__ k_in, long long k_stride, int N, int Np, int reverse,
+                                     double K_q, double* __restrict__ k_pad, double* __restrict__ k_int,
+                                     long long pad_stride, double* __restrict__ scal /* [n][3] */) {
+  __shared__ double red[32];
+  const long long i = blockIdx.x;
+  kernel_prep_one(k_in + i * k_stride, N, Np, reverse, K_q, k_pad + i * pad_stride, k_int + i * pad_stride,
+                  scal + 3 * i, red);
+}
+
+__device__ __forceinline__ double core_tap(const double* __restrict__ k_pad, const double* __restrict__ k_int,
+                                           int Np, int packing, double eps_inv, int K, int j) {
+  if (j >= K) return 0.0;
+  const int n = K - 1 - j;   // reversed: kr[j] = core tap K-1-j
+  if (packing == PACK_SYM) {
+    // Eq. (5) under reading C1: k_bar[n] = k~[2n+1] + eps^-1 k~[2n], k~[N'] = 0
+    const double kev = k_int[2 * n];
+    const double kod = (2 * n + 1 < Np) ? k_int[2 * n + 1] : 0.0;
+    return __dadd_rn(kod, __dmul_rn(eps_inv, kev));
+  }
+  if (packing == PACK_FULL) return k_pad[n];
+  return k_int[n];             // Eq. (8): asymmetric packing convolves with k~
+}
+
 __global__ void pc_build_taps(const double* __restrict__ k_pad, const double* __restrict__ k_int, int Np,
                               int packing, double eps_inv, int K, int K_pad, double* __restrict__ kr) {
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < K_pad; j += gridDim.x * blockDim.x) {
-    double v = 0.0;
-    if (j < K) {
-      const int n = K - 1 - j;   // reversed: kr[j] = core tap K-1-j
-      if (packing == PACK_SYM) {
-        // Eq. (5) under reading C1: k_bar[n] = k~[2n+1] + eps^-1 k~[2n], k~[N'] = 0
-        const double kev = k_int[2 * n];
-        const double kod = (2 * n + 1 < Np) ? k_int[2 * n + 1] : 0.0;
-        v = __dadd_rn(kod, __dmul_rn(eps_inv, kev));
-      } else if (packing == PACK_FULL) {
-        v = k_pad[n];
-      } else {
-        v = k_int[n];             // Eq. (8): asymmetric packing convolves with k~
-      }
-    }
-    kr[j] = v;
-  }
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < K_pad; j += gridDim.x * blockDim.x)
+    kr[j] = core_tap(k_pad, k_int, Np, packing, eps_inv, K, j);
+}
+
+__global__ void pc_build_taps_batch(const double* __restrict__ k_pad, const double* __restrict__ k_int,
+                                    long long pad_stride, int Np, int packing, double eps_inv, int K, int K_pad,
+                                    double* __restrict__ kr, long long kr_stride) {
+  const long long i = blockIdx.y;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < K_pad; j += gridDim.x * blockDim.x)
+    kr[i * kr_stride + j] = core_tap(k_pad + i * pad_stride, k_int + i * pad_stride, Np, packing, eps_inv, K, j);
 }
 
 // ------------------------------------------------------------------ fused per-block kernel
@@ -498,6 +523,24 @@ cudaError_t launch_adapt_decide(long long P, const double* sigma, const double* 
                                 cudaStream_t st) {
   pc_adapt_decide<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(P, sigma, peak, sig_k, peak_k, cand, qmode, ncand,
                                                                  thr, dp, dq, ds);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_kernel_prep_batch(const double* k_in, long long k_stride, long long n, int N, int Np, int reverse,
+                                     double K_q, double* k_pad, double* k_int, long long pad_stride, double* scal,
+                                     cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  pc_kernel_prep_batch<<<(unsigned)n, 256, 0, st>>>(k_in, k_stride, N, Np, reverse, K_q, k_pad, k_int, pad_stride,
+                                                    scal);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_build_taps_batch(const double* k_pad, const double* k_int, long long pad_stride, int Np,
+                                    int packing, double eps_inv, int K, int K_pad, double* kr, long long kr_stride,
+                                    long long n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  pc_build_taps_batch<<<dim3((unsigned)((K_pad + 255) / 256), (unsigned)n), 256, 0, st>>>(
+      k_pad, k_int, pad_stride, Np, packing, eps_inv, K, K_pad, kr, kr_stride);
   return cudaGetLastError();
 }
 

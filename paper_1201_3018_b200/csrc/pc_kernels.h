@@ -76,6 +76,11 @@ struct Exec {
   // the max over its valid lags and the lowest lag attaining it to [sig][job * npart + part]
   double* xc_val;                    // nullptr: store the lags
   long long* xc_lag;
+  // one kernel per signal (conv_xcorr_pairs, NEXT-3): taps kr_sig + sig * kr_stride (chunked
+  // through the stages, never resident) and c_k = scal_sig[3 sig + 1]; nullptr: the plan's kernel
+  const double* kr_sig;
+  long long kr_stride;
+  const double* scal_sig;
 };
 
 // FFT overlap-save core (pc_fft.cu).
@@ -101,6 +106,12 @@ cudaError_t launch_kernel_prep(const double* k_in, int N, int Np, int reverse, d
                                double* k_int, double* scal, cudaStream_t st);
 cudaError_t launch_build_taps(const double* k_pad, const double* k_int, int Np, int packing, double eps_inv, int K,
                               int K_pad, double* kr, cudaStream_t st);
+cudaError_t launch_kernel_prep_batch(const double* k_in, long long k_stride, long long n, int N, int Np, int reverse,
+                                     double K_q, double* k_pad, double* k_int, long long pad_stride, double* scal,
+                                     cudaStream_t st);
+cudaError_t launch_build_taps_batch(const double* k_pad, const double* k_int, long long pad_stride, int Np,
+                                    int packing, double eps_inv, int K, int K_pad, double* kr, long long kr_stride,
+                                    long long n, cudaStream_t st);
 cudaError_t launch_block_stats(const Geo& g, const double* s, double* sigma, double* peak, cudaStream_t st);
 cudaError_t launch_adapt_decide(long long P, const double* sigma, const double* peak, double sig_k, double peak_k,
                                 const int* cand, const int* qmode, int ncand, double thr, int* dp, int* dq, double* ds,

@@ -426,7 +426,8 @@ __global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec 
       const int nt = (c == nch - 1) ? mp.K_pad - c * KC : KC;
       double* xs = stg + (size_t)st * stage_words;
       mbar_arrive_expect_tx(&ps->full[st], (uint32_t)nt * 8u);
-      bulk_g2s(xs + stage_x, mp.kr + (size_t)c * KC, (uint32_t)nt * 8u, &ps->full[st]);
+      const double* kr_job = e.kr_sig ? e.kr_sig + (job / e.jobs_per_sig) * e.kr_stride : mp.kr;
+      bulk_g2s(xs + stage_x, kr_job + (size_t)c * KC, (uint32_t)nt * 8u, &ps->full[st]);
     } else {
       mbar_arrive(&ps->full[st]);
     }
@@ -474,7 +475,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec 
       if (frec) frec[2] = gtimer();
       if (gtid == 0) {
         ps->fcs[f] = cs;
-        ps->finv[f] = dequant_scale(cs, mp.c_k);
+        ps->finv[f] = dequant_scale(cs, e.scal_sig ? e.scal_sig[3 * jp.sig + 1] : mp.c_k);
       }
     }
   }
@@ -548,7 +549,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec 
         if (blk_id != cur_blk_w) {
           cur_blk_w = blk_id;
           c_s_w = warp_cs<PACK>(mp, gsrc, n_valid, lane);   // a2/a3 (Eq. (2))
-          inv_w = dequant_scale(c_s_w, mp.c_k);              // Eq. (16), once per block
+          inv_w = dequant_scale(c_s_w, e.scal_sig ? e.scal_sig[3 * jp.sig + 1] : mp.c_k);   // Eq. (16)
         }
       }
       for (int c = 0; c < nch; ++c) {

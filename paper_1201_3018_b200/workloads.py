@@ -151,3 +151,32 @@ def uniform_ints(seed: int, n: int, q: int) -> np.ndarray:
 
 
 GENERATORS = {"cfg1": cfg1, "cfg2": cfg2, "cfg3": cfg3, "cfg5": cfg5}
+
+
+def stereo(seed: int = 0, seconds: float = 10.0, delay: int = 17, snr_db: float = 40.0, mono: bool = False,
+           fs: float = FS):
+    """NEXT-3 stand-in for §IV.C's MPEG-7 clips (the clips are not available): a
+    synthetic stereo pair.  left = 16-sinusoid mixture + pink noise (0.1x std), peak-normalized;
+    right = left delayed by `delay` samples (right[n] = left[n - delay]) plus white noise at
+    `snr_db`; mono: right = left exactly.  Returns (left, right)."""
+    rng = np.random.default_rng(seed)
+    n = int(seconds * fs)
+    x = sinusoid_mixture(rng, n + abs(delay))
+    p = pink_noise(rng, n + abs(delay))
+    x = normalize_peak(x + p * (0.1 * np.std(x) / np.std(p)))
+    left = x[abs(delay):abs(delay) + n] if delay >= 0 else x[:n]
+    if mono:
+        return left.copy(), left.copy()
+    right = x[abs(delay) - delay:abs(delay) - delay + n]
+    return left, add_white_noise(rng, right, snr_db)
+
+
+def stereo_pairs(left: np.ndarray, right: np.ndarray, B: int):
+    """Blocks b of B samples: x_b = left block with B-1 zeros on each side (so the valid lags
+    j = 0..2B-2 of the xcorr are all 2B-1 lags l = j - (B-1)), q_b = right block.  Returns
+    (x: n x (3B-2), q: n x B) for the n = len // B whole blocks."""
+    n = min(len(left), len(right)) // B
+    x = np.zeros((n, 3 * B - 2))
+    x[:, B - 1:2 * B - 1] = left[:n * B].reshape(n, B)
+    q = right[:n * B].reshape(n, B).copy()
+    return x, q

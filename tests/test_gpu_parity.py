@@ -678,3 +678,33 @@ def test_xcorr_max_ties_lowest_lag(packing, Q):
             c = O.conv_pipeline(db[i], q, 2048, packing, Q, mode=O.XCORR, rmax_rule=O.RMAX_L1).out
             assert (sc[i], lag[i]) == O.xcorr_score(c)
             assert np.sum(c == sc[i]) > 1            # a real tie was resolved
+
+
+@pytest.mark.parametrize("packing,Q", [(O.FULL, 0), (O.SYM, 3), (O.ASYM2, 32), (O.ASYM3, 5)])
+def test_xcorr_pairs_per_pair_kernels(packing, Q):
+    """NEXT-3 (§IV.C regime): block b of the left channel (zero-padded to all 2B-1 lags)
+    cross-correlated with block b of the right channel, each right block companded as its own
+    kernel (conv_plan_set_kernels; PAPER R_max so eps is common).  Per-pair score and lowest
+    argmax equal the oracle pipeline run pair by pair; the lag recovers the channel delay."""
+    B, delay = 1024, 17
+    left, right = WL.stereo(seed=5, seconds=0.4, delay=delay)
+    x, q = WL.stereo_pairs(left, right, B)
+    n, L = x.shape
+    with pcb.Plan(L, B, 4096, pcb.MODE_XCORR, PK[packing], Q, rmax_rule=pcb.RMAX_PAPER) as p:
+        p.set_kernels(dev(q), n, B)
+        sc = torch.empty(n, dtype=torch.float64, device=DEV)
+        lag = torch.empty(n, dtype=torch.int64, device=DEV)
+        p.xcorr_pairs(dev(x), n, L, sc, lag)
+        torch.cuda.synchronize()
+        sc, lag = sc.cpu().numpy(), lag.cpu().numpy()
+    for i in range(n):
+        if packing == O.FULL:
+            c = O.full_precision(x[i], q[i], O.XCORR)
+            best, j = O.xcorr_score(c)
+            assert abs(sc[i] - best) <= 1e-12 * np.max(np.abs(c))
+            assert c[lag[i]] >= best - 1e-12 * np.max(np.abs(c))
+        else:
+            ref = O.conv_pipeline(x[i], q[i], 4096, packing, Q, mode=O.XCORR, rmax_rule=O.RMAX_PAPER)
+            assert ref.kernel.bound_ok and ref.mismatches == 0
+            assert (sc[i], lag[i]) == O.xcorr_score(ref.out), i
+    assert np.all(lag - (B - 1) == -delay)
