@@ -401,3 +401,21 @@ def test_adapt_spec_example():
     assert all(d[0] == O.SYM for d in dec0)
     dinf, _ = O.adapt_decisions(s, k, 3 * 801 + 1, math.inf, eps_rule=O.EPS_PAPER, rmax_rule=O.RMAX_PAPER)
     assert all(d[0] == O.FULL for d in dinf)
+
+
+def test_stereo_workload_delay_and_pairs():
+    """NEXT-3 generator: right = left delayed by d (plus 40 dB noise), mono = identical; the
+    padded pairs expose all 2B-1 lags and the brute-force xcorr peaks at lag -d."""
+    from paper_1201_3018_b200 import workloads as WL
+    d = 17
+    left, right = WL.stereo(seed=3, seconds=0.2, delay=d)
+    noise = right[d:] - left[:-d]
+    assert np.sqrt(np.mean(noise ** 2)) < 0.02 * np.sqrt(np.mean(left ** 2))
+    l2, r2 = WL.stereo(seed=3, seconds=0.2, delay=0, mono=True)
+    assert np.array_equal(l2, r2)
+    B = 512
+    x, q = WL.stereo_pairs(left, right, B)
+    assert x.shape == (len(left) // B, 3 * B - 2) and q.shape == (len(left) // B, B)
+    for i in (1, 5):
+        c = np.array([np.dot(x[i, j:j + B], q[i]) for j in range(2 * B - 1)])   # valid lags, brute force
+        assert int(np.argmax(c)) - (B - 1) == -d
