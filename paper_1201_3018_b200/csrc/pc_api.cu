@@ -505,6 +505,7 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
     if (grid_out) *grid_out = grid;
     return PC_OK;
   }
+  if (pairs || xc_val) return PC_E_CONFIG;  // per-pair taps / fused scores exist only in the tiled kernel
   if (!per_block_ok) return PC_E_CONFIG;   // debug dumps / adaptive need the per-block kernel
   return cuda_status(pc::launch_fused(launch_pack, make_geo(p), e, nblk * n_sig, sh.threads, sh.smem, st));
 }
