@@ -186,7 +186,10 @@ int conv_xcorr_pairs(conv_plan* plan, const double* x_dev, int64_t n, int64_t x_
                      int64_t* lag, void* stream);
 
 /* xcorr plans only: per signal, the maximum of c[j] over valid lags and its argmax
- * (lowest j on ties; C17) -- the music-matching score. */
+ * (lowest j on ties; C17) -- the music-matching score.  On the tiled kernel the
+ * score is fused into the epilogue (warp partials + a per-signal reduction; plan-owned
+ * partials of n_signals x jobs x parts entries, no lag buffer); otherwise the lags go
+ * through a plan-owned scratch of <= 2 GiB and are scanned. */
 int conv_xcorr_max(conv_plan* plan, const double* db_dev, int64_t n_signals, int64_t s_stride,
                    double* score_dev, int64_t* lag_dev, void* stream);
 
@@ -205,11 +208,15 @@ int conv_execute_debug(conv_plan* plan, const double* s_dev, double* r_dev, doub
 int conv_adapt_block(conv_plan* plan, const double* s_dev, double snr_floor_db,
                      double calib_offset_db, conv_block_decision* out_host, void* stream);
 
-/* Diagnostics: conv_execute that also records, per persistent CTA c, four uint64 at
- * cta_records_dev[4c..4c+3] = {SM id, start and end %globaltimer (ns), blocks processed};
- * the buffer must hold 8 * 148 * 32 entries; entries [4*148*32 + 4c ..] receive CTA c's
- * consumer-thread-0 clock64 totals {waiting for a packed stage, core, decode+store, fix-up}.  *grid_out receives the CTA count (0 if the
- * plan runs the per-block kernel, which records nothing). */
+/* Diagnostics: conv_execute that records, when the tiled kernel or the FFT core runs, a
+ * timeline into cta_records_dev (uint64, at least 24*148*32 + 148*16*16*4 + 148*4*16*4 entries,
+ * zeroed by the caller): tiled kernel -- per CTA c {SM id, start / end %globaltimer (ns), jobs}
+ * at [4c..4c+3], consumer-warp-0 cycle totals at [4*148*32 + 4c ..], per consumer warp and part
+ * {job sequence, ready, core done, stored} and per producer warp and job {sequence, turn,
+ * claimed, published} (layout in pc_tiled.cu, read by tools/tiled_timeline.py); FFT core -- per
+ * job {SM id, start, peak, packed, forward, product, inverse, end} at [8 job ..] for the first
+ * 4096 jobs (tools/fft_timeline.py).  *grid_out receives the CTA count (0 for the per-block
+ * kernel, which records nothing). */
 int conv_execute_profile(conv_plan* plan, const double* s_dev, double* r_dev, uint64_t* cta_records_dev,
                          int32_t* grid_out, void* stream);
 
