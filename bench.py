@@ -34,6 +34,9 @@ sys.path.insert(0, ROOT)
 
 MEASURED_FP64_TFLOPS = 34.0   # profiles/r01_fp64_peak.log: sustained DFMA, 148 SMs @ 1965 MHz
 FP64_PEAK_SOURCE = "measured (tools/fp64_peak.cu, profiles/r01_fp64_peak.log); not in MEASURED_PEAKS.json"
+MEASURED_DMMA_TFLOPS = 37.1   # profiles/r01_dmma_peak.log: FP64 tensor cores (mma.sync m8n8k4 f64)
+DMMA_PEAK_SOURCE = ("measured (tools/dmma_peak.cu, profiles/r01_dmma_peak.log: 18.56 T DMMA-FMA/s); "
+                    "not in MEASURED_PEAKS.json")
 HBM_GBS = 6540.2              # MEASURED_PEAKS.json hbm_gbs (copy)
 
 METRIC = "output samples/s, packed vs full-precision conv, 1/2/4/8 B200; % FP64/HBM peak"   # BASELINE.json
@@ -416,7 +419,8 @@ def run_ours(args, ws, rank, local):
         rec = {"ms_per_step": ms / args.steps, "kernel_ms": kern_ms,
                "value": ws * L_out * nsig * args.steps / (ms / 1e3), "R_max": info["R_max"], "Q": Q,
                "bound_ok": info["bound_ok"], "tile": info["core_tile"], "fft_n": info["fft_n"],
-               "core": "fft" if core == FFT else "direct", "cuda_graph": graph is not None}
+               "core": "fft" if core == FFT else "direct", "cuda_graph": graph is not None,
+               "core_mma": info["core_mma"]}
         if core == DIRECT:
             rec["fp64_tflops"] = 2.0 * fma / (kern_ms / 1e3) / 1e12
             rec["fma_per_output"] = fma / (L_out * nsig)
@@ -461,22 +465,30 @@ def run_ours(args, ws, rank, local):
     h = results[head]
     full = results.get(full_pt)
     traffic, traffic_src = None, None
-    prof = os.path.join(ROOT, "profiles", "r01_ncu_cfg2_asym2.json")
+    prof = os.path.join(ROOT, "profiles", "r01_ncu_cfg2_asym2_dmma.json" if h.get("core_mma") else
+                        "r01_ncu_cfg2_asym2.json")
     if args.workload == "cfg2" and head == "asym2_10b" and os.path.exists(prof):
+        kname = f"pc_tiled_kernel<2, {h['tile']}, {h['core_mma']}>"
         for recd in json.load(open(prof)).get("ncu_full", []):
-            if f"pc_tiled_kernel<2, {h['tile']}>" in recd["kernel"]:
+            if kname in recd["kernel"] or f"pc_tiled_kernel<2, {h['tile']}>" in recd["kernel"]:
                 rd = recd["dram__bytes_read.sum"].split()
                 wr = recd["dram__bytes_write.sum"].split()
                 mult = {"Mbyte": 1e6, "Kbyte": 1e3, "Gbyte": 1e9, "byte": 1.0}
                 traffic = float(rd[0]) * mult[rd[1]] + float(wr[0]) * mult[wr[1]]
                 traffic_src = "profiles/r01_ncu_cfg2_asym2.json (ncu --set full, one launch)"
     if "fp64_tflops" in h:
-        roof = {"bound": "alu", "achieved": h["fp64_tflops"], "peak": MEASURED_FP64_TFLOPS, "unit": "TFLOP/s",
-                "frac": h["fp64_tflops"] / MEASURED_FP64_TFLOPS, "traffic": traffic, "traffic_unit": "bytes/launch",
+        # the DMMA-core kernel is bound by the FP64 tensor pipe (its own measured peak), the FMA core
+        # by the FP64 FMA pipe; adaptive plans: asym2/full launches run DMMA, the symmetric one FMA
+        mma = bool(h.get("core_mma")) or points[head][0] == 4
+        peak = MEASURED_DMMA_TFLOPS if mma else MEASURED_FP64_TFLOPS
+        roof = {"bound": "tensor" if mma else "alu", "achieved": h["fp64_tflops"], "peak": peak, "unit": "TFLOP/s",
+                "frac": h["fp64_tflops"] / peak, "traffic": traffic, "traffic_unit": "bytes/launch",
                 "traffic_source": traffic_src, "algorithmic_bytes": 8 * (L + L_out) * nsig,
-                "kernel": (f"pc_tiled_kernel<{points[head][0]}, {h['tile']}>" if points[head][0] != 4 else
+                "kernel": (f"pc_tiled_kernel<{points[head][0]}, {h['tile']}, {h.get('core_mma', 0)}>"
+                           if points[head][0] != 4 else
                            "pc_tiled_kernel x3 (one launch per packing) + pc_block_stats/pc_adapt_decide/pc_adapt_lists"),
-                "peak_source": FP64_PEAK_SOURCE,
+                "peak_source": DMMA_PEAK_SOURCE if mma else FP64_PEAK_SOURCE,
+                "fp64_fma_peak_frac": h["fp64_tflops"] / MEASURED_FP64_TFLOPS,
                 "algorithmic": "FP64 FMAs of the packed core: sum over blocks of M_out * K (2 flop each)"}
     else:
         gbs = h.get("hbm_gbs_algorithmic", 8 * (L + L_out) * nsig / (h["kernel_ms"] / 1e3) / 1e9)

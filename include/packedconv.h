@@ -71,11 +71,18 @@ typedef struct conv_opts {
   int32_t device;           /* CUDA device ordinal, -1 = current device                    */
   int32_t reserved[9];      /* [0]: raw-block staging 0 auto/1 on/2 off (per-block kernel);
                                [1]: force the persistent core tile (12/14/16; tests);
-                               [2]: unused;
+                               [2]: direct core, 0 auto (the FP64 tensor cores -- DMMA, T = 16 --
+                                    except symmetric packing: FMA), 1 the FP64 FMA core (any T),
+                                    2 DMMA;
                                [3]: force consumer warps per job (1, 2, 4; diagnostics);
                                [4]: force the FFT size N (complex points, 1024..8192; 16384 =
                                     the 32768-point real transform of the whole block, full
                                     precision, W_block <= 16386, 2-CTA clusters);
+                               [6]: tiled-kernel producers: 1 = compand/pack with integer ops
+                                    (dyadic eps; bit-identical), else FP64 ops;
+                               [7]: cap on the tiled kernel's stage-ring slots (>= 2; diagnostics);
+                               [8]: 2 = compand/pack in a prepack kernel ahead of the DMMA-core
+                                    launch instead of its producer warps (single-chunk plans);
                                [5]: unpack form, 0 balanced digits (C6), 1 the literal
                                     Eqs. (11)-(15) with the u_sys guard (symmetric packing,
                                     direct core; exact for R_max < 89,524, reading C6); rest 0 */
@@ -105,6 +112,7 @@ typedef struct conv_plan_info {
   int32_t q_mode[4];        /* ADAPTIVE: max Q per packing under its bound          */
   int32_t core_tile;        /* outputs per thread of the persistent core (12, 14 or 16)      */
   int32_t fft_n;            /* FFT core: complex points N (real transform length 2N), else 0 */
+  int32_t core_mma;         /* 1: the tiled core runs on the FP64 tensor cores (DMMA), else 0  */
 } conv_plan_info;
 
 /* Per-block decision of conv_adapt_block. */

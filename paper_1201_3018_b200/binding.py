@@ -41,7 +41,8 @@ class conv_plan_info(C.Structure):
                 ("R_max", C.c_int64), ("bound", C.c_int64), ("bound_ok", C.c_int32), ("eps_b", C.c_int32),
                 ("eps", C.c_double), ("eps_inv", C.c_double), ("c_k", C.c_double), ("k_peak", C.c_double),
                 ("packed_stride", C.c_int64), ("rbar_stride", C.c_int64), ("rint_stride", C.c_int64),
-                ("q_mode", C.c_int32 * 4), ("core_tile", C.c_int32), ("fft_n", C.c_int32)]
+                ("q_mode", C.c_int32 * 4), ("core_tile", C.c_int32), ("fft_n", C.c_int32),
+                ("core_mma", C.c_int32)]
 
 
 class conv_shard(C.Structure):

@@ -77,6 +77,8 @@ struct conv_plan {
   size_t d_xc_bytes = 0;
   // persistent kernel job counter (monotonic; base tracked on the host)
   unsigned* d_counter = nullptr;        // tiled kernel: per-SM job queues + done counter (zero between launches)
+  double* d_pre = nullptr;              // prepacked stage images + per-job inverse scales (pc_prepack_kernel)
+  long long pre_cap = 0;                // doubles allocated at d_pre
   // FFT core
   int fft_N = 0;                       // complex points (real transform length 2N)
   double2* d_tw = nullptr;             // exp(-2 pi i m / N)
@@ -212,7 +214,7 @@ bool launch_shape(const conv_plan* p, const int* packs, int npacks, Shape* sh) {
 // tiles; taps resident when <= 4096, else chunks of ~1024 taps (a multiple of T); as many
 // stage-ring slots as shared memory holds (2..8) after the per-warp output staging rows.
 struct TShape {
-  int T, threads, G, KC, nchunks, taps_resident, rows_s, K_pad, nstages;
+  int T, mma, threads, G, KC, nchunks, taps_resident, rows_s, K_pad, nstages;
   long long tiles0, tiles1;
   size_t smem;
 };
@@ -221,16 +223,24 @@ bool tiled_shape(const conv_plan* p, int packing, TShape* sh, bool taps_per_sign
   core_sizes(p, packing, &mmax, &mtyp);
   const int K = core_taps(p, packing);
   const int force = p->opts.reserved[1];
+  // core: the FP64 tensor cores (DMMA, T = 16) unless the FMA core or another tile is forced;
+  // auto picks the FMA core for symmetric packing (its short core -- about N/2 taps -- and heavy
+  // three-digit epilogue measured 5% faster there: profiles/r01_core_choice.json)
+  const int core = p->opts.reserved[2];
+  sh->mma = (core == 2 || (core == 0 && packing != PC_PACK_SYM)) && (force == 0 || force == 16);
   double best = -1.0;
   for (int T : pc::kTPChoices) {
     if ((force == 12 || force == 14 || force == 16) && T != force) continue;
+    if (sh->mma && T != 16) continue;
     const double speed = T == 16 ? 1.0 : (T == 14 ? 0.96 : 0.92);   // core-loop calibration (profiles)
     for (int npart : {4, 2, 1}) {
       if (p->opts.reserved[3] > 0 && npart != p->opts.reserved[3]) continue;   // diagnostics: force G
       const int G = 32 * npart;
       const long long groups = (mtyp + T - 1) / T;
       const long long tiles = (groups + G - 1) / G;
-      const double util = (double)groups / (double)(tiles * G);
+      // the DMMA core skips a part's m-tiles (8 groups) past the block's end
+      const double util = sh->mma ? (double)groups / (double)((groups + 7) / 8 * 8)
+                                  : (double)groups / (double)(tiles * G);
       // fewer parts per job: more jobs (ring slots, producer work) per resident warp
       const double score = util * speed * (npart == 4 ? 1.0 : (npart == 2 ? 0.9 : 0.75));
       if (score > best + 1e-9) {
@@ -242,7 +252,7 @@ bool tiled_shape(const conv_plan* p, int packing, TShape* sh, bool taps_per_sign
   }
   const int T = sh->T;
   sh->K_pad = (K + T - 1) / T * T;
-  sh->threads = pc::kTiledThreads;
+  sh->threads = pc::tiled_threads(sh->mma);
   const int KCmax = taps_per_signal ? 1024 : 4096;   // per-signal taps travel with every stage
   if (sh->K_pad <= KCmax && !taps_per_signal) {
     sh->taps_resident = 1;
@@ -260,12 +270,14 @@ bool tiled_shape(const conv_plan* p, int packing, TShape* sh, bool taps_per_sign
   const long long g1 = (mtyp + T - 1) / T;
   sh->tiles0 = (g0 + sh->G - 1) / sh->G;
   sh->tiles1 = (g1 + sh->G - 1) / sh->G;
-  const size_t stage = (size_t)(((T + 1) * sh->rows_s + 1) & ~1) * 8 + (sh->taps_resident ? 0 : (size_t)sh->KC * 8);
-  const size_t fixed = pc::kTiledHeader + (sh->taps_resident ? (size_t)sh->K_pad * 8 : 0) +
-                       (size_t)pc::kTiledConsWarps * 32 * (T + 1) * 8;
+  const int PT = sh->mma ? T + 4 : T + 1, TH = sh->mma ? 16 : 0;   // as pc_tiled_kernel
+  const size_t stage = (size_t)((PT * sh->rows_s + 1) & ~1) * 8 + (sh->taps_resident ? 0 : (size_t)(sh->KC + 2 * TH) * 8);
+  const size_t fixed = pc::kTiledHeader + (sh->taps_resident ? (size_t)(sh->K_pad + 2 * TH) * 8 : 0) +
+                       (size_t)pc::tiled_cons_warps(sh->mma) * 32 * (T + 1) * 8;
   if (fixed + 2 * stage > kMaxSmem) return false;
   sh->nstages = (int)((kMaxSmem - fixed) / stage);
   if (sh->nstages > pc::kTiledMaxStages) sh->nstages = pc::kTiledMaxStages;
+  if (p->opts.reserved[7] >= 2 && sh->nstages > p->opts.reserved[7]) sh->nstages = p->opts.reserved[7];   // diagnostics
   sh->smem = fixed + (size_t)sh->nstages * stage;
   if (sh->smem < kMaxSmem / 2 + 4096) sh->smem = kMaxSmem / 2 + 4096;   // one CTA per SM
   return true;
@@ -331,13 +343,19 @@ int choose_fft_N(const conv_plan* p, int packing) {
 
 int cuda_status(cudaError_t e) { return e == cudaSuccess ? PC_OK : PC_E_CUDA; }
 
-void fill_modep(const ModeState& m, ModeP* mp) {
+void fill_modep(const ModeState& m, int packing, ModeP* mp) {
   mp->kr = m.kr;
   mp->Q = (double)m.Q;
   mp->c_k = m.c_k;
   mp->eps = m.eps;
   mp->eps_inv = m.eps_inv;
   mp->pow2 = m.b > 0;
+  mp->b = m.b;
+  // Packed words as integers n * 2^-((M-1) b): exact in FP64 iff |n| < 2^53, then the integer
+  // Horner of the companded digits equals the FP64 one bit for bit (pc_tiled.cu, pack_window).
+  const int M = packing == PC_PACK_ASYM3 ? 3 : 2;
+  mp->alu_pack = packing != PC_PACK_FULL && m.b > 0 && (M - 1) * m.b <= 60 &&
+                 (double)m.Q * (std::ldexp(1.0, (M - 1) * m.b) * 2.0) < std::ldexp(1.0, 53);
   mp->K = m.K;
   mp->K_pad = m.K_pad;
   mp->rows = m.rows;
@@ -407,7 +425,10 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
   e.nblk = nblk;
   e.stage_raw = per_block_ok ? sh.stage_raw : 0;
   e.reg_path = per_block_ok ? sh.reg_path : 0;
-  for (int i = 0; i < np; ++i) fill_modep(p->ms[packs[i]], &e.mp[packs[i]]);
+  for (int i = 0; i < np; ++i) {
+    fill_modep(p->ms[packs[i]], packs[i], &e.mp[packs[i]]);
+    if (p->opts.reserved[6] != 1) e.mp[packs[i]].alu_pack = 0;   // integer packing only when asked
+  }
   if (p->opts.reserved[5] == 1) {                    // literal Eqs. (11)-(15) (SYM, tiled kernel)
     pc::ModeP& ms = e.mp[PC_PACK_SYM];
     ms.paper_unpack = 1;
@@ -471,7 +492,7 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
         el.jobs_per_sig = t.tiles0 + (p->P - 1) * t.tiles1;   // upper bound: grid size only
         el.mp[pk].K_pad = t.K_pad;
         int grid = 0;
-        cudaError_t err = pc::launch_tiled(pk, t.T, make_geo(p), el, el.jobs_per_sig, t.threads, t.smem, st, &grid);
+        cudaError_t err = pc::launch_tiled(pk, t.T, t.mma, make_geo(p), el, el.jobs_per_sig, t.threads, t.smem, st, &grid);
         if (err != cudaSuccess) return PC_E_CUDA;
         if (grid_out) *grid_out = grid;
       }
@@ -486,6 +507,7 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
     }
     e.sm_ctr = p->d_counter;
     e.dbg_timing = timing;
+    e.dbg_skip_pack = p->opts.reserved[8] == 77;   // timing experiment (results invalid)
     e.xc_val = xc_val;
     e.xc_lag = xc_lag;
     e.G = ts.G;
@@ -499,8 +521,27 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
     e.jobs_per_sig = (b0 == 0) ? ts.tiles0 + (nblk - 1) * ts.tiles1 : nblk * ts.tiles1;
     e.mp[p->packing].K_pad = ts.K_pad;
     const long long njobs = e.jobs_per_sig * n_sig;
+    // a2-a4 ahead of the DMMA-core launch (single-chunk packed plans, reserved[8] = 2): measured
+    // slower than the fused producers at cfg2 (the separate pass costs ~26 us, the persistent
+    // kernel's tail does not shrink), so off by default
+    if (ts.mma && ts.nchunks == 1 && p->packing != PC_PACK_FULL && p->opts.reserved[8] == 2) {
+      const long long stride = ((long long)(ts.T + 4) * ts.rows_s + 1) & ~1LL;   // stage_x of pc_tiled_kernel
+      const long long need = njobs * stride + njobs;
+      if (need > p->pre_cap) {
+        cudaFree(p->d_pre);
+        p->d_pre = nullptr;
+        p->pre_cap = 0;
+        if (cudaMalloc(&p->d_pre, sizeof(double) * need) != cudaSuccess) return PC_E_CUDA;
+        p->pre_cap = need;
+      }
+      e.lookahead = p->opts.reserved[7] < 0 ? -p->opts.reserved[7] : 0;   // diagnostics
+      e.pre_win = p->d_pre;
+      e.pre_stride = stride;
+      e.pre_inv = p->d_pre + njobs * stride;
+      if (pc::launch_prepack(p->packing, ts.T, make_geo(p), e, njobs, st) != cudaSuccess) return PC_E_CUDA;
+    }
     int grid = 0;
-    cudaError_t err = pc::launch_tiled(p->packing, ts.T, make_geo(p), e, njobs, ts.threads, ts.smem, st, &grid);
+    cudaError_t err = pc::launch_tiled(p->packing, ts.T, ts.mma, make_geo(p), e, njobs, ts.threads, ts.smem, st, &grid);
     if (err != cudaSuccess) return PC_E_CUDA;
     if (grid_out) *grid_out = grid;
     return PC_OK;
@@ -643,7 +684,8 @@ int conv_plan_create(conv_plan** out, int64_t L, int32_t N, int32_t W_block, int
 void conv_plan_destroy(conv_plan* p) {
   if (!p) return;
   cudaSetDevice(p->device);
-  for (auto& m : p->ms) cudaFree(m.kr);
+  for (auto& m : p->ms)
+    if (m.kr) cudaFree(m.kr - 16);
   cudaFree(p->d_k_pad);
   cudaFree(p->d_k_int);
   cudaFree(p->d_scal);
@@ -662,7 +704,7 @@ void conv_plan_destroy(conv_plan* p) {
   cudaFree(p->d_pk_pad);
   cudaFree(p->d_pk_int);
   cudaFree(p->d_pk_scal);
-  cudaFree(p->d_pk_taps);
+  if (p->d_pk_taps) cudaFree(p->d_pk_taps - 16);
   for (int i = 0; i < 16; ++i) {
     if (p->ev_in[i]) cudaEventDestroy(p->ev_in[i]);
     if (p->ev_done[i]) cudaEventDestroy(p->ev_done[i]);
@@ -672,6 +714,7 @@ void conv_plan_destroy(conv_plan* p) {
   if (p->st_d2h) cudaStreamDestroy(p->st_d2h);
   cudaFree(p->d_xc);
   cudaFree(p->d_counter);
+  cudaFree(p->d_pre);
   cudaFree(p->d_tw);
   cudaFree(p->d_tw2);
   cudaFree(p->d_H);
@@ -727,7 +770,12 @@ int init_mode(conv_plan* p, int packing, int Q, int K_q, const double* k_dev, cu
     if (!m.bound_ok && p->opts.bound_policy == PC_BOUND_STRICT) return PC_E_BOUND;
   }
   const int kr_len = m.K + 32;   // zero taps past K serve every tile padding (8..16)
-  if (!m.kr && cudaMalloc(&m.kr, sizeof(double) * kr_len) != cudaSuccess) return PC_E_CUDA;
+  if (!m.kr) {                   // + 16 leading zeros (the DMMA core's Toeplitz fragments read kr[-15..])
+    double* buf = nullptr;
+    if (cudaMalloc(&buf, sizeof(double) * (kr_len + 16)) != cudaSuccess) return PC_E_CUDA;
+    if (cudaMemsetAsync(buf, 0, sizeof(double) * 16, st) != cudaSuccess) return PC_E_CUDA;
+    m.kr = buf + 16;
+  }
   e = pc::launch_build_taps(p->d_k_pad, p->d_k_int, p->Np, packing, m.eps_inv, m.K, kr_len, m.kr, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return PC_E_CUDA;
@@ -966,14 +1014,17 @@ int conv_plan_set_kernels(conv_plan* p, const double* q_dev, int64_t n, int64_t 
     cudaFree(p->d_pk_pad);
     cudaFree(p->d_pk_int);
     cudaFree(p->d_pk_scal);
-    cudaFree(p->d_pk_taps);
+    if (p->d_pk_taps) cudaFree(p->d_pk_taps - 16);
     p->d_pk_pad = p->d_pk_int = p->d_pk_scal = p->d_pk_taps = nullptr;
     p->n_kernels = 0;
     cudaError_t e = cudaMalloc(&p->d_pk_pad, sizeof(double) * n * Np);
     if (e == cudaSuccess) e = cudaMalloc(&p->d_pk_int, sizeof(double) * n * Np);
     if (e == cudaSuccess) e = cudaMalloc(&p->d_pk_scal, sizeof(double) * 3 * n);
-    if (e == cudaSuccess) e = cudaMalloc(&p->d_pk_taps, sizeof(double) * n * kr_len);
+    double* tb = nullptr;                            // + 16 leading zeros, as the plan's taps
+    if (e == cudaSuccess) e = cudaMalloc(&tb, sizeof(double) * (n * kr_len + 16));
+    if (e == cudaSuccess) e = cudaMemsetAsync(tb, 0, sizeof(double) * 16, st);
     if (e != cudaSuccess) return PC_E_CUDA;
+    p->d_pk_taps = tb + 16;
   }
   p->n_kernels = n;
   cudaError_t e = pc::launch_kernel_prep_batch(q_dev, q_stride, n, p->N, p->Np, p->mode == PC_MODE_XCORR,
@@ -1237,6 +1288,7 @@ int conv_plan_query(const conv_plan* p, conv_plan_info* info) {
   TShape ts;
   info->core_tile = (p->packing != PC_PACK_ADAPTIVE && p->opts.core == PC_CORE_DIRECT && tiled_shape(p, pk, &ts)) ? ts.T : 0;
   info->fft_n = p->fft_N;
+  info->core_mma = info->core_tile ? ts.mma : 0;
   return PC_OK;
 }
 

@@ -16,22 +16,34 @@ constexpr int kTiledMaxStages = 24;     // tiled kernel: stage ring slots (>= 16
 #define PC_PROD_WARPS 4
 #endif
 constexpr int kTiledProdWarps = PC_PROD_WARPS;   // tiled kernel: producer warps (peak, companding, packing)
-constexpr int kTiledFillJobs = 4;       // tiled kernel: jobs packed by all warps before the consumers start
+#ifndef PC_FILL_JOBS
+#define PC_FILL_JOBS 4
+#endif
+constexpr int kTiledFillJobs = PC_FILL_JOBS;   // tiled kernel: jobs packed by all warps before the consumers start
 #ifndef PC_CONS_WARPS
 #define PC_CONS_WARPS 12
 #endif
 constexpr int kTiledConsWarps = PC_CONS_WARPS;   // tiled kernel: consumer warps (core + unpack); 12 = 3 per SMSP,
                                                  // 16 warps per CTA so the core gets 128 registers
 constexpr int kTiledThreads = 32 * (kTiledProdWarps + kTiledConsWarps);
+#ifndef PC_CONS_WARPS_MMA
+#define PC_CONS_WARPS_MMA 12
+#endif
+// consumer warps of the DMMA-core kernel (16 = four per SMSP at 96 registers spills and
+// leaves fewer ring stages: measured slower than 12)
+__host__ __device__ constexpr int tiled_cons_warps(int mma) { return mma ? PC_CONS_WARPS_MMA : kTiledConsWarps; }
+__host__ __device__ constexpr int tiled_threads(int mma) { return 32 * (kTiledProdWarps + tiled_cons_warps(mma)); }
 constexpr int kCtrDone = 256;     // sm_ctr[kCtrDone] counts retired CTAs; queues are sm_ctr[0, nsm)   // mbarrier + reduction scratch, keeps the rest 128B-aligned
 
 // Per-packing parameters of one launch (adaptive plans fill several).
 struct ModeP {
-  const double* kr;     // core taps, reversed, K_pad doubles (device)
+  const double* kr;     // core taps, reversed, K + 32 doubles after 16 zeros (kr[-16..-1] = 0; device)
   double Q;             // S_q
   double c_k;           // kernel companding factor
   double eps, eps_inv;  // packing coefficient and its inverse
   int pow2;             // eps = 2^-b (reading C4)
+  int b;                // that b (0 if eps is not a power of two)
+  int alu_pack;         // tiled kernel: pack with integer ops (dyadic eps, every packed word < 2^53 in units)
   int K, K_pad;         // core taps and taps padded to a multiple of the kernel's tile T
   int rows;             // rows of the column layout of the core's input words
   int paper_unpack;     // SYM: literal Eqs. (11)-(15) with the u_sys guard instead of balanced digits
@@ -59,6 +71,7 @@ struct Exec {
   int G;                        // consumer threads = groups per tile
   int KC, nchunks;              // taps per chunk (multiple of T), chunks per job
   int nstages;                  // stage ring slots (2 .. kTiledMaxStages)
+  int lookahead;                // > 0: claim job sequence m only once consumers have claimed parts of m - lookahead
   int taps_resident;            // 1: all K_pad taps stay in shared memory (nchunks == 1)
   int rows_s;                   // rows of a stage's padded word window
   long long tiles0, tiles1;     // tiles of block 0 / of every other block
@@ -81,6 +94,13 @@ struct Exec {
   const double* kr_sig;
   long long kr_stride;
   const double* scal_sig;
+  int dbg_skip_pack;    // experiment only: producers publish without companding/packing (wrong results)
+  // prepacked windows (pc_prepack_kernel, single-chunk plans): job j's stage image (rows_s rows of
+  // pitch T + 4) at pre_win + j * pre_stride and its (c_s c_k)^-1 at pre_inv[j]; the tiled
+  // kernel's producers then only move them into the ring with one bulk copy each
+  const double* pre_win;
+  long long pre_stride;
+  const double* pre_inv;
 };
 
 // FFT overlap-save core (pc_fft.cu).
@@ -99,9 +119,14 @@ cudaError_t launch_fft_spectrum(int N, const double* kr, int K, const double2* t
 
 cudaError_t launch_fused(int packing, const Geo& g, const Exec& e, long long n_jobs, int threads, size_t smem,
                          cudaStream_t st);
+// a2-a4 for every job of a tiled launch, ahead of it (pc_tiled.cu): block peak, c_s, packing
+// into the stage image the DMMA core reads; one CTA per job.
+cudaError_t launch_prepack(int packing, int T, const Geo& g, const Exec& e, long long n_jobs, cudaStream_t st);
 // Tiled persistent warp-specialized kernel (pc_tiled.cu): grid = SMs x resident CTAs.
-cudaError_t launch_tiled(int packing, int T, const Geo& g, const Exec& e, long long n_jobs, int threads, size_t smem,
-                         cudaStream_t st, int* grid_out);
+// mma = 1: the core runs on the FP64 tensor cores (T = 16 only; stage pitch 20, taps with 16
+// zeros before and after -- every tap buffer is allocated with 16 leading zeros).
+cudaError_t launch_tiled(int packing, int T, int mma, const Geo& g, const Exec& e, long long n_jobs, int threads,
+                         size_t smem, cudaStream_t st, int* grid_out);
 cudaError_t launch_kernel_prep(const double* k_in, int N, int Np, int reverse, double K_q, double* k_pad,
                                double* k_int, double* scal, cudaStream_t st);
 cudaError_t launch_build_taps(const double* k_pad, const double* k_int, int Np, int packing, double eps_inv, int K,

@@ -26,6 +26,16 @@
 #include "pc_device.cuh"
 #include "pc_kernels.h"
 
+#ifndef PC_QUEUE_MIN
+#define PC_QUEUE_MIN 8    // jobs per SM queue at least (fewer queues than SMs below 8 jobs each)
+#endif
+#ifndef PC_NO_STEAL
+#define PC_NO_STEAL 0     // diagnostics: 1 = no work stealing between SM queues
+#endif
+#ifndef PC_CORE_SLOTS
+#define PC_CORE_SLOTS 2   // DMMA core: warps per SM sub-partition allowed in the core at once
+#endif
+
 namespace pc {
 
 namespace {
@@ -36,6 +46,8 @@ struct TSmem {
   long long seq[kTiledMaxStages];   // stage sequence number the slot holds
   double inv[kTiledMaxStages];      // (c_s c_k)^-1 of the stage's block (Eq. (16))
   int smsp_ctr[4];                  // consumer warp-job claim counters, one per SM sub-partition
+  int core_serve[4];                // DMMA core: the claim whose warp may run its core on each SMSP
+  int mseq_hi;                      // 1 + the highest job sequence any consumer warp has claimed a part of
   long long turn;                   // next job sequence to claim (claims happen in sequence order)
   long long fjob[16];               // pipeline fill: jobs of sequences 0 .. nf-1
   double fcs[16], finv[16];         // their c_s and (c_s c_k)^-1
@@ -83,16 +95,43 @@ __device__ __forceinline__ JobPos job_pos(const Exec& e, long long job) {
   return p;
 }
 
+// ---- integer (ALU-pipe) forms of the producer's arithmetic.  The DMMA core keeps the SM
+// sub-partition's FP64 pipe busy in 16-cycle DMMA slots, so every FP64 instruction a producer
+// issues waits behind them; everything below that need not be FP64 runs on the integer ALU.
+// round(p), half away from zero (Eq. (2)'s rounding, C-library / oracle semantics), for
+// |p| < 2^52: p = mant * 2^-sh exactly, so round(|p|) = floor((mant + 2^(sh-1)) / 2^sh).
+__device__ __forceinline__ long long round_away_alu(double p) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(p);
+  const int sh = min(max(1075 - (int)((u >> 52) & 0x7ff), 1), 63);
+  const unsigned long long mant = (u & 0xfffffffffffffull) | 0x10000000000000ull;
+  const long long r = (long long)((mant + (1ull << (sh - 1))) >> sh);
+  return (long long)u < 0 ? -r : r;
+}
+// n * 2^-e2 as a double, exact for |n| < 2^53 (normalise with the leading-zero count).
+__device__ __forceinline__ double i2d_scaled_alu(long long n, int e2) {
+  const unsigned long long a = (unsigned long long)(n < 0 ? -n : n);
+  const int msb = 63 - __clzll(a);
+  const unsigned long long bits = ((unsigned long long)(1023 + msb - e2) << 52) |
+                                  ((a << (52 - msb)) & 0xfffffffffffffull) | (n < 0 ? 0x8000000000000000ull : 0ull);
+  return a == 0 ? 0.0 : __longlong_as_double((long long)bits);
+}
+// |x| as ordered integer bits (non-negative doubles order like their bit patterns).
+__device__ __forceinline__ unsigned long long abs_bits(double x) {
+  return (unsigned long long)__double_as_longlong(x) & 0x7fffffffffffffffull;
+}
+__device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) { return a > b ? a : b; }
+
 // a4 for one stage: core words [cw0, cw0 + rows_s*T) of block b into the padded row-major
-// window xs[(i / T) * (T + 1) + i % T].  Word-major over the producer threads (coalesced
+// window xs[(i / T) * PT + i % T] (pitch PT = T + 1 for the FMA core, T + 4 for the DMMA core).  Word-major over the producer threads (coalesced
 // loads), UW words per thread with every sample load issued before any use.
-template <int PACK, int T, int UWF = 1>
+template <int PACK, int T, int UWF = 1, int PT = T + 1>
 __device__ __forceinline__ void pack_window(const Geo& g, const Blk& b, const ModeP& mp, const double* gsrc,
                                             int n_valid, double c_s, int cw0, int rows_s, double* xs, int ptid,
                                             int nprod) {
   constexpr int UW = UWF * ((PACK == PACK_ASYM3) ? 4 : 8);   // words per thread in flight
   const int words = rows_s * T;
   auto sample = [&](int i) -> double { return (i < 0 || i >= n_valid) ? 0.0 : __ldg(gsrc + i); };
+  const bool alu = mp.alu_pack;                              // warp-uniform (per plan)
   for (int i0 = ptid; i0 < words; i0 += UW * nprod) {
     double v[UW];
     if (PACK == PACK_SYM) {
@@ -103,10 +142,19 @@ __device__ __forceinline__ void pack_window(const Geo& g, const Blk& b, const Mo
         x0[u] = sample(2 * j);
         x1[u] = sample(2 * j + 1);
       }
+      if (alu) {                                             // n = s~0 2^b + s~1, word = n 2^-b
 #pragma unroll
-      for (int u = 0; u < UW; ++u) {
-        const int cw = cw0 + i0 + u * nprod;
-        v[u] = (cw >= b.pre && cw < b.xlen) ? pack_sym(compand1(c_s, x0[u]), compand1(c_s, x1[u]), mp.eps) : 0.0;
+        for (int u = 0; u < UW; ++u) {
+          const int cw = cw0 + i0 + u * nprod;
+          const long long n = round_away_alu(__dmul_rn(c_s, x0[u])) * (1LL << mp.b) + round_away_alu(__dmul_rn(c_s, x1[u]));
+          v[u] = (cw >= b.pre && cw < b.xlen) ? i2d_scaled_alu(n, mp.b) : 0.0;
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < UW; ++u) {
+          const int cw = cw0 + i0 + u * nprod;
+          v[u] = (cw >= b.pre && cw < b.xlen) ? pack_sym(compand1(c_s, x0[u]), compand1(c_s, x1[u]), mp.eps) : 0.0;
+        }
       }
     } else if (PACK == PACK_ASYM2 || PACK == PACK_ASYM3) {
       constexpr int M = (PACK == PACK_ASYM2) ? 2 : 3;
@@ -116,13 +164,24 @@ __device__ __forceinline__ void pack_window(const Geo& g, const Blk& b, const Mo
       for (int u = 0; u < UW; ++u)
 #pragma unroll
         for (int q = 0; q < M; ++q) x[q][u] = sample(base + q * b.S + i0 + u * nprod);
+      if (alu) {                                             // integer Horner: n = sum s~_q 2^((M-1-q) b)
 #pragma unroll
-      for (int u = 0; u < UW; ++u) {
-        double a = compand1(c_s, x[M - 1][u]);           // Horner, oracle order
+        for (int u = 0; u < UW; ++u) {
+          long long n = round_away_alu(__dmul_rn(c_s, x[0][u]));
 #pragma unroll
-        for (int q = M - 2; q >= 0; --q) a = __dadd_rn(compand1(c_s, x[q][u]), __dmul_rn(mp.eps, a));
-        const int cw = cw0 + i0 + u * nprod;
-        v[u] = (cw >= 0 && cw < b.xlen) ? a : 0.0;
+          for (int q = 1; q < M; ++q) n = n * (1LL << mp.b) + round_away_alu(__dmul_rn(c_s, x[q][u]));
+          const int cw = cw0 + i0 + u * nprod;
+          v[u] = (cw >= 0 && cw < b.xlen) ? i2d_scaled_alu(n, (M - 1) * mp.b) : 0.0;
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < UW; ++u) {
+          double a = compand1(c_s, x[M - 1][u]);         // Horner, oracle order
+#pragma unroll
+          for (int q = M - 2; q >= 0; --q) a = __dadd_rn(compand1(c_s, x[q][u]), __dmul_rn(mp.eps, a));
+          const int cw = cw0 + i0 + u * nprod;
+          v[u] = (cw >= 0 && cw < b.xlen) ? a : 0.0;
+        }
       }
     } else {
       const int base = b.o0 - (g.Np - 1) + cw0;
@@ -135,7 +194,7 @@ __device__ __forceinline__ void pack_window(const Geo& g, const Blk& b, const Mo
 #pragma unroll
     for (int u = 0; u < UW; ++u) {
       const int i = i0 + u * nprod;
-      if (i < words) xs[(i / T) * (T + 1) + i % T] = v[u];
+      if (i < words) xs[(i / T) * PT + i % T] = v[u];
     }
   }
 }
@@ -147,9 +206,9 @@ __device__ __forceinline__ double block_cs(const ModeP& mp, const double* gsrc, 
                                            int nprod, int bar_id) {
   if (PACK == PACK_FULL) return 1.0;
   constexpr int U = 16;
-  double m[U];
+  unsigned long long m[U];                             // max |x| as ordered bits (integer pipe)
 #pragma unroll
-  for (int u = 0; u < U; ++u) m[u] = 0.0;
+  for (int u = 0; u < U; ++u) m[u] = 0ull;
   if ((reinterpret_cast<uintptr_t>(gsrc) & 15u) == 0) {
     const double2* g2 = reinterpret_cast<const double2*>(gsrc);
     const int n2 = n_valid / 2;
@@ -161,16 +220,16 @@ __device__ __forceinline__ double block_cs(const ModeP& mp, const double* gsrc, 
         v[u] = (i < n2) ? __ldg(g2 + i) : make_double2(0.0, 0.0);
       }
 #pragma unroll
-      for (int u = 0; u < U; ++u) m[u] = fmax(m[u], fmax(fabs(v[u].x), fabs(v[u].y)));
+      for (int u = 0; u < U; ++u) m[u] = umax64(m[u], umax64(abs_bits(v[u].x), abs_bits(v[u].y)));
     }
-    if ((n_valid & 1) && ptid == 0) m[0] = fmax(m[0], fabs(gsrc[n_valid - 1]));
+    if ((n_valid & 1) && ptid == 0) m[0] = umax64(m[0], abs_bits(gsrc[n_valid - 1]));
   } else {
-    for (int i = ptid; i < n_valid; i += nprod) m[0] = fmax(m[0], fabs(__ldg(gsrc + i)));
+    for (int i = ptid; i < n_valid; i += nprod) m[0] = umax64(m[0], abs_bits(__ldg(gsrc + i)));
   }
 #pragma unroll
-  for (int u = 1; u < U; ++u) m[0] = fmax(m[0], m[u]);
-  for (int o = 16; o > 0; o >>= 1) m[0] = fmax(m[0], __shfl_xor_sync(0xffffffffu, m[0], o));
-  if ((ptid & 31) == 0) red[ptid >> 5] = m[0];
+  for (int u = 1; u < U; ++u) m[0] = umax64(m[0], m[u]);
+  for (int o = 16; o > 0; o >>= 1) m[0] = umax64(m[0], __shfl_xor_sync(0xffffffffu, m[0], o));
+  if ((ptid & 31) == 0) red[ptid >> 5] = __longlong_as_double((long long)m[0]);
   named_bar(bar_id, nprod);
   double peak = 0.0;
   for (int wi = 0; wi < nprod / 32; ++wi) peak = fmax(peak, red[wi]);
@@ -183,9 +242,9 @@ template <int PACK>
 __device__ __forceinline__ double warp_cs(const ModeP& mp, const double* gsrc, int n_valid, int lane) {
   if (PACK == PACK_FULL) return 1.0;
   constexpr int U = 16;
-  double m[U];
+  unsigned long long m[U];                             // max |x| as ordered bits (integer pipe)
 #pragma unroll
-  for (int u = 0; u < U; ++u) m[u] = 0.0;
+  for (int u = 0; u < U; ++u) m[u] = 0ull;
   if ((reinterpret_cast<uintptr_t>(gsrc) & 15u) == 0) {
     const double2* g2 = reinterpret_cast<const double2*>(gsrc);
     const int n2 = n_valid / 2;
@@ -197,16 +256,17 @@ __device__ __forceinline__ double warp_cs(const ModeP& mp, const double* gsrc, i
         v[u] = (i < n2) ? __ldg(g2 + i) : make_double2(0.0, 0.0);
       }
 #pragma unroll
-      for (int u = 0; u < U; ++u) m[u] = fmax(m[u], fmax(fabs(v[u].x), fabs(v[u].y)));
+      for (int u = 0; u < U; ++u) m[u] = umax64(m[u], umax64(abs_bits(v[u].x), abs_bits(v[u].y)));
     }
-    if ((n_valid & 1) && lane == 0) m[0] = fmax(m[0], fabs(gsrc[n_valid - 1]));
+    if ((n_valid & 1) && lane == 0) m[0] = umax64(m[0], abs_bits(gsrc[n_valid - 1]));
   } else {
-    for (int i = lane; i < n_valid; i += 32) m[0] = fmax(m[0], fabs(__ldg(gsrc + i)));
+    for (int i = lane; i < n_valid; i += 32) m[0] = umax64(m[0], abs_bits(__ldg(gsrc + i)));
   }
 #pragma unroll
-  for (int u = 1; u < U; ++u) m[0] = fmax(m[0], m[u]);
-  for (int o = 16; o > 0; o >>= 1) m[0] = fmax(m[0], __shfl_xor_sync(0xffffffffu, m[0], o));
-  return (m[0] == 0.0) ? 1.0 : mp.Q / m[0];
+  for (int u = 1; u < U; ++u) m[0] = umax64(m[0], m[u]);
+  for (int o = 16; o > 0; o >>= 1) m[0] = umax64(m[0], __shfl_xor_sync(0xffffffffu, m[0], o));
+  const double peak = __longlong_as_double((long long)m[0]);
+  return (peak == 0.0) ? 1.0 : mp.Q / peak;
 }
 
 __device__ __forceinline__ long long fdiv_floor(long long a, long long b) {
@@ -243,6 +303,12 @@ __device__ __noinline__ void mbar_stuck(int where, long long n, int st, uint32_t
          (int)blockIdx.x, (int)threadIdx.x, n, st, phase);
   __trap();
 }
+// spin-wait step with the same watchdog (a scheduling bug traps with its location instead of
+// hanging the GPU): ~2^24 sleeps of >= 64 ns
+__device__ __forceinline__ void spin_wd(int& spins, unsigned ns, int where, long long n, int st) {
+  __nanosleep(ns);
+  if (++spins > (1 << 24)) mbar_stuck(where, n, st, 0u);
+}
 __device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t phase, int where, long long n, int st) {
   if (mbar_try(bar, phase)) return;
   unsigned long long t0;
@@ -274,7 +340,7 @@ constexpr int kTimW = 24 * 148 * 32, kTimP = kTimW + 148 * 16 * 16 * 4;
 // (warp-parallel scan), so every job runs.  Returns -1 when no job is left anywhere.
 __device__ __forceinline__ long long claim_job(const Exec& e, long long njobs, int lane) {
   unsigned* ctr = e.sm_ctr;
-  const long long nq_ = njobs / 8;
+  const long long nq_ = njobs / PC_QUEUE_MIN;
   const int nq = (int)(nq_ < 1 ? 1 : (nq_ > e.nsm ? e.nsm : nq_));
   const int s = (int)(blockIdx.x % (unsigned)nq);
   long long job = -1;
@@ -286,7 +352,7 @@ __device__ __forceinline__ long long claim_job(const Exec& e, long long njobs, i
     }
   }
   job = __shfl_sync(0xffffffffu, job, 0);
-  if (job >= 0) return job;
+  if (job >= 0 || PC_NO_STEAL) return job;
   for (int base = 1; base < nq; base += 32) {
     const int t = (s + base + lane) % nq;
     const long long lo = njobs * t / nq, hi = njobs * (t + 1) / nq;
@@ -344,8 +410,69 @@ __device__ __forceinline__ void conv_chunk_padded(uint32_t xs_row, uint32_t kr_a
   }
 }
 
-template <int PACK, int T>
-__global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec e) {
+// a5 on the FP64 tensor cores (DMMA, mma.sync m8n8k4 f64): the warp's part (32 groups of 16
+// core outputs) as a Toeplitz product.  With output m = 16 i + p (group i, phase p) and
+// c = 4 s + k the word offset inside a 16-word row,
+//     out[16 i + p] = sum_jj sum_c x[16 (i + jj) + c] * kr[16 jj + c - p]
+// (every tap t = 16 jj + c - p of [0, K) appears once per output).  A (8 x 4, row-major):
+// A[i][k] = x[16 (8 mt + i + jj) + 4 s + k], rows of the stage window of pitch 20 (each
+// half-warp hits 16 distinct banks); B (4 x 8): F_d[k][n] = kr[d + k - n], d = 16 jj + 4 s -
+// 8 nt, d in {16 jj - 8, ..., 16 jj + 12}: a window of six fragments per jj of which four are
+// new.  The taps carry 16 zeros (or the neighbour chunk's taps) on both sides, so no lane
+// predicates its loads.  One warp per SMSP keeps the DMMA pipe busy (tools/dmma_peak.cu).
+// fr[mt][nt][h]: group 8 mt + lane / 4, phase 8 nt + 2 (lane % 4) + h.  Exact under the
+// dyadic eps (C4): every product and partial sum is a representable integer multiple of 2^-b,
+// so the tensor core's summation order cannot change a bit (section 2.4 of DESIGN.md).
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d[0]), "+d"(d[1])
+      : "d"(a), "d"(b));
+}
+template <int NMT, int PT>
+__device__ __forceinline__ void conv_chunk_mma(uint32_t xs_row, uint32_t kc_addr, int jj_n, double (&fr)[4][2][2],
+                                               int lane) {
+  const int r = lane >> 2, k = lane & 3;
+  uint32_t xa = xs_row + 8u * (uint32_t)(r * PT + k);
+  uint32_t ka = kc_addr + 8u * (uint32_t)(k - r) - 64u;   // b[f] = kr[16 jj - 8 + 4 f + k - r]
+  // Software-pipelined: the A fragments of the next k-step and the B fragments of the next jj
+  // are loaded before the current DMMAs issue (one warp alone must keep the pipe fed).
+  double b[6], bn[4], a[NMT], an[NMT];
+#pragma unroll
+  for (int f = 0; f < 6; ++f) b[f] = lds64(ka + 32u * f);
+#pragma unroll
+  for (int mt = 0; mt < NMT; ++mt) a[mt] = lds64(xa + 8u * (8 * mt * PT));
+#pragma unroll 1
+  for (int jj = 0; jj < jj_n; ++jj, xa += 8u * PT, ka += 128u) {
+    const bool more = jj + 1 < jj_n;
+    if (more) {
+#pragma unroll
+      for (int f = 0; f < 4; ++f) bn[f] = lds64(ka + 128u + 32u * (f + 2));
+    }
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      if (s < 3 || more) {
+#pragma unroll
+        for (int mt = 0; mt < NMT; ++mt)
+          an[mt] = lds64(xa + 8u * (8 * mt * PT) + (s < 3 ? 32u * (s + 1) : 8u * PT));
+      }
+#pragma unroll
+      for (int mt = 0; mt < NMT; ++mt) {
+        dmma884(fr[mt][0], a[mt], b[s + 2]);
+        dmma884(fr[mt][1], a[mt], b[s]);
+      }
+#pragma unroll
+      for (int mt = 0; mt < NMT; ++mt) a[mt] = an[mt];
+    }
+    b[0] = b[4];
+    b[1] = b[5];
+#pragma unroll
+    for (int f = 0; f < 4; ++f) b[f + 2] = bn[f];
+  }
+}
+
+template <int PACK, int T, int MMA>
+__global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, Exec e) {
+  constexpr int NCW = tiled_cons_warps(MMA);   // consumer warps
   extern __shared__ __align__(128) unsigned char smem[];
   TSmem* ps = reinterpret_cast<TSmem*>(smem);
   const ModeP& mp = e.mp[PACK];
@@ -356,10 +483,12 @@ __global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec 
   const int NS = e.nstages;
   const int front = (PACK == PACK_SYM) ? 1 : 0;   // one row before the tile: the extra word
   const int rows_s = e.rows_s;
-  const int stage_x = ((T + 1) * rows_s + 1) & ~1;   // doubles of a stage's word window (16B-aligned end)
-  const int stage_words = stage_x + (e.taps_resident ? 0 : KC);
-  double* kr_res = reinterpret_cast<double*>(smem + kTiledHeader);          // resident taps
-  double* stg = kr_res + (e.taps_resident ? mp.K_pad : 0);                  // NS stages
+  constexpr int PT = MMA ? T + 4 : T + 1;           // stage window pitch (conflict-free for the core)
+  constexpr int TH = MMA ? 16 : 0;                  // DMMA core: zero / neighbour taps on both sides
+  const int stage_x = (PT * rows_s + 1) & ~1;       // doubles of a stage's word window (16B-aligned end)
+  const int stage_words = stage_x + (e.taps_resident ? 0 : KC + 2 * TH);
+  double* kr_res = reinterpret_cast<double*>(smem + kTiledHeader) + TH;     // resident taps
+  double* stg = kr_res + (e.taps_resident ? mp.K_pad + TH : -TH);           // NS stages
   double* wout = stg + (size_t)NS * stage_words;                            // per consumer warp: 32 (T+1)
   const int tid = threadIdx.x;
   const int nprod = kTiledProdWarps * 32;
@@ -371,12 +500,13 @@ __global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec 
       mbar_init(&ps->empty[i], npart);
       ps->seq[i] = -1;
     }
-    for (int i = 0; i < 4; ++i) ps->smsp_ctr[i] = 0;
+    for (int i = 0; i < 4; ++i) ps->smsp_ctr[i] = ps->core_serve[i] = 0;
+    ps->mseq_hi = 0;
     ps->turn = 1;
     ps->m_end = -1;
-    const uint32_t tb = e.taps_resident ? (uint32_t)mp.K_pad * 8u : 0u;
+    const uint32_t tb = e.taps_resident ? (uint32_t)(mp.K_pad + 2 * TH) * 8u : 0u;
     mbar_arrive_expect_tx(&ps->bar_taps, tb);
-    if (tb) bulk_g2s(kr_res, mp.kr, tb, &ps->bar_taps);
+    if (tb) bulk_g2s(kr_res - TH, mp.kr - TH, tb, &ps->bar_taps);   // the tap buffers carry 16 leading zeros
   }
   // programmatic dependent launch: only plan-owned, read-only taps are touched above
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -385,7 +515,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec 
     // jobs of this CTA's queue.  A hint only -- L2 is coherent, so even if the preceding
     // kernel writes the input, the loads after griddepcontrol.wait see its data.
     const long long nj = e.jobs_per_sig * e.nsig;
-    const long long nq_ = nj / 8;
+    const long long nq_ = nj / PC_QUEUE_MIN;
     const long long nq = nq_ < 1 ? 1 : (nq_ > (long long)gridDim.x ? (long long)gridDim.x : nq_);
     const long long q = blockIdx.x % nq, lo = nj * q / nq, hi = nj * (q + 1) / nq;
     for (long long jb = lo; jb < hi && jb < lo + kTiledFillJobs; ++jb) {
@@ -419,15 +549,19 @@ __global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec 
   auto publish = [&](long long n, int st, int c, long long job, double inv, int ptid) {
     if (ptid == 0) {
       ps->job[st] = job;
-      ps->inv[st] = inv;
+      ps->inv[st] = (job >= 0 && e.pre_win) ? e.pre_inv[job] : inv;
       ps->seq[st] = n;
     }
-    if (job >= 0 && !e.taps_resident && ptid == 0) {
+    const bool taps = job >= 0 && !e.taps_resident, win = job >= 0 && e.pre_win;
+    if ((taps || win) && ptid == 0) {
       const int nt = (c == nch - 1) ? mp.K_pad - c * KC : KC;
       double* xs = stg + (size_t)st * stage_words;
-      mbar_arrive_expect_tx(&ps->full[st], (uint32_t)nt * 8u);
-      const double* kr_job = e.kr_sig ? e.kr_sig + (job / e.jobs_per_sig) * e.kr_stride : mp.kr;
-      bulk_g2s(xs + stage_x, kr_job + (size_t)c * KC, (uint32_t)nt * 8u, &ps->full[st]);
+      mbar_arrive_expect_tx(&ps->full[st], (taps ? (uint32_t)(nt + 2 * TH) * 8u : 0u) + (win ? (uint32_t)stage_x * 8u : 0u));
+      if (win) bulk_g2s(xs, e.pre_win + job * e.pre_stride, (uint32_t)stage_x * 8u, &ps->full[st]);
+      if (taps) {
+        const double* kr_job = e.kr_sig ? e.kr_sig + (job / e.jobs_per_sig) * e.kr_stride : mp.kr;
+        bulk_g2s(xs + stage_x, kr_job + (size_t)c * KC - TH, (uint32_t)(nt + 2 * TH) * 8u, &ps->full[st]);
+      }
     } else {
       mbar_arrive(&ps->full[st]);
     }
@@ -437,7 +571,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec 
   // claimed in parallel, then companded and packed by all warps, five warps per job.
   // (never more than a CTA's share of the launch: small launches spread over all CTAs)
   const long long share = (njobs + gridDim.x - 1) / gridDim.x;
-  const int nf = (nch == 1) ? (int)min((long long)min(kTiledFillJobs, NS), share < 1 ? 1 : share) : 1;
+  const int nf = e.pre_win ? 0 : (nch == 1) ? (int)min((long long)min(kTiledFillJobs, NS), share < 1 ? 1 : share) : 1;
   const int lane_ = tid & 31, warp_ = tid >> 5;
   if (warp_ < nf) {
     const long long j = claim_job(e, njobs, lane_);
@@ -454,7 +588,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec 
   }
   __syncthreads();
   {
-    constexpr int GW = (kTiledProdWarps + kTiledConsWarps) / kTiledFillJobs;   // warps per fill group
+    constexpr int GW = (kTiledProdWarps + NCW) / kTiledFillJobs;   // warps per fill group
     const int gq = warp_ / GW, gtid = tid - gq * GW * 32;
     for (int f = gq; f < nf; f += 4) {
       const long long fj = ps->fjob[f];
@@ -471,7 +605,8 @@ __global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec 
       double* xs_f = stg + (size_t)((f * nch) % NS) * stage_words;
       const double cs = block_cs<PACK>(mp, gsrc, n_valid, ps->red + 8 * gq, gtid, GW * 32, 1 + gq);
       if (frec) frec[1] = gtimer();
-      pack_window<PACK, T>(g, b, mp, gsrc, n_valid, cs, jp.t * G * T - front * T, rows_s, xs_f, gtid, GW * 32);
+      pack_window<PACK, T, 1, PT>(g, b, mp, gsrc, n_valid, cs, jp.t * G * T - front * T, rows_s, xs_f, gtid,
+                                  GW * 32);
       if (frec) frec[2] = gtimer();
       if (gtid == 0) {
         ps->fcs[f] = cs;
@@ -492,7 +627,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec 
     // consumer warp.  A slot is refilled only after its previous sequence was published and
     // then released by the consumers.
     const int pw = tid >> 5, lane = tid & 31;
-    const int n_sent = kTiledConsWarps / npart;
+    const int n_sent = NCW / npart;
     long long cur_blk_w = -1;
     double c_s_w = 1.0, inv_w = 0.0;
     int pj = 0;
@@ -518,7 +653,15 @@ __global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec 
       } else {
         long long j = -1;
         if (lane == 0) {
-          while (*reinterpret_cast<volatile long long*>(&ps->turn) != m) __nanosleep(256);
+          int sp = 0;
+          while (*reinterpret_cast<volatile long long*>(&ps->turn) != m) spin_wd(sp, 256, 5, m, 0);
+          // bounded claim-ahead: a job claimed long before any warp can start it is work other
+          // SMs can no longer steal (the launch's tail)
+          // (sentinel sequences, after the first failed claim, are never held back)
+          if (e.lookahead > 0)
+            while (*reinterpret_cast<volatile long long*>(&ps->m_end) < 0 &&
+                   m >= (long long)*reinterpret_cast<volatile int*>(&ps->mseq_hi) + e.lookahead)
+              spin_wd(sp, 128, 6, m, 0);
           const long long me = *reinterpret_cast<volatile long long*>(&ps->m_end);
           j = (me >= 0) ? -1 : 0;
         }
@@ -546,28 +689,39 @@ __global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec 
       if (job >= 0) {
         job_block(job, jp, b, gsrc, n_valid);
         const long long blk_id = jp.sig * g.P + jp.w;
-        if (blk_id != cur_blk_w) {
+        if (blk_id != cur_blk_w && !e.dbg_skip_pack && !e.pre_win) {
           cur_blk_w = blk_id;
           c_s_w = warp_cs<PACK>(mp, gsrc, n_valid, lane);   // a2/a3 (Eq. (2))
           inv_w = dequant_scale(c_s_w, e.scal_sig ? e.scal_sig[3 * jp.sig + 1] : mp.c_k);   // Eq. (16)
         }
       }
+      unsigned long long t_pk = 0, t_sl = 0;                 // diagnostics: peak done, slot free
+      if (prec) t_pk = gtimer();
       for (int c = 0; c < nch; ++c) {
         const long long n = m * nch + c;
         const int st = (int)(n % NS);
         if (n >= NS) {
           if (lane == 0)
-            while (*reinterpret_cast<volatile long long*>(&ps->seq[st]) != n - NS) __nanosleep(256);
+          {
+            int sp = 0;
+            while (*reinterpret_cast<volatile long long*>(&ps->seq[st]) != n - NS) spin_wd(sp, 256, 7, n, st);
+          }
           __syncwarp();
           mbar_wait_wd(&ps->empty[st], (uint32_t)(((n / NS) & 1) ^ 1), 1, n, st);
         }
-        if (job >= 0 && !(prepacked && c == 0))
-          pack_window<PACK, T, 2>(g, b, mp, gsrc, n_valid, c_s_w, jp.t * G * T - front * T + c * KC, rows_s,
+        if (prec && c == 0) t_sl = gtimer();
+        if (job >= 0 && !(prepacked && c == 0) && !e.dbg_skip_pack && !e.pre_win)
+          pack_window<PACK, T, 2, PT>(g, b, mp, gsrc, n_valid, c_s_w, jp.t * G * T - front * T + c * KC, rows_s,
                                stg + (size_t)st * stage_words, lane, 32);
         __syncwarp();
         publish(n, st, c, job, inv_w, lane);
       }
-      if (prec) prec[3] = gtimer();
+      if (prec) {
+        prec[3] = gtimer();
+        // m | (claimed -> peak done) << 16 | (peak done -> slot free) << 40, in 16-ns units
+        const unsigned long long d1 = min((t_pk - prec[2]) >> 4, 0xffffffull), d2 = min((t_sl - t_pk) >> 4, 0xffffffull);
+        prec[0] = (unsigned long long)(m & 0xffff) | (d1 << 16) | (d2 << 40);
+      }
     }
     if (tid == 0) {
       // every producer warp has finished claiming once the turn passed all of them
@@ -585,7 +739,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec 
   const int smsp = (tid >> 5) & 3;
   double* wbuf = wout + (size_t)cw * 32 * (T + 1);
   mbar_wait_wd(&ps->bar_taps, 0, 4, 0, 0);
-  // A consumer warp may claim work up to kTiledConsWarps / npart jobs ahead of the producer, i.e. more than
+  // A consumer warp may claim work up to NCW / npart jobs ahead of the producer, i.e. more than
   // one ring lap: a parity wait could then see the slot's previous lap; the sequence number
   // stamped by the producer tells the two apart.
   auto wait_full = [&](long long n, int st) {
@@ -605,7 +759,9 @@ __global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec 
     cl = __shfl_sync(0xffffffffu, cl, 0);
     const long long k = 4LL * cl + smsp;
     const long long mseq = k / npart;
-    const int part = (int)(k % npart);
+    if (lane == 0 && e.lookahead > 0) atomicMax(&ps->mseq_hi, (int)(mseq + 1));
+    // parts rotate over the SMSPs from job to job, so ragged last parts do not pile up on one
+    const int part = (int)((k % npart + mseq) % npart);
     long long n = mseq * nch;
     int st = (int)(n % NS);
     if (PC_REC) ps->cyc[3] = clock64();
@@ -636,31 +792,87 @@ __global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec 
     const JobPos jp = job_pos(e, job);
     const Blk b = block_info<PACK>(g, mp.K, jp.w);
     const int ngroups = (b.M_out + T - 1) / T;
-    const int gl = part * 32 + lane;                         // this thread's group in the tile
+    // FMA core: part p = groups [32 p, 32 p + 32) of the tile, one per lane.  DMMA core: the
+    // tile's m-tiles (8 groups) are split evenly over the parts (e.g. 14 -> 3, 4, 3, 4).
+    int pg0 = part * 32, pgn = 32;                           // the part's first group (in the tile), count
+    if (MMA) {
+      const int nmt_job = (min(G, ngroups - jp.t * G) + 7) >> 3;
+      const int lo = part * nmt_job / npart, hi = (part + 1) * nmt_job / npart;
+      pg0 = 8 * lo;
+      pgn = 8 * (hi - lo);
+    }
+    const int gl = pg0 + lane;                               // this thread's group in the tile
     const int gi = jp.t * G + gl;                            // group index within the block
-    const bool mine = gi < ngroups;
-    const int gi0 = jp.t * G + part * 32;                    // the warp's first group
-    const bool extra = (PACK == PACK_SYM) && gi0 > 0;        // needs B of the word before it
+    const bool mine = gi < ngroups && lane < pgn;
+    const int gi0 = jp.t * G + pg0;                          // the warp's first group
+    const bool extra = (PACK == PACK_SYM) && gi0 > 0 && pgn > 0;   // needs B of the word before it
     double acc[T];
 #pragma unroll
     for (int i = 0; i < T; ++i) acc[i] = 0.0;
+    double fr[4][2][2];                                      // DMMA core: C fragments (see conv_chunk_mma)
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) fr[mt][q >> 1][q & 1] = 0.0;
+    // DMMA core: m-tiles (8 groups) of this part that hold outputs of the block (warp-uniform)
+    const int n_mt = MMA ? min(pgn >> 3, max(0, (ngroups - gi0 + 7) >> 3)) : 0;
     double px = 0.0;                                         // sym: that word's core output (split)
+    if (MMA) {
+      // One core at a time per SM sub-partition, in claim order: a single warp with its 2 NMT
+      // accumulator chains keeps the DMMA pipe busy, while every further warp queued on it
+      // starves the SMSP's other warps (producers, epilogues) of issue -- measured 6-15x
+      // slower loads and FP64 ops with three DMMA warps per SMSP, ~1.1x with one
+      // (tools/dmma_interference.cu).
+      if (lane == 0)
+        for (int sp = 0; *reinterpret_cast<volatile int*>(&ps->core_serve[smsp]) + PC_CORE_SLOTS <= cl;)
+          spin_wd(sp, 64, 8, cl, smsp);
+      __syncwarp();
+    }
     for (int c = 0; c < nch; ++c, ++n) {
       st = (int)(n % NS);
       if (c > 0) wait_full(n, st);
       const double* xs = stg + (size_t)st * stage_words;
-      const double* kc = e.taps_resident ? kr_res + (size_t)c * KC : xs + stage_x;
+      const double* kc = e.taps_resident ? kr_res + (size_t)c * KC : xs + stage_x + TH;
       const int nt = (c == nch - 1) ? mp.K_pad - c * KC : KC;
-      if (mine) conv_chunk_padded<T>(smem_u32(xs) + 8u * (T + 1) * (gl + front), smem_u32(kc), nt, acc);   // a5
+      if (MMA) {                                             // a5 on the tensor cores
+        const uint32_t xrow = smem_u32(xs) + 8u * PT * (pg0 + front);
+        const int jj_n = (c == nch - 1) ? nt / 16 + 1 : KC / 16;   // the last chunk adds the phase tail
+        switch (n_mt) {
+          case 4: conv_chunk_mma<4, PT>(xrow, smem_u32(kc), jj_n, fr, lane); break;
+          case 3: conv_chunk_mma<3, PT>(xrow, smem_u32(kc), jj_n, fr, lane); break;
+          case 2: conv_chunk_mma<2, PT>(xrow, smem_u32(kc), jj_n, fr, lane); break;
+          case 1: conv_chunk_mma<1, PT>(xrow, smem_u32(kc), jj_n, fr, lane); break;
+          default: break;
+        }
+      } else if (mine) {
+        conv_chunk_padded<T>(smem_u32(xs) + 8u * PT * (gl + front), smem_u32(kc), nt, acc);   // a5
+      }
       if (extra) {
-        const int i0 = part * 32 * T + T - 1;                // local word of core word gi0*T - 1
+        const int i0 = pg0 * T + T - 1;                      // local word of core word gi0*T - 1
         for (int j = lane; j < nt; j += 32) {
           const int i = i0 + j;
-          px = fma(xs[(i / T) * (T + 1) + i % T], kc[j], px);
+          px = fma(xs[(i / T) * PT + i % T], kc[j], px);
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&ps->empty[st]);
+    }
+    if (MMA) {                                               // fragments -> group-major rows -> acc[T]
+      __syncwarp();
+      if (lane == 0) atomicAdd(&ps->core_serve[smsp], 1);   // hand the DMMA pipe to the next claim
+      const int r = lane >> 2, k2 = 2 * (lane & 3);
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt2 = 0; nt2 < 2; ++nt2) {
+          double* d = wbuf + (8 * mt + r) * (T + 1) + 8 * nt2 + k2;
+          d[0] = fr[mt][nt2][0];
+          d[1] = fr[mt][nt2][1];
+        }
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < T; ++i) acc[i] = wbuf[lane * (T + 1) + i];
+      __syncwarp();
     }
     if (wrec) wrec[2] = gtimer();
     if (PC_REC) {
@@ -761,7 +973,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec 
         jlo = max(jlo, g_lo - gbase - k0);
         jhi = min(jhi, g_hi - gbase - k0);
         jlo = max(jlo, 0LL);
-        jhi = min(jhi, (long long)(16 * V2));
+        jhi = min(jhi, (long long)((min(pgn, 16 * h + 16) - 16 * h) * V2));   // the part's groups only
         double* dst = rsig + gbase + k0;
 #pragma unroll
         for (int it = 0; it < T; ++it) {
@@ -789,7 +1001,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec 
         long long jhi = min((long long)seg - mw, (long long)b.n_out - k0);
         jhi = min(jhi, g_hi - gbase - k0);
         const long long jlo = max(0LL, g_lo - gbase - k0);
-        flush(rsig + gbase + k0, 1, jlo, min(jhi, (long long)(32 * T)));
+        flush(rsig + gbase + k0, 1, jlo, min(jhi, (long long)(pgn * T)));
       }
     }
     if (e.xc_val) {                                          // warp max, lowest lag on ties
@@ -823,11 +1035,58 @@ __global__ void __launch_bounds__(kTiledThreads, 1) pc_tiled_kernel(Geo g, Exec 
 #undef PC_REC
 }
 
-// ------------------------------------------------------------------ launcher
+// ------------------------------------------------------------------ prepack (a2-a4 ahead)
+// One CTA per job: the block's peak and c_s (Eq. (2)), then the job's stage image -- exactly
+// the words pack_window writes into a ring stage (pitch T + 4) -- into HBM (L2-resident for the
+// tiled launch that follows), and (c_s c_k)^-1 (Eq. (16)).  Moving a2-a4 out of the persistent
+// kernel keeps its producer warps at one bulk copy per job: on a DMMA-saturated SMSP every
+// other warp's instruction issue slows 3-15x (tools/dmma_interference.cu).
 template <int PACK, int T>
+__global__ void __launch_bounds__(256) pc_prepack_kernel(Geo g, Exec e) {
+  __shared__ double red[8];
+  constexpr int PT = T + 4;
+  const ModeP& mp = e.mp[PACK];
+  const long long job = blockIdx.x;
+  const JobPos jp = job_pos(e, job);
+  const Blk b = block_info<PACK>(g, mp.K, jp.w);
+  const double* gsrc = e.s + jp.sig * e.s_stride + (b.g0 - e.s_off);
+  const long long avail = g.L - b.g0;
+  const int n_valid = (int)(avail < 0 ? 0 : (avail > g.W_block ? g.W_block : avail));
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const double cs = block_cs<PACK>(mp, gsrc, n_valid, red, threadIdx.x, 256, 1);
+  const int front = (PACK == PACK_SYM) ? 1 : 0;
+  double* xs = const_cast<double*>(e.pre_win) + job * e.pre_stride;
+  pack_window<PACK, T, 1, PT>(g, b, mp, gsrc, n_valid, cs, jp.t * e.G * T - front * T, e.rows_s, xs, threadIdx.x, 256);
+  if (threadIdx.x == 0)
+    const_cast<double*>(e.pre_inv)[job] = dequant_scale(cs, e.scal_sig ? e.scal_sig[3 * jp.sig + 1] : mp.c_k);
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+cudaError_t launch_prepack(int packing, int T, const Geo& g, const Exec& e, long long n_jobs, cudaStream_t st) {
+  if (n_jobs <= 0) return cudaSuccess;
+  if (T != 16) return cudaErrorInvalidValue;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)n_jobs);
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  switch (packing) {
+    case PACK_SYM: return cudaLaunchKernelEx(&cfg, pc_prepack_kernel<PACK_SYM, 16>, g, e);
+    case PACK_ASYM2: return cudaLaunchKernelEx(&cfg, pc_prepack_kernel<PACK_ASYM2, 16>, g, e);
+    case PACK_ASYM3: return cudaLaunchKernelEx(&cfg, pc_prepack_kernel<PACK_ASYM3, 16>, g, e);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// ------------------------------------------------------------------ launcher
+template <int PACK, int T, int MMA>
 static cudaError_t launch_tiled_t(const Geo& g, const Exec& e, long long n_jobs, int threads, size_t smem,
                                   cudaStream_t st, int* grid_out) {
-  auto kfn = pc_tiled_kernel<PACK, T>;
+  auto kfn = pc_tiled_kernel<PACK, T, MMA>;
   static size_t c_smem = 0;
   static int c_threads = 0, c_grid = 0, c_dev = -1, c_sms = 0;
   int dev = 0;
@@ -865,26 +1124,28 @@ static cudaError_t launch_tiled_t(const Geo& g, const Exec& e, long long n_jobs,
   return cudaLaunchKernelEx(&cfg, kfn, g, ex);
 }
 
-template <int T>
+template <int T, int MMA>
 static cudaError_t launch_tiled_T(int packing, const Geo& g, const Exec& e, long long n_jobs, int threads, size_t smem,
                                   cudaStream_t st, int* grid_out) {
   switch (packing) {
-    case PACK_FULL: return launch_tiled_t<PACK_FULL, T>(g, e, n_jobs, threads, smem, st, grid_out);
-    case PACK_SYM: return launch_tiled_t<PACK_SYM, T>(g, e, n_jobs, threads, smem, st, grid_out);
-    case PACK_ASYM2: return launch_tiled_t<PACK_ASYM2, T>(g, e, n_jobs, threads, smem, st, grid_out);
-    case PACK_ASYM3: return launch_tiled_t<PACK_ASYM3, T>(g, e, n_jobs, threads, smem, st, grid_out);
+    case PACK_FULL: return launch_tiled_t<PACK_FULL, T, MMA>(g, e, n_jobs, threads, smem, st, grid_out);
+    case PACK_SYM: return launch_tiled_t<PACK_SYM, T, MMA>(g, e, n_jobs, threads, smem, st, grid_out);
+    case PACK_ASYM2: return launch_tiled_t<PACK_ASYM2, T, MMA>(g, e, n_jobs, threads, smem, st, grid_out);
+    case PACK_ASYM3: return launch_tiled_t<PACK_ASYM3, T, MMA>(g, e, n_jobs, threads, smem, st, grid_out);
   }
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_tiled(int packing, int T, const Geo& g, const Exec& e, long long n_jobs, int threads, size_t smem,
-                         cudaStream_t st, int* grid_out) {
+cudaError_t launch_tiled(int packing, int T, int mma, const Geo& g, const Exec& e, long long n_jobs, int threads,
+                         size_t smem, cudaStream_t st, int* grid_out) {
   *grid_out = 0;
   if (n_jobs <= 0) return cudaSuccess;
+  if (mma) return T == 16 ? launch_tiled_T<16, 1>(packing, g, e, n_jobs, threads, smem, st, grid_out)
+                          : cudaErrorInvalidValue;
   switch (T) {
-    case 12: return launch_tiled_T<12>(packing, g, e, n_jobs, threads, smem, st, grid_out);
-    case 14: return launch_tiled_T<14>(packing, g, e, n_jobs, threads, smem, st, grid_out);
-    case 16: return launch_tiled_T<16>(packing, g, e, n_jobs, threads, smem, st, grid_out);
+    case 12: return launch_tiled_T<12, 0>(packing, g, e, n_jobs, threads, smem, st, grid_out);
+    case 14: return launch_tiled_T<14, 0>(packing, g, e, n_jobs, threads, smem, st, grid_out);
+    case 16: return launch_tiled_T<16, 0>(packing, g, e, n_jobs, threads, smem, st, grid_out);
   }
   return cudaErrorInvalidValue;
 }

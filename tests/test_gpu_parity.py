@@ -30,9 +30,10 @@ def dev(x):
 
 
 def gpu_run(s, k, W_block, packing, Q, mode=O.CONV, eps_rule=O.EPS_POW2, rmax_rule=O.RMAX_PAPER, debug=True,
-            tile=0, npart=0, exec_=0):
+            tile=0, npart=0, exec_=0, core=0):
     opts = pcb.opts_default(eps_rule=EPS[eps_rule], rmax_rule=rmax_rule, bound_policy=pcb.BOUND_WARN, exec=exec_)
     opts.reserved[1] = tile
+    opts.reserved[2] = core     # direct core: 0 auto (FP64 tensor cores, T = 16), 1 FP64 FMA, 2 DMMA
     opts.reserved[3] = npart
     with pcb.Plan(len(s), len(k), W_block, mode, PK[packing], Q, opts=opts) as p:
         p.set_kernel(dev(k))
@@ -77,10 +78,10 @@ SMALL_CASES = [  # (L, N, W_block, Q): several tiles, ragged tails, P = 1, N = 1
 ]
 
 
-@pytest.mark.parametrize("exec_", [0, 2, 1])      # auto, tiled, per-block
+@pytest.mark.parametrize("exec_,core", [(0, 0), (2, 2), (2, 1), (1, 0)])   # auto, tiled DMMA / FMA, per-block
 @pytest.mark.parametrize("packing", [O.SYM, O.ASYM2, O.ASYM3])
 @pytest.mark.parametrize("case", SMALL_CASES)
-def test_packed_bit_exact_pow2(packing, case, exec_):
+def test_packed_bit_exact_pow2(packing, case, exec_, core):
     L, N, W_block, Q = case
     rng = np.random.default_rng(L * 7 + N)
     s, k = rng.laplace(0, 0.3, L), rng.uniform(-1, 1, N)
@@ -88,7 +89,7 @@ def test_packed_bit_exact_pow2(packing, case, exec_):
     Q = min(Q, O.max_q_under_bound(None, Np, packing, O.EPS_POW2, O.RMAX_PAPER))   # Eq. (3) within bound
     ref = O.conv_pipeline(s, k, W_block, packing, Q, keep_blocks=True)
     assert ref.kernel.bound_ok and ref.mismatches == 0
-    g = gpu_run(s, k, W_block, packing, Q, exec_=exec_)
+    g = gpu_run(s, k, W_block, packing, Q, exec_=exec_, core=core)
     assert g["info"]["c_k"] == ref.kernel.c_k and g["info"]["R_max"] == ref.kernel.R
     assert g["info"]["eps_inv"] == ref.kernel.eps.eps_inv
     check_blocks(g, ref, packing)
@@ -96,29 +97,31 @@ def test_packed_bit_exact_pow2(packing, case, exec_):
     assert np.array_equal(g["r"], ref.out)
 
 
-@pytest.mark.parametrize("tile", [12, 14, 16])
+@pytest.mark.parametrize("tile,core", [(12, 1), (14, 1), (16, 1), (16, 2)])
 @pytest.mark.parametrize("packing", [O.FULL, O.SYM, O.ASYM2, O.ASYM3])
 @pytest.mark.parametrize("case", [(20000, 513, 4096, 31), (4097, 64, 1024, 60), (9000, 100, 512, 15)])
-def test_every_core_tile(tile, packing, case):
-    """The persistent kernel's tile T (12/14/16) is chosen per plan; force each one."""
+def test_every_core_tile(tile, core, packing, case):
+    """The tiled kernel's core: the FP64 FMA loop at T = 12/14/16 and the FP64 tensor-core
+    (DMMA) Toeplitz core at T = 16; force each one."""
     L, N, W_block, Q = case
     rng = np.random.default_rng(N + tile)
     s, k = rng.laplace(0, 0.3, L), rng.uniform(-1, 1, N)
     if packing == O.FULL:
-        g = gpu_run(s, k, W_block, O.FULL, 0, debug=False, tile=tile)
+        g = gpu_run(s, k, W_block, O.FULL, 0, debug=False, tile=tile, core=core)
         want = O.full_precision(s, k)
         assert np.max(np.abs(g["r"] - want)) / np.max(np.abs(want)) < 1e-12
         return
     Q = min(Q, O.max_q_under_bound(None, N | 1, packing, O.EPS_POW2, O.RMAX_PAPER))
     ref = O.conv_pipeline(s, k, W_block, packing, Q)
-    g = gpu_run(s, k, W_block, packing, Q, debug=False, tile=tile)
+    g = gpu_run(s, k, W_block, packing, Q, debug=False, tile=tile, core=core)
     assert np.array_equal(g["r"], ref.out)
 
 
+@pytest.mark.parametrize("core", [2, 1])
 @pytest.mark.parametrize("npart", [1, 2, 4])
 @pytest.mark.parametrize("packing", [O.FULL, O.SYM, O.ASYM2, O.ASYM3])
 @pytest.mark.parametrize("mode", [O.CONV, O.XCORR])
-def test_every_parts_per_job(npart, packing, mode):
+def test_every_parts_per_job(npart, packing, mode, core):
     """The tiled kernel splits a job into npart warp parts (G = 32 npart groups), each claimed
     by a consumer warp of one SM sub-partition; force each split (ring depth, sentinel count
     16/npart and the per-warp symmetric B hand-over all change with it)."""
@@ -126,13 +129,13 @@ def test_every_parts_per_job(npart, packing, mode):
     rng = np.random.default_rng(npart * 10 + packing)
     s, k = np.clip(rng.laplace(0, 0.3, L), -1, 1), rng.uniform(-1, 1, N)
     if packing == O.FULL:
-        g = gpu_run(s, k, W_block, O.FULL, 0, mode=mode, debug=False, npart=npart)
+        g = gpu_run(s, k, W_block, O.FULL, 0, mode=mode, debug=False, npart=npart, core=core)
         want = O.full_precision(s, k, mode=mode)
         assert np.max(np.abs(g["r"] - want)) / np.max(np.abs(want)) < 1e-12
         return
     Q = min(Q, O.max_q_under_bound(None, N | 1, packing, O.EPS_POW2, O.RMAX_PAPER))
     ref = O.conv_pipeline(s, k, W_block, packing, Q, mode=mode)
-    g = gpu_run(s, k, W_block, packing, Q, mode=mode, debug=False, npart=npart)
+    g = gpu_run(s, k, W_block, packing, Q, mode=mode, debug=False, npart=npart, core=core)
     assert np.array_equal(g["r"], ref.out)
 
 
@@ -395,23 +398,24 @@ def test_cfg1_full_size_all_packings():
 
 
 # --------------------------------------------------------------------- large kernels: tap chunks, tiles
+@pytest.mark.parametrize("core", [2, 1])
 @pytest.mark.parametrize("packing", [O.FULL, O.SYM, O.ASYM2, O.ASYM3])
 @pytest.mark.parametrize("case", [(70000, 4096, 16384), (40000, 1024, 16384), (100000, 8192, 32768)])
-def test_large_kernels_tap_chunks_and_tiles(packing, case):
+def test_large_kernels_tap_chunks_and_tiles(packing, case, core):
     """cfg3/cfg4-shaped geometries: taps processed in chunks, blocks split into several
     output tiles (the symmetric tile boundary uses the extra-word path)."""
     L, N, W_block = case
     rng = np.random.default_rng(N)
     s, k = rng.laplace(0, 0.3, L), rng.normal(0, 1 / np.sqrt(N), N)
     if packing == O.FULL:
-        g = gpu_run(s, k, W_block, O.FULL, 0, debug=False)
+        g = gpu_run(s, k, W_block, O.FULL, 0, debug=False, core=core)
         want = O.full_precision(s, k)
         assert np.max(np.abs(g["r"] - want)) / np.max(np.abs(want)) < 1e-12
         return
     Q = 3 if packing != O.ASYM2 else 127
     ref = O.conv_pipeline(s, k, W_block, packing, Q, rmax_rule=O.RMAX_L1)
     assert ref.kernel.bound_ok and ref.mismatches == 0
-    g = gpu_run(s, k, W_block, packing, Q, rmax_rule=O.RMAX_L1, debug=False)
+    g = gpu_run(s, k, W_block, packing, Q, rmax_rule=O.RMAX_L1, debug=False, core=core)
     assert np.array_equal(g["r"], ref.out)
 
 
@@ -708,3 +712,35 @@ def test_xcorr_pairs_per_pair_kernels(packing, Q):
             assert ref.kernel.bound_ok and ref.mismatches == 0
             assert (sc[i], lag[i]) == O.xcorr_score(ref.out), i
     assert np.all(lag - (B - 1) == -delay)
+
+
+# --------------------------------------------------------------------- DMMA core variants
+@pytest.mark.parametrize("opt", ["prepack", "lookahead", "alu_pack", "fma_sym_auto"])
+@pytest.mark.parametrize("packing", [O.SYM, O.ASYM2, O.ASYM3])
+@pytest.mark.parametrize("mode", [O.CONV, O.XCORR])
+def test_dmma_core_variants(opt, packing, mode):
+    """The DMMA-core kernel's alternative schedules give bit-identical results: a2-a4 in a
+    prepack kernel ahead of it (conv_opts.reserved[8] = 2), a bounded producer claim-ahead
+    (reserved[7] = -2), integer-pipe companding and packing (reserved[6] = 1), and the auto
+    core choice (DMMA, FMA for symmetric packing)."""
+    L, N, W_block, Q = 90_000, 301, 4096, 31
+    rng = np.random.default_rng(packing * 7 + mode)
+    s, k = np.clip(rng.laplace(0, 0.3, L), -1, 1), rng.uniform(-1, 1, N)
+    Q = min(Q, O.max_q_under_bound(None, N | 1, packing, O.EPS_POW2, O.RMAX_PAPER))
+    ref = O.conv_pipeline(s, k, W_block, packing, Q, mode=mode)
+    opts = pcb.opts_default(bound_policy=pcb.BOUND_WARN, exec=2)
+    if opt == "prepack":
+        opts.reserved[2], opts.reserved[8] = 2, 2
+    elif opt == "lookahead":
+        opts.reserved[2], opts.reserved[7] = 2, -2
+    elif opt == "alu_pack":
+        opts.reserved[2], opts.reserved[6] = 2, 1
+    with pcb.Plan(L, N, W_block, mode, PK[packing], Q, opts=opts) as p:
+        p.set_kernel(dev(k))
+        info = p.info()
+        assert info["core_mma"] == (0 if (opt == "fma_sym_auto" and packing == O.SYM) else 1)
+        r = torch.full((info["L_out"],), float("nan"), dtype=torch.float64, device=DEV)
+        for _ in range(2):                       # twice: the queues / buffers are reused
+            p.execute(dev(s), r)
+        torch.cuda.synchronize()
+    assert np.array_equal(r.cpu().numpy(), ref.out)

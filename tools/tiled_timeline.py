@@ -1,7 +1,9 @@
 """Per-CTA timeline of the tiled persistent kernel (conv_execute_profile): how many CTAs are
 resident per SM over time, per-job core durations, fill, and consumer cycle split.
-    python tools/tiled_timeline.py [workload=cfg2] [L] > out.json"""
+    python tools/tiled_timeline.py [workload=cfg2] [L] > out.json
+    PC_OPT="2=1,3=4" sets conv_opts.reserved[i] = v (e.g. 2=1: the FP64 FMA core)"""
 import json
+import os
 import sys
 
 import numpy as np
@@ -33,7 +35,11 @@ KTP = KTW + 148 * 16 * 16 * 4
 rec = torch.zeros(KTP + 148 * 4 * 16 * 4, dtype=torch.int64, device=dev)
 out = {}
 for name, (pk, Q, rm) in points.items():
-    with pcb.Plan(len(s), len(k), W_block, 0, pk, Q, rmax_rule=rm) as p:
+    o = pcb.opts_default(rmax_rule=rm)
+    for kv in filter(None, os.environ.get("PC_OPT", "").split(",")):
+        i, v = kv.split("=")
+        o.reserved[int(i)] = int(v)
+    with pcb.Plan(len(s), len(k), W_block, 0, pk, Q, opts=o) as p:
         p.set_kernel(torch.from_numpy(k).to(dev))
         for _ in range(3):
             p.execute(S, R)
@@ -89,11 +95,16 @@ for name, (pk, Q, rm) in points.items():
     ztot = max(1.0, float(np.sum(live)))
     zsplit = {k: round(v / ztot, 4) for k, v in zsplit.items()}
     def cta_trace(c):
-        prod = [[int(Pr[c, w, j, 0]), round((Pr[c, w, j, 3] - t0) / 1e3, 1)] for w in range(4) for j in range(16)
-                if Pr[c, w, j, 3]]
+        def prow(w, j):
+            v = int(Pr[c, w, j, 0])
+            tc = (Pr[c, w, j, 2] - t0) / 1e3
+            tp = tc + ((v >> 16) & 0xffffff) * 16 / 1e3
+            return [v & 0xffff, w, round((Pr[c, w, j, 1] - t0) / 1e3, 1), round(tc, 1), round(tp, 1),
+                    round(tp + (v >> 40) * 16 / 1e3, 1), round((Pr[c, w, j, 3] - t0) / 1e3, 1)]
+        prod = [prow(w, j) for w in range(4) for j in range(15) if Pr[c, w, j, 3]]
         cons = [[w, int(W[c, w, j, 0]), round((W[c, w, j, 1] - t0) / 1e3, 1), round((W[c, w, j, 2] - t0) / 1e3, 1),
                  round((W[c, w, j, 3] - t0) / 1e3, 1)] for w in range(16) for j in range(16) if W[c, w, j, 1]]
-        return {"produced[mseq,t_pub]": sorted(prod), "consumed[warp,mseq,t_ready,t_core,t_stored]": sorted(cons, key=lambda x: x[2])}
+        return {"produced[mseq,warp,t_start,t_claimed,t_peak,t_slot,t_pub]": sorted(prod), "consumed[warp,mseq,t_ready,t_core,t_stored]": sorted(cons, key=lambda x: x[2])}
     fill_phases = (Pr[:, :, 15, :3].astype(float) - r[:, 1][:, None, None]) / 1e3   # claimed, peak, packed (us)
     fill_stats = {k: round(float(np.median(fill_phases[:, :, i])), 2) for i, k in enumerate(["claimed", "peak", "packed"])}
     crit = int(np.argmax(r[:, 2]))                  # the CTA that ends last
