@@ -216,6 +216,19 @@ int conv_execute_debug(conv_plan* plan, const double* s_dev, double* r_dev, doub
 int conv_adapt_block(conv_plan* plan, const double* s_dev, double snr_floor_db,
                      double calib_offset_db, conv_block_decision* out_host, void* stream);
 
+/* Single-point calibration of the Eq. (19) SNR model (Fig. 5: "calibrated via a single
+ * measurement at the coarsest quantization (S_q = K_q = 8)"; reading C18).  Runs the plan's
+ * geometry (L, N, W_block, mode, options) on s_dev (L samples, device) with kernel k_dev (N taps,
+ * device) twice -- packed at S_q = K_q = Q (the plan's packing if SYM/ASYM3, else ASYM2; at Q = 8
+ * every exact packing gives the same integers) and full precision -- and returns the measured
+ * SNR over all outputs, the model's prediction sum_b (sigma_b sigma_k)^2 / sum_b D_b (per-block
+ * Eq. (19) terms, P:222 statistics) and offset_db = measured - model, the calib_offset_db for
+ * conv_adapt_block.  Temporary plans and buffers (2 L_out doubles) are created and freed inside;
+ * synchronizes `stream`.  PC_E_CONFIG on invalid arguments, PC_E_BOUND if Q exceeds the packing's
+ * bound under STRICT. */
+int conv_snr_calibrate(conv_plan* plan, const double* s_dev, const double* k_dev, int32_t Q,
+                       double* offset_db, double* measured_db, double* model_db, void* stream);
+
 /* Diagnostics: conv_execute that records, when the tiled kernel or the FFT core runs, a
  * timeline into cta_records_dev (uint64, at least 24*148*32 + 148*16*16*4 + 148*4*16*4 entries,
  * zeroed by the caller): tiled kernel -- per CTA c {SM id, start / end %globaltimer (ns), jobs}

@@ -543,6 +543,38 @@ def adapt_decisions(s, k, W_block, floor_db, calib_offset_db=0.0, candidates=(SY
     return out, qmode
 
 
+def snr_calibration(s, k, W_block, Q=8, packing=ASYM2, mode=CONV, eps_rule=EPS_POW2, rmax_rule=RMAX_PAPER):
+    """Single-point calibration of the Eq. (19) SNR model (Fig. 5: "calibrated via a
+    single measurement at the coarsest quantization (S_q = K_q = 8)"; reading C18).  Measure
+    the packed pipeline's SNR against full precision at S_q = K_q = Q over the whole signal,
+    predict it with Eq. (19) per block -- signal power (sigma_s sigma_k)^2 and noise D_b of
+    snr_linear, blocks of equal size, so the signal-level prediction is sum(signal)/sum(noise)
+    -- and return (offset_db = measured - model, measured_db, model_db).  The offset is what
+    adapt_decisions adds to every prediction."""
+    s = np.asarray(s, dtype=np.float64)
+    ref = full_precision(s, k, mode=mode)
+    out = conv_pipeline(s, k, W_block, packing, Q, mode=mode, eps_rule=eps_rule, rmax_rule=rmax_rule).out
+    measured = measured_snr_db(ref, out)
+    geom = Geometry(s.shape[0], len(k), W_block)
+    kp = np.zeros(geom.Np)
+    kp[:len(k)] = k
+    sig_k, pk = kernel_sigma(kp)
+    num = 0.0
+    den = 0.0
+    for w in range(geom.P):
+        sig_s, ps = block_sigma(geom.block_input(s, w))
+        v_s = ps / (Q * SQRT12)                          # snr_linear's terms, same order
+        v_k = pk / (Q * SQRT12)
+        a = sig_s * v_k
+        b = sig_k * v_s
+        c = v_k * v_s
+        den += (a * a + b * b) + c * c
+        n = sig_s * sig_k
+        num += n * n
+    model = 10.0 * math.log10(num / den)
+    return measured - model, measured, model
+
+
 # ----------------------------------------------------------------------------- Table 1
 
 def flop_count(packing, domain, N):

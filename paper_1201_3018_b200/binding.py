@@ -84,6 +84,7 @@ def load():
             "conv_xcorr_pairs": (C.c_int, [P, VP, I64, I64, VP, VP, VP]),
             "conv_execute_debug": (C.c_int, [P, VP, VP, VP, VP, VP, VP, VP]),
             "conv_adapt_block": (C.c_int, [P, VP, D, D, C.POINTER(conv_block_decision), VP]),
+            "conv_snr_calibrate": (C.c_int, [P, VP, VP, I32, C.POINTER(D), C.POINTER(D), C.POINTER(D), VP]),
             "conv_plan_query": (C.c_int, [P, C.POINTER(conv_plan_info)]),
             "conv_execute_profile": (C.c_int, [P, VP, VP, VP, C.POINTER(C.c_int32), VP]),
             "conv_shard_range": (C.c_int, [I64, I32, I32, I32, I32, I32, C.POINTER(conv_shard)]),
@@ -203,6 +204,14 @@ def adapt_block(plan, s_dev, snr_floor_db, calib_offset_db=0.0, P=None, stream=N
     return [(d.packing, d.Q, d.snr_lin) for d in out] if out is not None else None
 
 
+def snr_calibrate(plan, s_dev, k_dev, Q=8, stream=None):
+    """Single-point SNR-model calibration: returns (offset_db, measured_db, model_db)."""
+    off, meas, model = C.c_double(), C.c_double(), C.c_double()
+    _check(load().conv_snr_calibrate(plan, _ptr(s_dev), _ptr(k_dev), int(Q), C.byref(off), C.byref(meas),
+                                     C.byref(model), _stream(stream)), "conv_snr_calibrate")
+    return off.value, meas.value, model.value
+
+
 def execute_profile(plan, s_dev, r_dev, records_dev, stream=None):
     """Returns the persistent grid size; records_dev (uint64, 4*148*32) gets per-CTA
     {smid, t_start_ns, t_end_ns, blocks}."""
@@ -280,6 +289,9 @@ class Plan:
 
     def adapt_block(self, s_dev, floor_db, calib_offset_db=0.0, stream=None):
         return adapt_block(self.h, s_dev, floor_db, calib_offset_db, self.info()["P"], stream)
+
+    def snr_calibrate(self, s_dev, k_dev, Q=8, stream=None):
+        return snr_calibrate(self.h, s_dev, k_dev, Q, stream)
 
     def info(self):
         return plan_query(self.h)

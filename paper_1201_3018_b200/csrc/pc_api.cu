@@ -1120,6 +1120,63 @@ int conv_xcorr_max(conv_plan* p, const double* db, int64_t n_signals, int64_t s_
   return PC_OK;
 }
 
+int conv_snr_calibrate(conv_plan* p, const double* s, const double* k, int32_t Q, double* offset_db,
+                       double* measured_db, double* model_db, void* stream) {
+  if (!p || !s || !k || Q < 1) return PC_E_CONFIG;
+  if (cudaSetDevice(p->device) != cudaSuccess) return PC_E_CUDA;
+  cudaStream_t st = (cudaStream_t)stream;
+  // any exact packing gives the same integer results at S_q = K_q = Q; the plan's own if packed
+  const int pk = (p->packing == PC_PACK_SYM || p->packing == PC_PACK_ASYM3) ? p->packing : PC_PACK_ASYM2;
+  conv_opts o = p->opts;
+  o.core = PC_CORE_DIRECT;
+  conv_plan *pq = nullptr, *pf = nullptr;
+  double *d_ref = nullptr, *d_x = nullptr, *d_st = nullptr;
+  const long long L_out = p->mode == PC_MODE_XCORR ? p->L - p->N + 1 : p->L + p->N - 1;
+  const long long P = p->P;
+  int rc = conv_plan_create(&pq, p->L, p->N, p->W_block, p->mode, pk, Q, &o);
+  if (!rc) rc = conv_plan_create(&pf, p->L, p->N, p->W_block, p->mode, PC_PACK_FULL, 0, &o);
+  if (!rc) rc = conv_plan_set_kernel(pq, k, stream);
+  if (!rc) rc = conv_plan_set_kernel(pf, k, stream);
+  if (!rc && (cudaMalloc(&d_ref, sizeof(double) * L_out) != cudaSuccess ||
+              cudaMalloc(&d_x, sizeof(double) * L_out) != cudaSuccess ||
+              cudaMalloc(&d_st, sizeof(double) * (2 * P + 2 + 4)) != cudaSuccess))
+    rc = PC_E_CUDA;
+  if (!rc) rc = conv_execute(pf, s, d_ref, stream);
+  if (!rc) rc = conv_execute(pq, s, d_x, stream);
+  double h[6] = {0, 0, 0, 0, 0, 0};
+  if (!rc) {
+    // sigma_s, peak per block and sigma_k, ||k||_inf (reading C12), then the sums
+    Geo gk;
+    std::memset(&gk, 0, sizeof(gk));
+    gk.L = pq->Np;
+    gk.P = 1;
+    gk.W_block = pq->Np;
+    gk.W = pq->Np;
+    double* d_sk = d_st + 2 * P;
+    cudaError_t e = pc::launch_block_stats(make_geo(pq), s, d_st, d_st + P, st);
+    if (e == cudaSuccess) e = pc::launch_block_stats(gk, pq->d_k_pad, d_sk, d_sk + 1, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h, d_sk, 2 * sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess)
+      e = pc::launch_snr_sums(d_ref, d_x, L_out, d_st, d_st + P, P, h[0], h[1], (double)Q, d_sk + 2, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h + 2, d_sk + 2, 4 * sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = PC_E_CUDA;
+  }
+  cudaFree(d_ref);
+  cudaFree(d_x);
+  cudaFree(d_st);
+  conv_plan_destroy(pq);
+  conv_plan_destroy(pf);
+  if (rc) return rc;
+  const double meas = h[3] == 0.0 ? INFINITY : 10.0 * std::log10(h[2] / h[3]);
+  const double model = 10.0 * std::log10(h[4] / h[5]);
+  if (measured_db) *measured_db = meas;
+  if (model_db) *model_db = model;
+  if (offset_db) *offset_db = meas - model;
+  return PC_OK;
+}
+
 int conv_adapt_block(conv_plan* p, const double* s, double snr_floor_db, double calib_offset_db,
                      conv_block_decision* out, void* stream) {
   if (!p || !s) return PC_E_CONFIG;

@@ -596,6 +596,51 @@ cudaError_t launch_xcorr_reduce(const double* val, const long long* lag, long lo
   return cudaGetLastError();
 }
 
+// Reductions of the single-point SNR calibration (reading C18), one CTA, fixed order:
+// out[0] = sum ref^2, out[1] = sum (ref - x)^2 over n outputs, out[2] = sum_b (sigma_b sigma_k)^2,
+// out[3] = sum_b D_b with D_b Eq. (19)'s noise terms at S_q = K_q = Q (the oracle's
+// snr_linear operation order per block; the sums differ from NumPy's only in order).
+__global__ void __launch_bounds__(1024) pc_snr_sums(const double* __restrict__ ref, const double* __restrict__ x,
+                                                    long long n, const double* __restrict__ sigma,
+                                                    const double* __restrict__ peak, long long P, double sig_k,
+                                                    double peak_k, double Q, double* __restrict__ out) {
+  __shared__ double red[4][32];
+  const int tid = threadIdx.x;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  for (long long i = tid; i < n; i += blockDim.x) {
+    const double r = ref[i], d = __dsub_rn(r, x[i]);
+    s0 = __dadd_rn(s0, __dmul_rn(r, r));
+    s1 = __dadd_rn(s1, __dmul_rn(d, d));
+  }
+  const double q12 = __dmul_rn(Q, 3.4641016151377544);   // Q sqrt(12), sqrt(12) correctly rounded
+  for (long long b = tid; b < P; b += blockDim.x) {
+    const double v_s = __ddiv_rn(peak[b], q12), v_k = __ddiv_rn(peak_k, q12);
+    const double a = __dmul_rn(sigma[b], v_k), bb = __dmul_rn(sig_k, v_s), c = __dmul_rn(v_k, v_s);
+    const double D = __dadd_rn(__dadd_rn(__dmul_rn(a, a), __dmul_rn(bb, bb)), __dmul_rn(c, c));
+    const double nn = __dmul_rn(sigma[b], sig_k);
+    s2 = __dadd_rn(s2, __dmul_rn(nn, nn));
+    s3 = __dadd_rn(s3, D);
+  }
+  double v[4] = {s0, s1, s2, s3};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    for (int o = 16; o > 0; o >>= 1) v[q] = __dadd_rn(v[q], __shfl_xor_sync(0xffffffffu, v[q], o));
+    if ((tid & 31) == 0) red[q][tid >> 5] = v[q];
+  }
+  __syncthreads();
+  if (tid < 4) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) t = __dadd_rn(t, red[tid][w]);
+    out[tid] = t;
+  }
+}
+
+cudaError_t launch_snr_sums(const double* ref, const double* x, long long n, const double* sigma, const double* peak,
+                            long long P, double sig_k, double peak_k, double Q, double* out, cudaStream_t st) {
+  pc_snr_sums<<<1, 1024, 0, st>>>(ref, x, n, sigma, peak, P, sig_k, peak_k, Q, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_xcorr_max(const double* c, long long n_signals, long long n_lags, long long stride,
                              double* score, long long* lag, cudaStream_t st) {
   pc_xcorr_max<<<(unsigned)n_signals, 1024, 0, st>>>(c, n_lags, stride, score, lag);

@@ -144,6 +144,8 @@ cudaError_t launch_adapt_decide(long long P, const double* sigma, const double* 
 cudaError_t launch_adapt_lists(long long P, const int* dec_pack, int* lists, int* counts, cudaStream_t st);
 cudaError_t launch_xcorr_reduce(const double* val, const long long* lag, long long n_signals, long long n_part,
                                 double* score, long long* best, cudaStream_t st);
+cudaError_t launch_snr_sums(const double* ref, const double* x, long long n, const double* sigma, const double* peak,
+                            long long P, double sig_k, double peak_k, double Q, double* out, cudaStream_t st);
 cudaError_t launch_xcorr_max(const double* c, long long n_signals, long long n_lags, long long stride,
                              double* score, long long* lag, cudaStream_t st);
 

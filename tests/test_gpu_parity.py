@@ -744,3 +744,25 @@ def test_dmma_core_variants(opt, packing, mode):
             p.execute(dev(s), r)
         torch.cuda.synchronize()
     assert np.array_equal(r.cpu().numpy(), ref.out)
+
+
+@pytest.mark.parametrize("mode", [O.CONV, O.XCORR])
+@pytest.mark.parametrize("sig", ["uniform", "cfg2"])
+def test_snr_calibration_matches_oracle(sig, mode):
+    """conv_snr_calibrate (reading C18) against oracle.snr_calibration: the packed and
+    full-precision outputs are the CUDA path's (bit-exact / 1e-12), the block statistics are
+    bit-identical (C12), only the summation order of the four sums differs -- so the measured
+    SNR, the model and the offset agree to 1e-9 dB; the offset then drives conv_adapt_block."""
+    rng = np.random.default_rng(5 + mode)
+    if sig == "uniform":
+        s, k, W_block = rng.uniform(-128, 128, 1 << 16), rng.uniform(-128, 128, 401), 8192
+    else:
+        s, k = WL.cfg2(seed=3, L=1 << 17)
+        W_block = 4096
+    off, meas, model = O.snr_calibration(s, k, W_block, Q=8, packing=O.ASYM2, mode=mode)
+    opts = pcb.opts_default(bound_policy=pcb.BOUND_WARN)
+    with pcb.Plan(len(s), len(k), W_block, mode, PK[O.ASYM2], 8, opts=opts) as p:
+        g_off, g_meas, g_model = p.snr_calibrate(dev(s), dev(k), 8)
+    assert abs(g_meas - meas) < 1e-9 and abs(g_model - model) < 1e-9 and abs(g_off - off) < 1e-9
+    if sig == "uniform":
+        assert abs(g_off) < 1.0

@@ -419,3 +419,24 @@ def test_stereo_workload_delay_and_pairs():
     for i in (1, 5):
         c = np.array([np.dot(x[i, j:j + B], q[i]) for j in range(2 * B - 1)])   # valid lags, brute force
         assert int(np.argmax(c)) - (B - 1) == -d
+
+
+def test_snr_calibration_single_point():
+    """P:230 / Fig. 5 (reading C18): the model calibrated by one measurement at S_q = K_q = 8.
+    Pins: for the paper's i.i.d. uniform setting Eq. (19)'s assumptions hold, so the
+    offset is within 1 dB of zero and the calibrated prediction at Q = 16 lands within 0.5 dB of the
+    measurement (P:166 prints 27.1 predicted vs 27.5 measured); at Q = 8 the integer results
+    are exact for every packing, so the offset is packing-independent; and model + offset
+    reproduces the measurement by construction."""
+    rng = np.random.default_rng(11)
+    s, k = rng.uniform(-128, 128, 1 << 15), rng.uniform(-128, 128, 401)
+    off, meas, model = O.snr_calibration(s, k, 8192, Q=8, packing=O.ASYM2, rmax_rule=O.RMAX_L1)
+    assert abs(off) < 1.0 and math.isclose(model + off, meas, rel_tol=0, abs_tol=1e-12)
+    for pk in (O.SYM, O.ASYM3):
+        off2, meas2, model2 = O.snr_calibration(s, k, 8192, Q=8, packing=pk, rmax_rule=O.RMAX_L1)
+        assert meas2 == meas and model2 == model and off2 == off
+    out16 = O.conv_pipeline(s, k, 8192, O.ASYM2, 16, rmax_rule=O.RMAX_L1).out
+    meas16 = O.measured_snr_db(O.full_precision(s, k), out16)
+    _, _, model16 = O.snr_calibration(s, k, 8192, Q=16, packing=O.ASYM2, rmax_rule=O.RMAX_L1)
+    assert abs((model16 + off) - meas16) < 0.5
+    assert 26.0 < meas16 < 28.5                      # the paper's 27.5 dB regime (P:166)
