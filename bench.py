@@ -347,6 +347,9 @@ def run_ours(args, ws, rank, local):
                         0 if adaptive else Q, opts=opts)
         plan.set_kernel(k_d)
         info = plan.info()
+        calib = 0.0
+        if adaptive:                                 # §IV.D: the model calibrated once at S_q = K_q = 8
+            calib, _, _ = plan.snr_calibrate(S[0], k_d, 8)
         if xcorr:
             score = torch.empty(nsig, dtype=torch.float64, device=dev)
             lag = torch.empty(nsig, dtype=torch.int64, device=dev)
@@ -355,7 +358,7 @@ def run_ours(args, ws, rank, local):
             if xcorr:
                 plan.xcorr_max(S[0], nsig, L, score, lag)
             elif adaptive:
-                pcb.adapt_block(plan.h, S[i % n_buf], Q, 0.0, None)
+                pcb.adapt_block(plan.h, S[i % n_buf], Q, calib, None)
                 plan.execute(S[i % n_buf], R[i % n_buf])
             else:
                 plan.execute(S[i % n_buf], R[i % n_buf])
@@ -410,7 +413,7 @@ def run_ours(args, ws, rank, local):
         ms = max_over_ranks(t0.elapsed_time(t1), ws)
         kern_ms = t0.elapsed_time(t1) / args.steps   # mean launch duration (one step = the path's launches)
         if adaptive:                                 # the blocks each packing ran (the decisions of this input)
-            dec = plan.adapt_block(S[(args.steps - 1) % n_buf], Q)
+            dec = plan.adapt_block(S[(args.steps - 1) % n_buf], Q, calib)
             fma = sum(core_fma(info, pk, [w for w, d in enumerate(dec) if d[0] == pk]) for pk in (FULL, SYM, ASYM2))
             rec_modes = {n_: sum(1 for d in dec if d[0] == pk) for n_, pk in (("full", FULL), ("sym", SYM),
                                                                                ("asym2", ASYM2))}
@@ -426,6 +429,7 @@ def run_ours(args, ws, rank, local):
             rec["fma_per_output"] = fma / (L_out * nsig)
         if adaptive:
             rec["blocks_per_packing"] = rec_modes
+            rec["calib_offset_db"] = calib
         if core == FFT:
             res, rc = plan.residual()
             rec["fft_residual_lsb"] = res

@@ -528,7 +528,11 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
         asm volatile("prefetch.global.L2 [%0];" ::"l"(src + i));
     }
   }
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // early_fill (host-checked: the preceding launch on this stream is not one that writes this
+  // input): the pipeline fill below only reads the input and the plan's taps and claims from
+  // this launch's own queue array, so it may overlap the preceding launch's tail; everything
+  // that writes global memory comes after griddepcontrol.wait.
+  if (!e.early_fill) asm volatile("griddepcontrol.wait;" ::: "memory");
   __syncthreads();
   if (e.dbg_timing && tid == 0) e.dbg_timing[kTimCyc + 4 * blockIdx.x + 2] = gtimer();   // t_start (stash)
   long long njobs = e.jobs_per_sig * e.nsig;
@@ -615,6 +619,7 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
     }
   }
   __syncthreads();
+  if (e.early_fill) asm volatile("griddepcontrol.wait;" ::: "memory");
   if (e.dbg_timing && tid == 0)
     e.dbg_timing[kTimCyc + 4 * blockIdx.x + 3] = gtimer() - e.dbg_timing[kTimCyc + 4 * blockIdx.x + 2];
 

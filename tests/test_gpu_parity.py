@@ -766,3 +766,48 @@ def test_snr_calibration_matches_oracle(sig, mode):
     assert abs(g_meas - meas) < 1e-9 and abs(g_model - model) < 1e-9 and abs(g_off - off) < 1e-9
     if sig == "uniform":
         assert abs(g_off) < 1.0
+
+
+@pytest.mark.parametrize("early", ["1", "0"])
+@pytest.mark.parametrize("packing", [O.ASYM2, O.FULL])
+def test_back_to_back_launches_early_fill(packing, early, monkeypatch):
+    """Consecutive tiled launches on one stream overlap (programmatic dependent launch): a
+    launch's pipeline fill may start before the preceding one finished unless it reads what that
+    one writes.  Chained (the second convolves the first's output, no sync in between): the
+    host check must hold the fill back; independent inputs: it may run early.  Both bit-exact
+    (full precision: the same bits as the unchained run)."""
+    monkeypatch.setenv("PC_EARLY_FILL", early)        # opt-in overlap of a launch's fill
+    L, N, W_block, Q = 60_000, 129, 2048, 63
+    rng = np.random.default_rng(17)
+    s, k = np.clip(rng.laplace(0, 0.3, L), -1, 1), rng.uniform(-1, 1, N)
+    Q = 0 if packing == O.FULL else Q
+    with pcb.Plan(L, N, W_block, O.CONV, PK[packing], Q, opts=pcb.opts_default(exec=2)) as p1, \
+            pcb.Plan(L + N - 1, N, W_block, O.CONV, PK[packing], Q, opts=pcb.opts_default(exec=2)) as p2:
+        p1.set_kernel(dev(k))
+        p2.set_kernel(dev(k))
+        s_d = dev(s)
+        r1 = torch.empty(L + N - 1, dtype=torch.float64, device=DEV)
+        r2 = torch.empty(L + 2 * (N - 1), dtype=torch.float64, device=DEV)
+        outs = []
+        for _ in range(3):                            # chained, repeatedly, no host sync
+            p1.execute(s_d, r1)
+            p2.execute(r1, r2)
+        torch.cuda.synchronize()
+        got1, got2 = r1.cpu().numpy(), r2.cpu().numpy()
+        s2 = np.clip(rng.laplace(0, 0.3, L), -1, 1)
+        s2_d = dev(s2)
+        ra, rb = torch.empty_like(r1), torch.empty_like(r1)
+        for _ in range(3):                            # independent inputs back to back
+            p1.execute(s_d, ra)
+            p1.execute(s2_d, rb)
+        torch.cuda.synchronize()
+        got_a, got_b = ra.cpu().numpy(), rb.cpu().numpy()
+    if packing == O.FULL:
+        assert np.array_equal(got_a, got1)
+        want2 = O.full_precision(O.full_precision(s, k), k)
+        assert np.max(np.abs(got2 - want2)) / np.max(np.abs(want2)) < 1e-12
+        return
+    ref1 = O.conv_pipeline(s, k, W_block, packing, Q).out
+    assert np.array_equal(got1, ref1) and np.array_equal(got_a, ref1)
+    assert np.array_equal(got2, O.conv_pipeline(ref1, k, W_block, packing, Q).out)
+    assert np.array_equal(got_b, O.conv_pipeline(s2, k, W_block, packing, Q).out)
