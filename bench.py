@@ -78,8 +78,9 @@ def parse():
     ap.add_argument("--opt", action="append", default=[], help="diagnostics: conv_opts.reserved[i]=v as i=v")
     ap.add_argument("--N", type=int, default=0, help="diagnostics: override the kernel length (cfg1/cfg2)")
     ap.add_argument("--exec", default="fused", choices=["fused", "perblock"], help="diagnostics: execution form")
-    ap.add_argument("--graph", type=int, default=-1,
-                    help="1: capture the K timed steps in one CUDA graph (default: on for cfg1, launch-bound)")
+    ap.add_argument("--graph", type=int, default=1,
+                    help="1 (default): the K timed steps are captured in one CUDA graph and replayed (every "
+                         "launch of every step runs; no host submission gaps); 0: launched back to back")
     return ap.parse_args()
 
 
@@ -367,7 +368,7 @@ def run_ours(args, ws, rank, local):
             step(i)
         torch.cuda.synchronize(dev)
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        use_graph = (args.graph == 1) or (args.graph == -1 and args.workload == "cfg1")
+        use_graph = args.graph == 1
         graph = None
         if use_graph:                                # K steps replayed as one graph (no host launch gaps)
             gs = torch.cuda.Stream(dev)

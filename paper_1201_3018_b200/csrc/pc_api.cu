@@ -81,6 +81,7 @@ struct conv_plan {
   // persistent kernel job counter (monotonic; base tracked on the host)
   unsigned* d_counter = nullptr;        // tiled kernel: two arrays of per-SM job queues + done counter (zero between launches)
   int ctr_flip = 0;                     // the array the next non-adaptive tiled launch uses
+  int cand_ok = 0;                      // adaptive: d_cand holds this kernel's candidate table
   double* d_pre = nullptr;              // prepacked stage images + per-job inverse scales (pc_prepack_kernel)
   long long pre_cap = 0;                // doubles allocated at d_pre
   // FFT core
@@ -859,6 +860,7 @@ int conv_plan_set_kernel(conv_plan* p, const double* k_dev, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   p->kernel_set = 0;
   p->adapt_ready = 0;
+  p->cand_ok = 0;
   int rc;
   if (p->packing == PC_PACK_ADAPTIVE) {
     const int cands[2] = {PC_PACK_SYM, PC_PACK_ASYM2};
@@ -1240,8 +1242,14 @@ int conv_adapt_block(conv_plan* p, const double* s, double snr_floor_db, double 
   }
   // predicted_db >= floor  <=>  snr_lin >= 10^((floor - offset)/10)
   const double thr = std::pow(10.0, (snr_floor_db - calib_offset_db) / 10.0);
-  e = cudaMemcpyAsync(p->d_cand, hc, sizeof(hc), cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess) e = pc::launch_block_stats(make_geo(p), s, p->d_sigma, p->d_peak, st);
+  // the candidate table changes only with the kernel: uploaded once (synchronously), so the
+  // call is stream-ordered device work only and can be captured in a CUDA graph
+  if (!p->cand_ok) {
+    if (cudaStreamSynchronize(st) != cudaSuccess || cudaMemcpy(p->d_cand, hc, sizeof(hc), cudaMemcpyHostToDevice) != cudaSuccess)
+      return PC_E_CUDA;
+    p->cand_ok = 1;
+  }
+  e = pc::launch_block_stats(make_geo(p), s, p->d_sigma, p->d_peak, st);
   if (e == cudaSuccess)
     e = pc::launch_adapt_decide(P, p->d_sigma, p->d_peak, p->k_sigma, p->k_peak, p->d_cand, p->d_cand + 4, nc, thr,
                                 p->d_dec_pack, p->d_dec_q, p->d_dec_snr, st);

@@ -811,3 +811,37 @@ def test_back_to_back_launches_early_fill(packing, early, monkeypatch):
     assert np.array_equal(got1, ref1) and np.array_equal(got_a, ref1)
     assert np.array_equal(got2, O.conv_pipeline(ref1, k, W_block, packing, Q).out)
     assert np.array_equal(got_b, O.conv_pipeline(s2, k, W_block, packing, Q).out)
+
+
+def test_adaptive_step_graph_replay():
+    """The adaptive step (a8 decisions + one tiled launch per packing) is stream-ordered device
+    work only (the candidate table is uploaded once per kernel), so a CUDA graph of it replays
+    with the eager result, for inputs whose decisions differ between replays."""
+    s1, k = WL.cfg5(seed=1, L=1 << 17, N=1024)
+    s2, _ = WL.cfg5(seed=2, L=1 << 17, N=1024)
+    W_block, floor = 4096, 40.0
+    with pcb.Plan(len(s1), len(k), W_block, pcb.MODE_CONV, pcb.PACK_ADAPTIVE, 0, rmax_rule=pcb.RMAX_L1) as p:
+        p.set_kernel(dev(k))
+        L_out = p.info()["L_out"]
+        S = dev(s1)
+        want = []
+        for x in (s1, s2):
+            r = torch.empty(L_out, dtype=torch.float64, device=DEV)
+            p.adapt_block(dev(x), floor)
+            p.execute(dev(x), r)
+            torch.cuda.synchronize()
+            want.append(r.cpu().numpy())
+        R = torch.empty(L_out, dtype=torch.float64, device=DEV)
+        gs = torch.cuda.Stream(DEV)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(gs):
+            with torch.cuda.graph(graph, stream=gs):
+                pcb.adapt_block(p.h, S, floor, 0.0, None, gs.cuda_stream)
+                pcb.execute(p.h, S, R, gs.cuda_stream)
+        for x, w in ((s1, want[0]), (s2, want[1]), (s1, want[0])):
+            S.copy_(dev(x))
+            R.fill_(float("nan"))
+            torch.cuda.synchronize()
+            graph.replay()
+            torch.cuda.synchronize()
+            assert np.array_equal(R.cpu().numpy(), w)
