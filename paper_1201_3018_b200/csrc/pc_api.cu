@@ -937,7 +937,10 @@ int conv_execute_host(conv_plan* p, const double* s_host, double* r_host, void* 
   if (!p->d_out && cudaMalloc(&p->d_out, sizeof(double) * L_out) != cudaSuccess) return PC_E_CUDA;
   // Adaptive plans (decisions belong to one device input) and small plans: one pass.
   // Chunk weights: small first and last ranges shorten the pipeline ramp (the first H2D and
-  // the last D2H are not overlapped).
+  // the last D2H are not overlapped).  (Zero-copy was measured and dropped: the tiled kernel
+  // reading pinned input over PCIe took 2.1 ms at cfg2 -- the peak and packing passes read each
+  // sample twice over the link -- and storing outputs straight to pinned memory 1.07-1.36 ms,
+  // against 1.04 ms for this copy pipeline; the link's duplex floor is 0.71 ms.)
   static const int kW[9] = {1, 2, 4, 4, 4, 4, 4, 2, 1};
   int nchunk = (p->packing == PC_PACK_ADAPTIVE || p->P < 128) ? 1 : 9;
   long long cum[33] = {0};
