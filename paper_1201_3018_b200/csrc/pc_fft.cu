@@ -323,7 +323,10 @@ __global__ void __launch_bounds__(N / 16) pc_fft_spectrum(const double* __restri
 
 // ------------------------------------------------------------------ the FFT-core conv kernel
 template <int PACK, int N>
-__global__ void __launch_bounds__(N / 16, (N <= 4096 ? 2 : 1)) pc_fft_conv_kernel(Geo g, Exec e, FftArgs f) {
+#ifndef PC_FFT_MINB
+#define PC_FFT_MINB 2   // CTAs per SM the N <= 4096 transform is compiled for (register cap)
+#endif
+__global__ void __launch_bounds__(N / 16, (N <= 4096 ? PC_FFT_MINB : 1)) pc_fft_conv_kernel(Geo g, Exec e, FftArgs f) {
   extern __shared__ __align__(16) double2 sm[];
   __shared__ double red[32];
   const ModeP& mp = e.mp[PACK];

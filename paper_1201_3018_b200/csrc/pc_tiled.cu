@@ -12,9 +12,13 @@
 //                   packing (Eq. (4) / Eq. (7)) of the words one (tile, chunk) needs into a
 //                   stage of the ring; non-resident tap chunks arrive by TMA bulk copy on the
 //                   stage's mbarrier
-//   consumer warps  a5: the FP64 core (conv_chunk_padded, accumulators live across chunks)
-//                   on one 32-group part of a job; a6-a7: unpacking, inverse companding and
-//                   placement through per-warp staging rows, coalesced stores
+//   consumer warps  a5: the core on one part of a job (accumulators live across chunks):
+//                   MMA = 1, a Toeplitz product on the FP64 tensor cores (conv_chunk_mma; at
+//                   most PC_CORE_SLOTS = 2 warps per SMSP in it at once, claim-ordered ticket),
+//                   the part a balanced share of the tile's 8-group m-tiles; MMA = 0, the
+//                   register-tiled FMA loop (conv_chunk_padded) on 32 groups of T outputs;
+//                   a6-a7: unpacking, inverse companding and placement through per-warp
+//                   staging rows, coalesced stores
 //
 // Stages are handed over with mbarriers (full: producer -> consumers, + TMA bytes; empty:
 // the job's part warps -> producers) and stamped with their sequence number.  Warp parts are
