@@ -575,6 +575,35 @@ def snr_calibration(s, k, W_block, Q=8, packing=ASYM2, mode=CONV, eps_rule=EPS_P
     return measured - model, measured, model
 
 
+def validate_backend(N, r_max, trials=100, seed=0, backend="fft"):
+    """Backend validation behind the u_sys guard (the paper's u_sys = 3.1193e-11 is
+    a machine-precision measurement): convolve `trials` randomized worst-case packed
+    operands -- asymmetric M = 2 words of full-magnitude digits +-S_q at the dyadic eps of
+    R_max = r_max (Eq. (7) Horner order), kernel digits +-K_q with N S_q K_q ~ r_max -- on the
+    backend and on the direct (exact, np.convolve) one, and return (max |deviation|,
+    u_sys = 4 max |deviation|) ("measure max fft deviation on integer inputs, scale by
+    safety factor 4").  backend: "fft" (NumPy's real FFT, the Tier-2 FFT core of the CPU spec)
+    or "direct" (self-comparison: 0)."""
+    rng = np.random.default_rng(seed)
+    q = max(1, int(math.isqrt(max(1, r_max // max(1, N)))))         # S_q = K_q with N S_q K_q <= r_max
+    eps = 1.0 / (1 << (int(2 * r_max).bit_length()))              # reading C4: 2^-b, b = ceil(log2(2R+1))
+    n_sig = 4 * N
+    dev = 0.0
+    for _ in range(trials):
+        d0 = q * rng.choice([-1.0, 1.0], n_sig)
+        d1 = q * rng.choice([-1.0, 1.0], n_sig)
+        x = d0 + eps * d1                                         # Eq. (7), M = 2
+        k = q * rng.choice([-1.0, 1.0], N)
+        exact = np.convolve(x, k)
+        if backend == "direct":
+            got = np.convolve(x, k)
+        else:
+            n = 1 << int(n_sig + N - 1 - 1).bit_length()
+            got = np.fft.irfft(np.fft.rfft(x, n) * np.fft.rfft(k, n), n)[:n_sig + N - 1]
+        dev = max(dev, float(np.max(np.abs(got - exact))))
+    return dev, 4.0 * dev
+
+
 # ----------------------------------------------------------------------------- Table 1
 
 def flop_count(packing, domain, N):

@@ -845,3 +845,27 @@ def test_adaptive_step_graph_replay():
             graph.replay()
             torch.cuda.synchronize()
             assert np.array_equal(R.cpu().numpy(), w)
+
+
+@pytest.mark.parametrize("packing,Q", [(O.ASYM2, 127), (O.ASYM2, 63), (O.SYM, 5)])   # R within each bound
+def test_fft_core_backend_validation_worst_case(packing, Q):
+    """Backend validation of the GPU FFT core (the u_sys guard's purpose, P:103,
+    P:153): worst-case packed operands -- every sample and tap at full magnitude (+-1, so
+    every companded digit is +-S_q / +-K_q) -- over 100 random sign patterns in 4 launches at
+    the cfg3 geometry; the core's last-digit deviation (the residual monitor) stays below
+    0.5 LSB, so the integers equal the exact direct core's bit for bit, and u_sys calibrated
+    as 4 x the measured absolute deviation is reported next to the paper's value."""
+    rng = np.random.default_rng(Q)
+    L, N, W_block = 1 << 17, 4096, 16384
+    worst = 0.0
+    for _ in range(4):
+        s = rng.choice([-1.0, 1.0], L)
+        k = rng.choice([-1.0, 1.0], N)
+        got, res, rc, info = fft_run(s, k, W_block, packing, Q)
+        ref = gpu_run(s, k, W_block, packing, Q, rmax_rule=O.RMAX_L1, debug=False)["r"]
+        assert np.array_equal(got, ref)
+        assert res < 0.5
+        worst = max(worst, res)
+    u_sys = 4.0 * worst * info["eps"]              # absolute deviation of a packed core output
+    print(f"FFT core {packing} Q={Q}: max last-digit residual {worst:.3g} LSB, calibrated u_sys {u_sys:.3g} "
+          f"(paper {O.U_SYS_PAPER:.4g})")

@@ -440,3 +440,18 @@ def test_snr_calibration_single_point():
     _, _, model16 = O.snr_calibration(s, k, 8192, Q=16, packing=O.ASYM2, rmax_rule=O.RMAX_L1)
     assert abs((model16 + off) - meas16) < 0.5
     assert 26.0 < meas16 < 28.5                      # the paper's 27.5 dB regime
+
+
+def test_validate_backend_u_sys():
+    """S:248-256 examples and the guard's purpose: the direct backend compared with itself
+    deviates by exactly 0; the FFT backend at N = 3, r_max = 3 stays orders below the paper's
+    u_sys (3.1193e-11); its deviation grows with r_max at fixed N; and at N = 801,
+    r_max = 51,200 (the §IV.A kernel length) the calibrated u_sys = 4 x deviation is far below
+    half the last packed digit (eps = 2^-17 here), so floor-based unpacking stays exact."""
+    assert O.validate_backend(801, 51200, trials=5, backend="direct") == (0.0, 0.0)
+    d_small, u_small = O.validate_backend(3, 3, trials=100)
+    assert d_small < 1e-13 and u_small == 4 * d_small
+    d_big, u_big = O.validate_backend(801, 51200, trials=20)
+    d_huge, _ = O.validate_backend(801, 12_800_000, trials=20)
+    assert d_small < d_big < d_huge
+    assert u_big < 0.5 * 2.0 ** -17
