@@ -480,7 +480,7 @@ def run_ours(args, ws, rank, local):
                 wr = recd["dram__bytes_write.sum"].split()
                 mult = {"Mbyte": 1e6, "Kbyte": 1e3, "Gbyte": 1e9, "byte": 1.0}
                 traffic = float(rd[0]) * mult[rd[1]] + float(wr[0]) * mult[wr[1]]
-                traffic_src = "profiles/r01_ncu_cfg2_asym2.json (ncu --set full, one launch)"
+                traffic_src = f"profiles/{os.path.basename(prof)} (ncu --set full, one launch)"
     if "fp64_tflops" in h:
         # the DMMA-core kernel is bound by the FP64 tensor pipe (its own measured peak), the FMA core
         # by the FP64 FMA pipe; adaptive plans: asym2/full launches run DMMA, the symmetric one FMA
