@@ -36,6 +36,9 @@
 #ifndef PC_NO_STEAL
 #define PC_NO_STEAL 0     // diagnostics: 1 = no work stealing between SM queues
 #endif
+#ifndef PC_PROD_YIELD
+#define PC_PROD_YIELD 0   // 1: one DMMA core slot on an SMSP while its producer packs (measured: asym2 +1%, full +14%)
+#endif
 #ifndef PC_CORE_SLOTS
 #define PC_CORE_SLOTS 2   // DMMA core: warps per SM sub-partition allowed in the core at once
 #endif
@@ -52,6 +55,7 @@ struct TSmem {
   int smsp_ctr[4];                  // consumer warp-job claim counters, one per SM sub-partition
   int core_serve[4];                // DMMA core: the claim whose warp may run its core on each SMSP
   int mseq_hi;                      // 1 + the highest job sequence any consumer warp has claimed a part of
+  int prod_busy[4];                 // producer warp of SMSP s is companding/packing (DMMA core: one core slot)
   long long turn;                   // next job sequence to claim (claims happen in sequence order)
   long long fjob[16];               // pipeline fill: jobs of sequences 0 .. nf-1
   double fcs[16], finv[16];         // their c_s and (c_s c_k)^-1
@@ -504,7 +508,7 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
       mbar_init(&ps->empty[i], npart);
       ps->seq[i] = -1;
     }
-    for (int i = 0; i < 4; ++i) ps->smsp_ctr[i] = ps->core_serve[i] = 0;
+    for (int i = 0; i < 4; ++i) ps->smsp_ctr[i] = ps->core_serve[i] = ps->prod_busy[i] = 0;
     ps->mseq_hi = 0;
     ps->turn = 1;
     ps->m_end = -1;
@@ -695,6 +699,8 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
       Blk b;
       const double* gsrc = nullptr;
       int n_valid = 0;
+      if (job >= 0 && MMA && PC_PROD_YIELD && lane == 0 && !e.pre_win)
+        *reinterpret_cast<volatile int*>(&ps->prod_busy[pw & 3]) = 1;
       if (job >= 0) {
         job_block(job, jp, b, gsrc, n_valid);
         const long long blk_id = jp.sig * g.P + jp.w;
@@ -725,6 +731,7 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
         __syncwarp();
         publish(n, st, c, job, inv_w, lane);
       }
+      if (MMA && PC_PROD_YIELD && lane == 0) *reinterpret_cast<volatile int*>(&ps->prod_busy[pw & 3]) = 0;
       if (prec) {
         prec[3] = gtimer();
         // m | (claimed -> peak done) << 16 | (peak done -> slot free) << 40, in 16-ns units
@@ -833,8 +840,13 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
       // slower loads and FP64 ops with three DMMA warps per SMSP, ~1.1x with one
       // (tools/dmma_interference.cu).
       if (lane == 0)
-        for (int sp = 0; *reinterpret_cast<volatile int*>(&ps->core_serve[smsp]) + PC_CORE_SLOTS <= cl;)
+        // while the SMSP's producer warp packs, one core slot: a second queued DMMA warp would
+        // slow its loads and FP64 ops 3x (tools/dmma_interference.cu)
+        for (int sp = 0;
+             *reinterpret_cast<volatile int*>(&ps->core_serve[smsp]) +
+                 (PC_PROD_YIELD && *reinterpret_cast<volatile int*>(&ps->prod_busy[smsp]) ? 1 : PC_CORE_SLOTS) <= cl;)
           spin_wd(sp, 64, 8, cl, smsp);
+      if (wrec) wrec[0] |= ((gtimer() - wrec[1]) >> 4) << 32;   // diagnostics: token wait (16 ns units)
       __syncwarp();
     }
     for (int c = 0; c < nch; ++c, ++n) {

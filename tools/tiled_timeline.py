@@ -70,7 +70,8 @@ for name, (pk, Q, rm) in points.items():
                 prev = tr[i, j]
     W = a[KTW:KTP].reshape(148, 16, 16, 4)[:g]
     Pr = a[KTP:KTP + 148 * 4 * 16 * 4].reshape(148, 4, 16, 4)[:g]
-    # per SMSP: how many warps are in their core phase over time (0.25 us bins)
+    # per SMSP: how many warps are in their core phase over time (0.25 us bins); DMMA core: from
+    # the core-token acquisition (wait recorded in the high word of the sequence) to core done
     tb = np.arange(0, T_end + 0.25, 0.25)
     act = np.zeros((g, 4, len(tb)))
     for cc in range(g):
@@ -79,6 +80,7 @@ for name, (pk, Q, rm) in points.items():
                 if W[cc, w, j, 1] == 0 or W[cc, w, j, 2] == 0:
                     continue
                 a0, b0_ = (W[cc, w, j, 1] - t0) / 1e3, (W[cc, w, j, 2] - t0) / 1e3
+                a0 += ((int(W[cc, w, j, 0]) >> 32) * 16) / 1e3
                 act[cc, (w + 4) % 4, (tb >= a0) & (tb < b0_)] += 1
     cta_end = {cc: (r[cc, 2] - t0) / 1e3 for cc in range(g)}
     live = np.array([[tb < cta_end[cc]] * 4 for cc in range(g)]).reshape(g, 4, len(tb))
@@ -102,9 +104,12 @@ for name, (pk, Q, rm) in points.items():
             return [v & 0xffff, w, round((Pr[c, w, j, 1] - t0) / 1e3, 1), round(tc, 1), round(tp, 1),
                     round(tp + (v >> 40) * 16 / 1e3, 1), round((Pr[c, w, j, 3] - t0) / 1e3, 1)]
         prod = [prow(w, j) for w in range(4) for j in range(15) if Pr[c, w, j, 3]]
-        cons = [[w, int(W[c, w, j, 0]), round((W[c, w, j, 1] - t0) / 1e3, 1), round((W[c, w, j, 2] - t0) / 1e3, 1),
-                 round((W[c, w, j, 3] - t0) / 1e3, 1)] for w in range(16) for j in range(16) if W[c, w, j, 1]]
-        return {"produced[mseq,warp,t_start,t_claimed,t_peak,t_slot,t_pub]": sorted(prod), "consumed[warp,mseq,t_ready,t_core,t_stored]": sorted(cons, key=lambda x: x[2])}
+        cons = [[w, int(W[c, w, j, 0]) & 0xffffffff, round((W[c, w, j, 1] - t0) / 1e3, 1),
+                 round((W[c, w, j, 1] - t0) / 1e3 + ((int(W[c, w, j, 0]) >> 32) * 16) / 1e3, 1),
+                 round((W[c, w, j, 2] - t0) / 1e3, 1), round((W[c, w, j, 3] - t0) / 1e3, 1)]
+                for w in range(16) for j in range(16) if W[c, w, j, 1]]
+        return {"produced[mseq,warp,t_start,t_claimed,t_peak,t_slot,t_pub]": sorted(prod),
+                "consumed[warp,mseq,t_ready,t_in_core,t_core_done,t_stored]": sorted(cons, key=lambda x: x[2])}
     fill_phases = (Pr[:, :, 15, :3].astype(float) - r[:, 1][:, None, None]) / 1e3   # claimed, peak, packed (us)
     fill_stats = {k: round(float(np.median(fill_phases[:, :, i])), 2) for i, k in enumerate(["claimed", "peak", "packed"])}
     crit = int(np.argmax(r[:, 2]))                  # the CTA that ends last
