@@ -536,7 +536,6 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
     e.sm_ctr = p->d_counter + (p->ctr_flip ? pc::kCtrDone + 1 : 0);   // alternate: see early_fill
     p->ctr_flip ^= 1;
     e.dbg_timing = timing;
-    e.dbg_skip_pack = p->opts.reserved[8] == 77;   // timing experiment (results invalid)
     e.lookahead = p->opts.reserved[7] < 0 ? -p->opts.reserved[7] : 0;   // diagnostics
     e.xc_val = xc_val;
     e.xc_lag = xc_lag;

@@ -95,7 +95,6 @@ struct Exec {
   const double* kr_sig;
   long long kr_stride;
   const double* scal_sig;
-  int dbg_skip_pack;    // experiment only: producers publish without companding/packing (wrong results)
   // prepacked windows (pc_prepack_kernel, single-chunk plans): job j's stage image (rows_s rows of
   // pitch T + 4) at pre_win + j * pre_stride and its (c_s c_k)^-1 at pre_inv[j]; the tiled
   // kernel's producers then only move them into the ring with one bulk copy each

@@ -704,7 +704,7 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
       if (job >= 0) {
         job_block(job, jp, b, gsrc, n_valid);
         const long long blk_id = jp.sig * g.P + jp.w;
-        if (blk_id != cur_blk_w && !e.dbg_skip_pack && !e.pre_win) {
+        if (blk_id != cur_blk_w && !e.pre_win) {
           cur_blk_w = blk_id;
           c_s_w = warp_cs<PACK>(mp, gsrc, n_valid, lane);   // a2/a3 (Eq. (2))
           inv_w = dequant_scale(c_s_w, e.scal_sig ? e.scal_sig[3 * jp.sig + 1] : mp.c_k);   // Eq. (16)
@@ -725,7 +725,7 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
           mbar_wait_wd(&ps->empty[st], (uint32_t)(((n / NS) & 1) ^ 1), 1, n, st);
         }
         if (prec && c == 0) t_sl = gtimer();
-        if (job >= 0 && !(prepacked && c == 0) && !e.dbg_skip_pack && !e.pre_win)
+        if (job >= 0 && !(prepacked && c == 0) && !e.pre_win)
           pack_window<PACK, T, 2, PT>(g, b, mp, gsrc, n_valid, c_s_w, jp.t * G * T - front * T + c * KC, rows_s,
                                stg + (size_t)st * stage_words, lane, 32);
         __syncwarp();
