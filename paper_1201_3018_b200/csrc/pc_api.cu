@@ -553,8 +553,9 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
     // a2-a4 ahead of the DMMA-core launch (single-chunk packed plans, reserved[8] = 2): measured
     // slower than the fused producers at cfg2 (the separate pass costs ~26 us, the persistent
     // kernel's tail does not shrink), so off by default
-    if (ts.mma && ts.nchunks == 1 && p->packing != PC_PACK_FULL && p->opts.reserved[8] == 2) {
-      const long long stride = ((long long)(ts.T + 4) * ts.rows_s + 1) & ~1LL;   // stage_x of pc_tiled_kernel
+    if (ts.nchunks == 1 && p->packing != PC_PACK_FULL && p->opts.reserved[8] == 2 &&
+        (long long)p->W_block * 8 <= 200 * 1024) {
+      const long long stride = ((long long)(ts.T + (ts.mma ? 4 : 1)) * ts.rows_s + 1) & ~1LL;   // stage_x of pc_tiled_kernel
       const long long need = njobs * stride + njobs;
       if (need > p->pre_cap) {
         cudaFree(p->d_pre);
@@ -566,7 +567,7 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
       e.pre_win = p->d_pre;
       e.pre_stride = stride;
       e.pre_inv = p->d_pre + njobs * stride;
-      if (pc::launch_prepack(p->packing, ts.T, make_geo(p), e, njobs, st) != cudaSuccess) return PC_E_CUDA;
+      if (pc::launch_prepack(p->packing, ts.T, ts.mma, make_geo(p), e, njobs, st) != cudaSuccess) return PC_E_CUDA;
     }
     // every address this launch may read as input / write as output (rows sig < n_sig)
     const uintptr_t in_lo = (uintptr_t)(s - s_off), in_hi = (uintptr_t)(s - s_off + (n_sig - 1) * s_stride + p->L);

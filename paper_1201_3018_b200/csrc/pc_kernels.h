@@ -121,7 +121,7 @@ cudaError_t launch_fused(int packing, const Geo& g, const Exec& e, long long n_j
                          cudaStream_t st);
 // a2-a4 for every job of a tiled launch, ahead of it (pc_tiled.cu): block peak, c_s, packing
 // into the stage image the DMMA core reads; one CTA per job.
-cudaError_t launch_prepack(int packing, int T, const Geo& g, const Exec& e, long long n_jobs, cudaStream_t st);
+cudaError_t launch_prepack(int packing, int T, int mma, const Geo& g, const Exec& e, long long n_jobs, cudaStream_t st);
 // Tiled persistent warp-specialized kernel (pc_tiled.cu): grid = SMs x resident CTAs.
 // mma = 1: the core runs on the FP64 tensor cores (T = 16 only; stage pitch 20, taps with 16
 // zeros before and after -- every tap buffer is allocated with 16 leading zeros).

@@ -132,13 +132,15 @@ __device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsig
 // a4 for one stage: core words [cw0, cw0 + rows_s*T) of block b into the padded row-major
 // window xs[(i / T) * PT + i % T] (pitch PT = T + 1 for the FMA core, T + 4 for the DMMA core).  Word-major over the producer threads (coalesced
 // loads), UW words per thread with every sample load issued before any use.
-template <int PACK, int T, int UWF = 1, int PT = T + 1>
+template <int PACK, int T, int UWF = 1, int PT = T + 1, bool SRC_SMEM = false>
 __device__ __forceinline__ void pack_window(const Geo& g, const Blk& b, const ModeP& mp, const double* gsrc,
                                             int n_valid, double c_s, int cw0, int rows_s, double* xs, int ptid,
                                             int nprod) {
   constexpr int UW = UWF * ((PACK == PACK_ASYM3) ? 4 : 8);   // words per thread in flight
   const int words = rows_s * T;
-  auto sample = [&](int i) -> double { return (i < 0 || i >= n_valid) ? 0.0 : __ldg(gsrc + i); };
+  auto sample = [&](int i) -> double {
+    return (i < 0 || i >= n_valid) ? 0.0 : (SRC_SMEM ? gsrc[i] : __ldg(gsrc + i));
+  };
   const bool alu = mp.alu_pack;                              // warp-uniform (per plan)
   for (int i0 = ptid; i0 < words; i0 += UW * nprod) {
     double v[UW];
@@ -1057,48 +1059,100 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
 }
 
 // ------------------------------------------------------------------ prepack (a2-a4 ahead)
-// One CTA per job: the block's peak and c_s (Eq. (2)), then the job's stage image -- exactly
-// the words pack_window writes into a ring stage (pitch T + 4) -- into HBM (L2-resident for the
-// tiled launch that follows), and (c_s c_k)^-1 (Eq. (16)).  Moving a2-a4 out of the persistent
-// kernel keeps its producer warps at one bulk copy per job: on a DMMA-saturated SMSP every
-// other warp's instruction issue slows 3-15x (tools/dmma_interference.cu).
-template <int PACK, int T>
-__global__ void __launch_bounds__(256) pc_prepack_kernel(Geo g, Exec e) {
-  __shared__ double red[8];
-  constexpr int PT = T + 4;
+// One CTA per job: the block's W_block samples are loaded once into shared memory (coalesced,
+// every load in flight at once) while the block peak is reduced from them (integer max of |x|
+// bits), c_s = Q / peak (Eq. (2)); the job's stage image -- exactly the words pack_window writes
+// into a ring stage, pitch PT -- is then packed from shared memory into HBM (L2-resident for the
+// tiled launch that follows), with (c_s c_k)^-1 (Eq. (16)).  The tiled kernel's producer warps
+// then move each image with one bulk copy.
+constexpr int kPrepackThreads = 512;
+template <int PACK, int T, int PT>
+__global__ void __launch_bounds__(kPrepackThreads) pc_prepack_kernel(Geo g, Exec e) {
+  extern __shared__ __align__(16) double raw[];
+  __shared__ unsigned long long ired[kPrepackThreads / 32];
   const ModeP& mp = e.mp[PACK];
   const long long job = blockIdx.x;
+  const int tid = threadIdx.x;
   const JobPos jp = job_pos(e, job);
   const Blk b = block_info<PACK>(g, mp.K, jp.w);
   const double* gsrc = e.s + jp.sig * e.s_stride + (b.g0 - e.s_off);
   const long long avail = g.L - b.g0;
   const int n_valid = (int)(avail < 0 ? 0 : (avail > g.W_block ? g.W_block : avail));
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  const double cs = block_cs<PACK>(mp, gsrc, n_valid, red, threadIdx.x, 256, 1);
+  constexpr int U = 8;
+  unsigned long long m = 0ull;
+  for (int i0 = tid; i0 < n_valid; i0 += U * kPrepackThreads) {
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * kPrepackThreads;
+      v[u] = (i < n_valid) ? __ldg(gsrc + i) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * kPrepackThreads;
+      if (i < n_valid) raw[i] = v[u];
+      m = umax64(m, abs_bits(v[u]));
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) m = umax64(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((tid & 31) == 0) ired[tid >> 5] = m;
+  __syncthreads();
+  unsigned long long pm = 0ull;
+#pragma unroll
+  for (int w = 0; w < kPrepackThreads / 32; ++w) pm = umax64(pm, ired[w]);
+  const double peak = __longlong_as_double((long long)pm);
+  const double cs = (PACK == PACK_FULL || peak == 0.0) ? 1.0 : mp.Q / peak;   // Eq. (2)
   const int front = (PACK == PACK_SYM) ? 1 : 0;
   double* xs = const_cast<double*>(e.pre_win) + job * e.pre_stride;
-  pack_window<PACK, T, 1, PT>(g, b, mp, gsrc, n_valid, cs, jp.t * e.G * T - front * T, e.rows_s, xs, threadIdx.x, 256);
-  if (threadIdx.x == 0)
+  pack_window<PACK, T, 1, PT, true>(g, b, mp, raw, n_valid, cs, jp.t * e.G * T - front * T, e.rows_s, xs, tid,
+                                    kPrepackThreads);
+  if (tid == 0)
     const_cast<double*>(e.pre_inv)[job] = dequant_scale(cs, e.scal_sig ? e.scal_sig[3 * jp.sig + 1] : mp.c_k);
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-cudaError_t launch_prepack(int packing, int T, const Geo& g, const Exec& e, long long n_jobs, cudaStream_t st) {
-  if (n_jobs <= 0) return cudaSuccess;
-  if (T != 16) return cudaErrorInvalidValue;
+template <int PACK, int T, int PT>
+static cudaError_t launch_prepack_t(const Geo& g, const Exec& e, long long n_jobs, cudaStream_t st) {
+  auto kfn = pc_prepack_kernel<PACK, T, PT>;
+  const size_t smem = (size_t)g.W_block * sizeof(double);
+  static size_t c_smem = 0;
+  if (smem > c_smem) {
+    cudaError_t err = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err != cudaSuccess) return err;
+    c_smem = smem;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)n_jobs);
-  cfg.blockDim = dim3(256);
+  cfg.blockDim = dim3(kPrepackThreads);
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kfn, g, e);
+}
+
+template <int T, int PT>
+static cudaError_t launch_prepack_T(int packing, const Geo& g, const Exec& e, long long n_jobs, cudaStream_t st) {
   switch (packing) {
-    case PACK_SYM: return cudaLaunchKernelEx(&cfg, pc_prepack_kernel<PACK_SYM, 16>, g, e);
-    case PACK_ASYM2: return cudaLaunchKernelEx(&cfg, pc_prepack_kernel<PACK_ASYM2, 16>, g, e);
-    case PACK_ASYM3: return cudaLaunchKernelEx(&cfg, pc_prepack_kernel<PACK_ASYM3, 16>, g, e);
+    case PACK_SYM: return launch_prepack_t<PACK_SYM, T, PT>(g, e, n_jobs, st);
+    case PACK_ASYM2: return launch_prepack_t<PACK_ASYM2, T, PT>(g, e, n_jobs, st);
+    case PACK_ASYM3: return launch_prepack_t<PACK_ASYM3, T, PT>(g, e, n_jobs, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_prepack(int packing, int T, int mma, const Geo& g, const Exec& e, long long n_jobs, cudaStream_t st) {
+  if (n_jobs <= 0) return cudaSuccess;
+  if ((size_t)g.W_block * sizeof(double) > 200 * 1024) return cudaErrorInvalidValue;   // raw block in smem
+  if (mma) return T == 16 ? launch_prepack_T<16, 20>(packing, g, e, n_jobs, st) : cudaErrorInvalidValue;
+  switch (T) {
+    case 12: return launch_prepack_T<12, 13>(packing, g, e, n_jobs, st);
+    case 14: return launch_prepack_T<14, 15>(packing, g, e, n_jobs, st);
+    case 16: return launch_prepack_T<16, 17>(packing, g, e, n_jobs, st);
   }
   return cudaErrorInvalidValue;
 }
