@@ -573,6 +573,7 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
     const uintptr_t in_lo = (uintptr_t)(s - s_off), in_hi = (uintptr_t)(s - s_off + (n_sig - 1) * s_stride + p->L);
     const uintptr_t out_lo = (uintptr_t)(r - r_off - p->N), out_hi = (uintptr_t)(r - r_off + (n_sig - 1) * r_stride + p->L + 2 * p->N);
     e.early_fill = !timing && !e.pre_win && early_fill_ok(p->device, st, in_lo, in_hi);
+    e.early_claim = 1;                                 // claims touch only this launch's queue array
     int grid = 0;
     cudaError_t err = pc::launch_tiled(p->packing, ts.T, ts.mma, make_geo(p), e, njobs, ts.threads, ts.smem, st, &grid);
     record_out(p->device, st, out_lo, out_hi);

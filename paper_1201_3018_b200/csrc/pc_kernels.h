@@ -73,6 +73,7 @@ struct Exec {
   int nstages;                  // stage ring slots (2 .. kTiledMaxStages)
   int lookahead;                // > 0: claim job sequence m only once consumers have claimed parts of m - lookahead
   int early_fill;               // 1: the pipeline fill runs before griddepcontrol.wait (see pc_tiled_kernel)
+  int early_claim;              // 1: the fill's job claims run before griddepcontrol.wait (alternating queue arrays)
   int taps_resident;            // 1: all K_pad taps stay in shared memory (nchunks == 1)
   int rows_s;                   // rows of a stage's padded word window
   long long tiles0, tiles1;     // tiles of block 0 / of every other block

@@ -518,8 +518,10 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
     mbar_arrive_expect_tx(&ps->bar_taps, tb);
     if (tb) bulk_g2s(kr_res - TH, mp.kr - TH, tb, &ps->bar_taps);   // the tap buffers carry 16 leading zeros
   }
-  // programmatic dependent launch: only plan-owned, read-only taps are touched above
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // Programmatic dependent launch: the next launch may start once every CTA of this one has
+  // passed griddepcontrol.wait (the trigger follows each wait below), i.e. once the launch before
+  // this one has completed -- so the next launch's queue array (the one the launch before used,
+  // reset by its last CTA) is free when it claims before its own wait.
   if (!e.blk_list) {
     // While the previous launch drains: L2 prefetch of the input of the (likely) first four
     // jobs of this CTA's queue.  A hint only -- L2 is coherent, so even if the preceding
@@ -542,7 +544,11 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
   // input): the pipeline fill below only reads the input and the plan's taps and claims from
   // this launch's own queue array, so it may overlap the preceding launch's tail; everything
   // that writes global memory comes after griddepcontrol.wait.
-  if (!e.early_fill) asm volatile("griddepcontrol.wait;" ::: "memory");
+  auto dep_wait = [&]() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  };
+  if (!e.early_fill && !e.early_claim) dep_wait();
   __syncthreads();
   if (e.dbg_timing && tid == 0) e.dbg_timing[kTimCyc + 4 * blockIdx.x + 2] = gtimer();   // t_start (stash)
   long long njobs = e.jobs_per_sig * e.nsig;
@@ -601,6 +607,7 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
     ps->turn = nf;
   }
   __syncthreads();
+  if (e.early_claim && !e.early_fill) dep_wait();   // the fill reads the input: after the wait
   {
     constexpr int GW = (kTiledProdWarps + NCW) / kTiledFillJobs;   // warps per fill group
     const int gq = warp_ / GW, gtid = tid - gq * GW * 32;
@@ -629,7 +636,7 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
     }
   }
   __syncthreads();
-  if (e.early_fill) asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (e.early_fill) dep_wait();
   if (e.dbg_timing && tid == 0)
     e.dbg_timing[kTimCyc + 4 * blockIdx.x + 3] = gtimer() - e.dbg_timing[kTimCyc + 4 * blockIdx.x + 2];
 
