@@ -707,14 +707,16 @@ static cudaError_t launch_fft_N(int packing, const Geo& g, const Exec& e, const 
 #define PC_FFT_CASE(PK)                                                                                  \
   case PK: {                                                                                             \
     auto kfn = pc_fft_conv_kernel<PK, N>;                                                               \
-    static bool set = false;                                                                             \
-    if (!set) {                                                                                          \
+    static unsigned set = 0; /* attributes are per device: one bit each */                             \
+    int dev_ = 0;                                                                                        \
+    if ((err = cudaGetDevice(&dev_)) != cudaSuccess) return err;                                         \
+    if (!((set >> (dev_ & 31)) & 1u)) {                                                                  \
       err = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);          \
       if (err != cudaSuccess) return err;                                                                \
       /* leave the rest of the 256 KB unified array to L1: the spectrum tables stay cached */           \
       err = cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, PC_FFT_CARVEOUT);  \
       if (err != cudaSuccess) return err;                                                                \
-      set = true;                                                                                        \
+      set |= 1u << (dev_ & 31);                                                                          \
     }                                                                                                    \
     kfn<<<(unsigned)n_jobs, N / 16, smem, st>>>(g, e, f);                                              \
     break;                                                                                               \
@@ -740,12 +742,14 @@ cudaError_t launch_fft_conv(int packing, int N, const Geo& g, const Exec& e, con
     case 16384: {                                         // full precision only (2-CTA clusters)
       if (packing != PACK_FULL) return cudaErrorInvalidValue;
       const size_t smem = (size_t)(kN32 + kN32 / 16 + 64 + kN32 / 64) * sizeof(double2);
-      static bool set = false;
-      if (!set) {
+      static unsigned set = 0;                            // per device
+      int dev = 0;
+      if (cudaGetDevice(&dev) != cudaSuccess) return cudaErrorInvalidDevice;
+      if (!((set >> (dev & 31)) & 1u)) {
         cudaError_t err = cudaFuncSetAttribute(pc_fft32k_full_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)smem);
         if (err != cudaSuccess) return err;
-        set = true;
+        set |= 1u << (dev & 31);
       }
       pc_fft32k_full_kernel<<<(unsigned)(2 * n_jobs), kN32 / 16, smem, st>>>(g, e, f);
       return cudaGetLastError();

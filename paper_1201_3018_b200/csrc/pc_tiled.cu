@@ -1123,11 +1123,16 @@ template <int PACK, int T, int PT>
 static cudaError_t launch_prepack_t(const Geo& g, const Exec& e, long long n_jobs, cudaStream_t st) {
   auto kfn = pc_prepack_kernel<PACK, T, PT>;
   const size_t smem = (size_t)g.W_block * sizeof(double);
-  static size_t c_smem = 0;
-  if (smem > c_smem) {
+  static size_t c_smem = 0;                          // attribute set for (device, size): per device
+  static int c_dev = -1;
+  int dev = 0;
+  cudaError_t err0 = cudaGetDevice(&dev);
+  if (err0 != cudaSuccess) return err0;
+  if (smem > c_smem || dev != c_dev) {
     cudaError_t err = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
     c_smem = smem;
+    c_dev = dev;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)n_jobs);
