@@ -588,7 +588,8 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
   };
 
   // Pipeline fill: the first nf jobs (one per producer warp when a job is one stage) are
-  // claimed in parallel, then companded and packed by all warps, five warps per job.
+  // claimed in parallel (before griddepcontrol.wait: only this launch's queue array is touched),
+  // then companded and packed by all 16 warps, four per job.
   // (never more than a CTA's share of the launch: small launches spread over all CTAs)
   const long long share = (njobs + gridDim.x - 1) / gridDim.x;
   const int nf = e.pre_win ? 0 : (nch == 1) ? (int)min((long long)min(kTiledFillJobs, NS), share < 1 ? 1 : share) : 1;
