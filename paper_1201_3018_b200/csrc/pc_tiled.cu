@@ -39,6 +39,9 @@
 #ifndef PC_PROD_YIELD
 #define PC_PROD_YIELD 0   // 1: one DMMA core slot on an SMSP while its producer packs (measured: asym2 +1%, full +14%)
 #endif
+#ifndef PC_DMMA_NAP
+#define PC_DMMA_NAP 0     // ns a DMMA-core warp sleeps after each k-step (0: none)
+#endif
 #ifndef PC_CORE_SLOTS
 #define PC_CORE_SLOTS 2   // DMMA core: warps per SM sub-partition allowed in the core at once
 #endif
@@ -472,6 +475,10 @@ __device__ __forceinline__ void conv_chunk_mma(uint32_t xs_row, uint32_t kc_addr
       }
 #pragma unroll
       for (int mt = 0; mt < NMT; ++mt) a[mt] = an[mt];
+      // optional nap after each k-step: in tools/dmma_interference.cu a 20-ns nap per 8 DMMAs
+      // lets the SMSP's other warps issue at ~5% of the DMMA rate; in this kernel it cost 5-12%
+      // (cfg2 asym2 103.7 / full 172.9 us), so off
+      if (PC_DMMA_NAP > 0) __nanosleep(PC_DMMA_NAP);
     }
     b[0] = b[4];
     b[1] = b[5];

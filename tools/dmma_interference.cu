@@ -55,7 +55,7 @@ probe(const double2* __restrict__ src, long long n2, int batches, int mode, int 
   }
   if (mode == 0) return;
   if (mode == 4 && warp >= 8) return;
-  if (mode == 5 && warp >= 12) return;
+  if ((mode == 5 || mode >= 6) && warp >= 12) return;
   double acc[8][2];
 #pragma unroll
   for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = i;
@@ -64,9 +64,13 @@ probe(const double2* __restrict__ src, long long n2, int batches, int mode, int 
   const int r = lane >> 2, k = lane & 3;
   while (*stop == 0) {
     for (int it = 0; it < 64; ++it) {
-      if (mode == 1 || mode >= 4) {
+      if (mode == 1 || mode == 4 || mode == 5) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) dmma(acc[i][0], acc[i][1], a, bb);
+      } else if (mode >= 6) {                      // 2 warps/SMSP, a short sleep after every 8 DMMAs
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dmma(acc[i][0], acc[i][1], a, bb);
+        __nanosleep(mode == 6 ? 20 : (mode == 7 ? 60 : 150));
       } else if (mode == 2) {
         const double* xb = sx + (warp & 3) * 1024 + r * 20 + k + (it & 7) * 20;
 #pragma unroll
@@ -91,6 +95,7 @@ probe(const double2* __restrict__ src, long long n2, int batches, int mode, int 
 #pragma unroll
   for (int i = 0; i < 8; ++i) s += acc[i][0] + acc[i][1];
   if (s == 12345.678) out[0] = work;
+  if (lane == 0 && warp == 4) atomicAdd(&out[148 * 4 * 2 + 1], work);   // DMMA batches of warp 4 per CTA
 }
 
 int main() {
@@ -101,15 +106,17 @@ int main() {
   int* stop;
   cudaMalloc(&stop, 4);
   unsigned long long* out;
-  cudaMalloc(&out, 148 * 4 * 2 * 8);
-  unsigned long long h[148 * 4 * 2];
+  cudaMalloc(&out, (148 * 4 * 2 + 2) * 8);
+  unsigned long long h[148 * 4 * 2 + 2];
   const char* names[] = {"no consumers", "DMMA (registers), 3 warps/SMSP", "DMMA + LDS.64 (core mix)",
                          "DFMA chains, 3 warps/SMSP", "DMMA (registers), 1 warp/SMSP",
-                         "DMMA (registers), 2 warps/SMSP"};
+                         "DMMA (registers), 2 warps/SMSP", "2 warps/SMSP, sleep 20 ns / 8 DMMA",
+                         "2 warps/SMSP, sleep 60 ns / 8 DMMA", "2 warps/SMSP, sleep 150 ns / 8 DMMA"};
   for (int fp : {0, 1})
-    for (int mode = 0; mode < 6; ++mode) {
+    for (int mode = 0; mode < 9; ++mode) {
       for (int rep = 0; rep < 2; ++rep) {
         cudaMemset(stop, 0, 4);
+        cudaMemset(out + 148 * 4 * 2, 0, 16);
         probe<<<148, 512>>>(src, n2, 64, mode, fp, stop, out);
         cudaError_t e = cudaDeviceSynchronize();
         if (e != cudaSuccess) {
@@ -120,8 +127,10 @@ int main() {
       cudaMemcpy(h, out, sizeof(h), cudaMemcpyDeviceToHost);
       double tot = 0;
       for (int i = 0; i < 148 * 4; ++i) tot += (double)h[2 * i];
-      printf("producer max %s | consumers: %-32s: %.0f cycles per batch of 16 x LDG.128 (+ %s max)\n",
-             fp ? "FP64" : "int ", names[mode], tot / (148 * 4) / 64, fp ? "FP64" : "integer");
+      printf("producer max %s | consumers: %-36s: %.0f cycles per batch of 16 x LDG.128 (+ %s max); "
+             "warp-4 DMMA per producer batch-time: %.2f\n",
+             fp ? "FP64" : "int ", names[mode], tot / (148 * 4) / 64, fp ? "FP64" : "integer",
+             (double)h[148 * 4 * 2 + 1] * 64 * 8 / 148 / (tot / (148 * 4)) * 16);
     }
   return 0;
 }
