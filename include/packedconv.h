@@ -78,14 +78,18 @@ typedef struct conv_opts {
                                [4]: force the FFT size N (complex points, 1024..8192; 16384 =
                                     the 32768-point real transform of the whole block, full
                                     precision, W_block <= 16386, 2-CTA clusters);
-                               [6]: tiled-kernel producers: 1 = compand/pack with integer ops
-                                    (dyadic eps; bit-identical), else FP64 ops;
-                               [7]: cap on the tiled kernel's stage-ring slots (>= 2; diagnostics);
-                               [8]: 2 = compand/pack in a prepack kernel ahead of the DMMA-core
-                                    launch instead of its producer warps (single-chunk plans);
                                [5]: unpack form, 0 balanced digits (C6), 1 the literal
                                     Eqs. (11)-(15) with the u_sys guard (symmetric packing,
-                                    direct core; exact for R_max < 89,524, reading C6); rest 0 */
+                                    direct core; exact for R_max < 89,524, reading C6);
+                               [6]: tiled-kernel producers: 1 = compand/pack with integer ops
+                                    (dyadic eps; bit-identical), else FP64 ops;
+                               [7]: >= 2: cap on the tiled kernel's stage-ring slots; < 0: the
+                                    producers claim job m only once consumers hold parts of
+                                    m + reserved[7] (diagnostics);
+                               [8]: 2 = compand/pack in a prepack kernel ahead of the tiled
+                                    launch instead of its producer warps (single-chunk plans,
+                                    W_block <= 25,600); rest 0.  All results are bit-identical
+                                    under every setting (tested). */
   double u_sys;             /* P:153; used only by the literal paper unpack form          */
 } conv_opts;
 
