@@ -88,8 +88,8 @@ typedef struct conv_opts {
                                     m + reserved[7] (diagnostics);
                                [8]: 2 = compand/pack in a prepack kernel ahead of the tiled
                                     launch instead of its producer warps (single-chunk plans,
-                                    W_block <= 25,600); rest 0.  All results are bit-identical
-                                    under every setting (tested). */
+                                    W_block <= 25,600); rest 0.  Packed results are bit-identical
+                                    under every setting, full precision within 1e-12 (tested). */
   double u_sys;             /* P:153; used only by the literal paper unpack form          */
 } conv_opts;
 
