@@ -229,10 +229,12 @@ bool tiled_shape(const conv_plan* p, int packing, TShape* sh, bool taps_per_sign
   const int K = core_taps(p, packing);
   const int force = p->opts.reserved[1];
   // core: the FP64 tensor cores (DMMA, T = 16) unless the FMA core or another tile is forced;
-  // auto picks the FMA core for symmetric packing (its short core -- about N/2 taps -- and heavy
-  // three-digit epilogue measured 5% faster there: profiles/r01_core_choice.json)
+  // auto keeps the FMA core for symmetric packing with a short core (about N/2 taps): there the
+  // three-digit epilogue weighs as much as the core and the DMMA interference slows it (cfg2,
+  // 257 taps: FMA 71.6 vs DMMA 75.6 us); from 384 taps on DMMA wins (512 taps: 129.7 vs 134.8 us,
+  // cfg4's 4097: 143.4 vs 160.0 ms)
   const int core = p->opts.reserved[2];
-  sh->mma = (core == 2 || (core == 0 && packing != PC_PACK_SYM)) && (force == 0 || force == 16);
+  sh->mma = (core == 2 || (core == 0 && (packing != PC_PACK_SYM || K >= 384))) && (force == 0 || force == 16);
   double best = -1.0;
   for (int T : pc::kTPChoices) {
     if ((force == 12 || force == 14 || force == 16) && T != force) continue;
