@@ -232,9 +232,11 @@ bool tiled_shape(const conv_plan* p, int packing, TShape* sh, bool taps_per_sign
   // auto keeps the FMA core for symmetric packing with a short core (about N/2 taps): there the
   // three-digit epilogue weighs as much as the core and the DMMA interference slows it (cfg2,
   // 257 taps: FMA 71.6 vs DMMA 75.6 us); from 384 taps on DMMA wins (512 taps: 129.7 vs 134.8 us,
-  // cfg4's 4097: 143.4 vs 160.0 ms)
+  // cfg4's 4097: 143.4 vs 160.0 ms); likewise asymmetric M = 3 below 256 taps (129 taps: FMA 49.9
+  // vs 55.1 us; 257: equal; 513: DMMA 82.6 vs 95); asym2 and full precision: DMMA at every length
   const int core = p->opts.reserved[2];
-  sh->mma = (core == 2 || (core == 0 && (packing != PC_PACK_SYM || K >= 384))) && (force == 0 || force == 16);
+  const bool long_core = packing == PC_PACK_SYM ? K >= 384 : (packing == PC_PACK_ASYM3 ? K >= 256 : true);
+  sh->mma = (core == 2 || (core == 0 && long_core)) && (force == 0 || force == 16);
   double best = -1.0;
   for (int T : pc::kTPChoices) {
     if ((force == 12 || force == 14 || force == 16) && T != force) continue;
