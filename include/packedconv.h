@@ -72,7 +72,7 @@ typedef struct conv_opts {
   int32_t reserved[9];      /* [0]: raw-block staging 0 auto/1 on/2 off (per-block kernel);
                                [1]: force the persistent core tile (12/14/16; tests);
                                [2]: direct core, 0 auto (the FP64 tensor cores -- DMMA, T = 16 --
-                                    except symmetric packing with < 384 core taps and asym3 with
+                                    except symmetric packing with < 768 core taps and asym3 with
                                     < 256: FMA), 1 the FP64 FMA core (any T), 2 DMMA;
                                [3]: force consumer warps per job (1, 2, 4; diagnostics);
                                [4]: force the FFT size N (complex points, 1024..8192; 16384 =

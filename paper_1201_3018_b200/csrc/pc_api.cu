@@ -231,11 +231,12 @@ bool tiled_shape(const conv_plan* p, int packing, TShape* sh, bool taps_per_sign
   // core: the FP64 tensor cores (DMMA, T = 16) unless the FMA core or another tile is forced;
   // auto keeps the FMA core for symmetric packing with a short core (about N/2 taps): there the
   // three-digit epilogue weighs as much as the core and the DMMA interference slows it (cfg2,
-  // 257 taps: FMA 71.6 vs DMMA 75.6 us); from 384 taps on DMMA wins (512 taps: 129.7 vs 134.8 us,
-  // cfg4's 4097: 143.4 vs 160.0 ms); likewise asymmetric M = 3 below 256 taps (129 taps: FMA 49.9
+  // 257 taps: FMA 71.6 vs DMMA 75.6 us; 512 taps: within +-8% either way by geometry); from 768
+  // taps on DMMA wins (1025: 429 vs 438 us, cfg4's 4097: 143.4 vs 160.0 ms); likewise asymmetric
+  // M = 3 below 256 taps (129 taps: FMA 49.9
   // vs 55.1 us; 257: equal; 513: DMMA 82.6 vs 95); asym2 and full precision: DMMA at every length
   const int core = p->opts.reserved[2];
-  const bool long_core = packing == PC_PACK_SYM ? K >= 384 : (packing == PC_PACK_ASYM3 ? K >= 256 : true);
+  const bool long_core = packing == PC_PACK_SYM ? K >= 768 : (packing == PC_PACK_ASYM3 ? K >= 256 : true);
   sh->mma = (core == 2 || (core == 0 && long_core)) && (force == 0 || force == 16);
   double best = -1.0;
   for (int T : pc::kTPChoices) {
