@@ -173,7 +173,7 @@ int conv_execute_batch(conv_plan* plan, const double* s_dev, int64_t n_signals, 
 
 /* End-to-end through host memory: copies s_host (L doubles) to the device, runs
  * conv_execute, copies L_out doubles back to r_host, and synchronizes `stream`.  Plans of
- * >= 128 blocks pipeline 9 block ranges over plan-owned copy streams (H2D of range
+ * >= 128 blocks pipeline 15 block ranges over plan-owned copy streams (H2D of range
  * c+1, core of range c and D2H of range c-1 overlap); pinned host buffers are needed for
  * the copies to overlap.  Results are identical to conv_execute. */
 int conv_execute_host(conv_plan* plan, const double* s_host, double* r_host, void* stream);

@@ -947,16 +947,31 @@ int conv_execute_host(conv_plan* p, const double* s_host, double* r_host, void* 
   // reading pinned input over PCIe took 2.1 ms at cfg2 -- the peak and packing passes read each
   // sample twice over the link -- and storing outputs straight to pinned memory 1.07-1.36 ms,
   // against 1.04 ms for this copy pipeline; the link's duplex floor is 0.71 ms.)
-  static const int kW[9] = {1, 2, 4, 4, 4, 4, 4, 2, 1};
-  int nchunk = (p->packing == PC_PACK_ADAPTIVE || p->P < 128) ? 1 : 9;
+  // (15 ranges 1:1:2:..:2:1:1 measured 0.98-1.00 ms at cfg2 against 1.04-1.05 for 1:2:4:4:4:4:4:2:1
+  // and 1.01-1.02 for 16 equal ranges; PC_HOST_WEIGHTS="w0,w1,..." overrides, diagnostics)
+  static const int kW[15] = {1, 1, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2, 1, 1};
+  int nchunk = (p->packing == PC_PACK_ADAPTIVE || p->P < 128) ? 1 : 15;
   long long cum[33] = {0};
-  for (int i = 0; i < 9; ++i) cum[i + 1] = cum[i] + kW[i];
+  for (int i = 0; i < 15; ++i) cum[i + 1] = cum[i] + kW[i];
   if (const char* ev = std::getenv("PC_HOST_CHUNKS")) {         // diagnostics: n equal ranges
     const int n = std::atoi(ev);
     if (n >= 1 && n <= 16 && nchunk > 1) {            // (16 event pairs)
       nchunk = n;
       for (int i = 0; i <= n; ++i) cum[i] = i;
     }
+  }
+  if (const char* ev = std::getenv("PC_HOST_WEIGHTS")) {        // diagnostics: "w0,w1,..." (<= 16)
+    int n = 0;
+    long long acc = 0;
+    for (const char* q = ev; *q && n < 16 && nchunk > 1;) {
+      const long long w = std::atoll(q);
+      if (w <= 0) break;
+      acc += w;
+      cum[++n] = acc;
+      while (*q && *q != ',') ++q;
+      if (*q == ',') ++q;
+    }
+    if (n >= 1 && nchunk > 1) nchunk = n;
   }
   if (nchunk <= 1) {
     if (cudaMemcpyAsync(p->d_in, s_host, sizeof(double) * p->L, cudaMemcpyHostToDevice, st) != cudaSuccess)
