@@ -874,7 +874,10 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
       const int nt = (c == nch - 1) ? mp.K_pad - c * KC : KC;
       if (MMA) {                                             // a5 on the tensor cores
         const uint32_t xrow = smem_u32(xs) + 8u * PT * (pg0 + front);
-        const int jj_n = (c == nch - 1) ? nt / 16 + 1 : KC / 16;   // the last chunk adds the phase tail
+        // the last chunk ends where the taps end: jj covers taps [16 jj - 15, 16 jj + 15], so the
+        // nonzero ones need jj < (K + 15) / 16 in all (one jj fewer than K_pad / 16 + 1 when
+        // K = 1 mod 16, e.g. N' = 513, 4097: a whole jj of zero DMMAs saved)
+        const int jj_n = (c == nch - 1) ? max(0, (mp.K + 30) / 16 - c * (KC / 16)) : KC / 16;
         switch (n_mt) {
           case 4: conv_chunk_mma<4, PT>(xrow, smem_u32(kc), jj_n, fr, lane); break;
           case 3: conv_chunk_mma<3, PT>(xrow, smem_u32(kc), jj_n, fr, lane); break;
