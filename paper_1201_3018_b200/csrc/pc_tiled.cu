@@ -441,50 +441,73 @@ __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
       : "+d"(d[0]), "+d"(d[1])
       : "d"(a), "d"(b));
 }
+// One jj step of conv_chunk_mma (the A/B fragments of the next k-step / jj are loaded first).
+// EDGE: the first or last jj of a chunk, where fragment F_d (taps [d - 7, d + 3]; d = 16 jj + 4 s
+// for n-tile 0, 16 jj + 4 s - 8 for n-tile 1) can lie wholly outside the chunk's nonzero taps
+// [t_lo, t_hi): its DMMAs are skipped (warp-uniform); the steps in between carry no test.
+template <int NMT, int PT, bool EDGE>
+__device__ __forceinline__ void mma_jj_step(int jj, int jj_n, uint32_t xa, uint32_t ka, double (&fr)[4][2][2],
+                                            double (&b)[6], double (&a)[NMT], int t_lo, int t_hi) {
+  double bn[4], an[NMT];
+  const bool more = jj + 1 < jj_n;
+  if (more) {
+#pragma unroll
+    for (int f = 0; f < 4; ++f) bn[f] = lds64(ka + 128u + 32u * (f + 2));
+  }
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    if (s < 3 || more) {
+#pragma unroll
+      for (int mt = 0; mt < NMT; ++mt)
+        an[mt] = lds64(xa + 8u * (8 * mt * PT) + (s < 3 ? 32u * (s + 1) : 8u * PT));
+    }
+    bool z0 = false, z1 = false;
+    if (EDGE) {
+      const int d0 = 16 * jj + 4 * s, d1 = d0 - 8;
+      z0 = d0 + 3 < t_lo || d0 - 7 >= t_hi;
+      z1 = d1 + 3 < t_lo || d1 - 7 >= t_hi;
+    }
+#pragma unroll
+    for (int mt = 0; mt < NMT; ++mt) {
+      if (!z0) dmma884(fr[mt][0], a[mt], b[s + 2]);
+      if (!z1) dmma884(fr[mt][1], a[mt], b[s]);
+    }
+#pragma unroll
+    for (int mt = 0; mt < NMT; ++mt) a[mt] = an[mt];
+    // optional nap after each k-step: in tools/dmma_interference.cu a 20-ns nap per 8 DMMAs
+    // lets the SMSP's other warps issue at ~5% of the DMMA rate; in this kernel it cost 5-12%
+    // (cfg2 asym2 103.7 / full 172.9 us), so off
+    if (PC_DMMA_NAP > 0) __nanosleep(PC_DMMA_NAP);
+  }
+  b[0] = b[4];
+  b[1] = b[5];
+  if (more) {
+#pragma unroll
+    for (int f = 0; f < 4; ++f) b[f + 2] = bn[f];
+  }
+}
+
 template <int NMT, int PT>
 __device__ __forceinline__ void conv_chunk_mma(uint32_t xs_row, uint32_t kc_addr, int jj_n, double (&fr)[4][2][2],
-                                               int lane) {
+                                               int lane, int t_lo = -(1 << 30), int t_hi = 1 << 30) {
   const int r = lane >> 2, k = lane & 3;
   uint32_t xa = xs_row + 8u * (uint32_t)(r * PT + k);
   uint32_t ka = kc_addr + 8u * (uint32_t)(k - r) - 64u;   // b[f] = kr[16 jj - 8 + 4 f + k - r]
   // Software-pipelined: the A fragments of the next k-step and the B fragments of the next jj
   // are loaded before the current DMMAs issue (one warp alone must keep the pipe fed).
-  double b[6], bn[4], a[NMT], an[NMT];
+  double b[6], a[NMT];
 #pragma unroll
   for (int f = 0; f < 6; ++f) b[f] = lds64(ka + 32u * f);
 #pragma unroll
   for (int mt = 0; mt < NMT; ++mt) a[mt] = lds64(xa + 8u * (8 * mt * PT));
+  if (jj_n <= 0) return;
+  mma_jj_step<NMT, PT, true>(0, jj_n, xa, ka, fr, b, a, t_lo, t_hi);      // first jj: peeled
 #pragma unroll 1
-  for (int jj = 0; jj < jj_n; ++jj, xa += 8u * PT, ka += 128u) {
-    const bool more = jj + 1 < jj_n;
-    if (more) {
-#pragma unroll
-      for (int f = 0; f < 4; ++f) bn[f] = lds64(ka + 128u + 32u * (f + 2));
-    }
-#pragma unroll
-    for (int s = 0; s < 4; ++s) {
-      if (s < 3 || more) {
-#pragma unroll
-        for (int mt = 0; mt < NMT; ++mt)
-          an[mt] = lds64(xa + 8u * (8 * mt * PT) + (s < 3 ? 32u * (s + 1) : 8u * PT));
-      }
-#pragma unroll
-      for (int mt = 0; mt < NMT; ++mt) {
-        dmma884(fr[mt][0], a[mt], b[s + 2]);
-        dmma884(fr[mt][1], a[mt], b[s]);
-      }
-#pragma unroll
-      for (int mt = 0; mt < NMT; ++mt) a[mt] = an[mt];
-      // optional nap after each k-step: in tools/dmma_interference.cu a 20-ns nap per 8 DMMAs
-      // lets the SMSP's other warps issue at ~5% of the DMMA rate; in this kernel it cost 5-12%
-      // (cfg2 asym2 103.7 / full 172.9 us), so off
-      if (PC_DMMA_NAP > 0) __nanosleep(PC_DMMA_NAP);
-    }
-    b[0] = b[4];
-    b[1] = b[5];
-#pragma unroll
-    for (int f = 0; f < 4; ++f) b[f + 2] = bn[f];
-  }
+  for (int jj = 1; jj < jj_n - 1; ++jj)
+    mma_jj_step<NMT, PT, false>(jj, jj_n, xa + 8u * PT * jj, ka + 128u * jj, fr, b, a, t_lo, t_hi);
+  if (jj_n > 1)                                                            // last jj: peeled
+    mma_jj_step<NMT, PT, true>(jj_n - 1, jj_n, xa + 8u * PT * (jj_n - 1), ka + 128u * (jj_n - 1), fr, b, a, t_lo,
+                               t_hi);
 }
 
 template <int PACK, int T, int MMA>
@@ -879,10 +902,10 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
         // K = 1 mod 16, e.g. N' = 513, 4097: a whole jj of zero DMMAs saved)
         const int jj_n = (c == nch - 1) ? max(0, (mp.K + 30) / 16 - c * (KC / 16)) : KC / 16;
         switch (n_mt) {
-          case 4: conv_chunk_mma<4, PT>(xrow, smem_u32(kc), jj_n, fr, lane); break;
-          case 3: conv_chunk_mma<3, PT>(xrow, smem_u32(kc), jj_n, fr, lane); break;
-          case 2: conv_chunk_mma<2, PT>(xrow, smem_u32(kc), jj_n, fr, lane); break;
-          case 1: conv_chunk_mma<1, PT>(xrow, smem_u32(kc), jj_n, fr, lane); break;
+          case 4: conv_chunk_mma<4, PT>(xrow, smem_u32(kc), jj_n, fr, lane, -c * KC, mp.K - c * KC); break;
+          case 3: conv_chunk_mma<3, PT>(xrow, smem_u32(kc), jj_n, fr, lane, -c * KC, mp.K - c * KC); break;
+          case 2: conv_chunk_mma<2, PT>(xrow, smem_u32(kc), jj_n, fr, lane, -c * KC, mp.K - c * KC); break;
+          case 1: conv_chunk_mma<1, PT>(xrow, smem_u32(kc), jj_n, fr, lane, -c * KC, mp.K - c * KC); break;
           default: break;
         }
       } else if (mine) {
