@@ -869,3 +869,16 @@ def test_fft_core_backend_validation_worst_case(packing, Q):
     u_sys = 4.0 * worst * info["eps"]              # absolute deviation of a packed core output
     print(f"FFT core {packing} Q={Q}: max last-digit residual {worst:.3g} LSB, calibrated u_sys {u_sys:.3g} "
           f"(paper {O.U_SYS_PAPER:.4g})")
+
+
+@pytest.mark.parametrize("packing,N,mma", [(O.SYM, 513, 0), (O.SYM, 2049, 1), (O.ASYM3, 129, 0), (O.ASYM3, 513, 1),
+                                           (O.ASYM2, 129, 1), (O.FULL, 129, 1)])
+def test_auto_core_choice(packing, N, mma):
+    """The auto core rule (conv_opts.reserved[2] = 0): DMMA except short symmetric (< 768 core taps)
+    and asym3 (< 256) cores, which keep the FMA loop -- the measured crossovers."""
+    W_block = 8192
+    with pcb.Plan(100_000, N, W_block, pcb.MODE_CONV, PK[packing], 0 if packing == O.FULL else 3,
+                  opts=pcb.opts_default(bound_policy=pcb.BOUND_WARN)) as p:
+        p.set_kernel(dev(np.linspace(-1, 1, N)))
+        info = p.info()
+        assert info["core_mma"] == mma and info["core_tile"] in (12, 14, 16)
