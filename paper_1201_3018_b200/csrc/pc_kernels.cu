@@ -332,8 +332,13 @@ __global__ void __launch_bounds__(kMaxThreads, 1) pc_fused_kernel(Geo g, Exec e)
 // ------------------------------------------------------------------ a8: block statistics
 // Per block: peak p and sigma from the second moment on the fixed grid z = [[x 2^20/p]]
 // with an exact int64 sum (reading C12).
-__global__ void pc_block_stats(Geo g, const double* __restrict__ s, double* __restrict__ sigma,
-                               double* __restrict__ peak_out) {
+// One CTA per block.  The block's samples (up to kStatsU per thread) stay in registers across
+// both passes -- the peak, then sum z^2 on the fixed 2^20 grid -- so the input is read from HBM
+// once with every load in flight (the two-pass loop re-read it and was latency-bound:
+// 46 us for 134 MB at L = 2^24); longer blocks fall back to the loop.
+constexpr int kStatsThreads = 256, kStatsU = 16;
+__global__ void __launch_bounds__(kStatsThreads) pc_block_stats(Geo g, const double* __restrict__ s,
+                                                                double* __restrict__ sigma, double* __restrict__ peak_out) {
   __shared__ double red[32];
   __shared__ unsigned long long ired[32];
   const long long w = blockIdx.x;
@@ -342,13 +347,39 @@ __global__ void pc_block_stats(Geo g, const double* __restrict__ s, double* __re
   const long long avail = g.L - g0;
   const int n_valid = (int)(avail < 0 ? 0 : (avail > g.W_block ? g.W_block : avail));
   const double* src = s + g0;
-  const double p = block_max_abs(nullptr, n_valid, src, n_valid, false, red);
   unsigned long long acc = 0;
-  if (p != 0.0) {
-    const double sc = 1048576.0 / p;
-    for (int i = tid; i < n_valid; i += nt) {
-      const long long z = (long long)round(__dmul_rn(src[i], sc));
-      acc += (unsigned long long)(z * z);
+  double p;
+  if (n_valid <= kStatsU * kStatsThreads && nt == kStatsThreads) {
+    double v[kStatsU];
+    double m = 0.0;
+#pragma unroll
+    for (int u = 0; u < kStatsU; ++u) {
+      const int i = tid + u * kStatsThreads;
+      v[u] = (i < n_valid) ? __ldg(src + i) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kStatsU; ++u) m = fmax(m, fabs(v[u]));
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((tid & 31) == 0) red[tid >> 5] = m;
+    __syncthreads();
+    p = 0.0;
+    for (int wi = 0; wi < kStatsThreads / 32; ++wi) p = fmax(p, red[wi]);
+    if (p != 0.0) {
+      const double sc = 1048576.0 / p;
+#pragma unroll
+      for (int u = 0; u < kStatsU; ++u) {
+        const long long z = (long long)round(__dmul_rn(v[u], sc));   // zeros beyond n_valid add 0
+        acc += (unsigned long long)(z * z);
+      }
+    }
+  } else {
+    p = block_max_abs(nullptr, n_valid, src, n_valid, false, red);
+    if (p != 0.0) {
+      const double sc = 1048576.0 / p;
+      for (int i = tid; i < n_valid; i += nt) {
+        const long long z = (long long)round(__dmul_rn(src[i], sc));
+        acc += (unsigned long long)(z * z);
+      }
     }
   }
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -514,7 +545,7 @@ cudaError_t launch_build_taps(const double* k_pad, const double* k_int, int Np, 
 }
 
 cudaError_t launch_block_stats(const Geo& g, const double* s, double* sigma, double* peak, cudaStream_t st) {
-  pc_block_stats<<<(unsigned)g.P, 256, 0, st>>>(g, s, sigma, peak);
+  pc_block_stats<<<(unsigned)g.P, kStatsThreads, 0, st>>>(g, s, sigma, peak);
   return cudaGetLastError();
 }
 
