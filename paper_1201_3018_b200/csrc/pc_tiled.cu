@@ -585,6 +585,10 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
   if (e.blk_list) {                                  // adaptive: count written by pc_adapt_lists
     const long long nb = *e.blk_count;
     njobs = nb == 0 ? 0 : (e.blk_list[0] == 0 ? e.tiles0 + (nb - 1) * e.tiles1 : nb * e.tiles1);
+    if (njobs == 0) {          // no block chose this packing: leave once the tap copy has landed
+      mbar_wait_wd(&ps->bar_taps, 0, 4, 0, 0);   // (every CTA leaves: the queues stay untouched)
+      return;
+    }
   }
 
   // Locate a job's block and input.
