@@ -433,7 +433,9 @@ __global__ void pc_adapt_decide(long long P, const double* __restrict__ sigma, c
 // ------------------------------------------------------------------ a8: per-packing block lists
 // Compacts the per-block decisions into one ascending block list per packing (FULL, SYM,
 // ASYM2, ASYM3), so the tiled kernel can run each packing's blocks in its own launch.
-// One CTA of 1024 threads: ballot prefix within warps, a scan over warp totals per round.
+// One CTA of 1024 threads, kListsPer consecutive blocks per thread per round (fewer rounds and
+// barriers): per-thread counts, a warp scan of them, a scan over warp totals per packing.
+constexpr int kListsPer = 4;
 __global__ void __launch_bounds__(1024) pc_adapt_lists(long long P, const int* __restrict__ dec_pack,
                                                        int* __restrict__ lists, int* __restrict__ counts) {
   __shared__ int woff[4][32];   // per round: warp counts, then their exclusive offsets
@@ -441,15 +443,25 @@ __global__ void __launch_bounds__(1024) pc_adapt_lists(long long P, const int* _
   __shared__ int rtot[4];       // round totals
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (tid < 4) base[tid] = 0;
-  for (long long r0 = 0; r0 < P; r0 += 1024) {
-    const long long w = r0 + tid;
-    const int d = (w < P) ? dec_pack[w] : -1;
-    int pre = 0;
+  for (long long r0 = 0; r0 < P; r0 += 1024 * kListsPer) {
+    int d[kListsPer], cnt[4] = {0, 0, 0, 0};
 #pragma unroll
-    for (int m = 0; m < 4; ++m) {
-      const unsigned bal = __ballot_sync(0xffffffffu, d == m);
-      if (d == m) pre = __popc(bal & ((1u << lane) - 1u));
-      if (lane == 0) woff[m][wid] = __popc(bal);
+    for (int j = 0; j < kListsPer; ++j) {
+      const long long w = r0 + (long long)kListsPer * tid + j;
+      d[j] = (w < P) ? dec_pack[w] : -1;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) cnt[m] += (d[j] == m);
+    }
+    int excl[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {                   // exclusive prefix of this thread within its warp
+      int x = cnt[m];
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      excl[m] = x - cnt[m];
+      if (lane == 31) woff[m][wid] = x;
     }
     __syncthreads();
     if (wid < 4) {                                  // warp m scans packing m's 32 warp counts
@@ -463,7 +475,17 @@ __global__ void __launch_bounds__(1024) pc_adapt_lists(long long P, const int* _
       if (lane == 31) rtot[wid] = x;
     }
     __syncthreads();
-    if (d >= 0) lists[(size_t)d * P + base[d] + woff[d][wid] + pre] = (int)w;
+#pragma unroll
+    for (int j = 0; j < kListsPer; ++j) {           // ascending: thread order, then j
+      const int m = d[j];
+      if (m >= 0) {
+        int pos = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q == m) pos = base[q] + woff[q][wid] + excl[q]++;
+        lists[(size_t)m * P + pos] = (int)(r0 + (long long)kListsPer * tid + j);
+      }
+    }
     __syncthreads();
     if (tid < 4) base[tid] += rtot[tid];
     __syncthreads();
