@@ -494,11 +494,8 @@ def max_q_under_bound(k_padded, Np, packing, eps_rule, rmax_rule, q_cap=1 << 15)
     bound = bound_for(packing, eps_rule)
     best = 0
     for Q in range(1, q_cap + 1):
-        if rmax_rule == RMAX_PAPER:
-            R = Np * Q * Q
-        else:
-            k_int, _, _ = compand(k_padded, Q)
-            R = Q * int(np.sum(np.abs(k_int)))
+        k_int = compand(k_padded, Q)[0] if rmax_rule == RMAX_L1 else None   # Eq. (2) at K_q = Q
+        R = companding_range(Np, Q, Q, k_int, rmax_rule)                  # Eq. (3) / C3
         if R <= bound:
             best = Q
         else:

@@ -455,3 +455,67 @@ def test_validate_backend_u_sys():
     d_huge, _ = O.validate_backend(801, 12_800_000, trials=20)
     assert d_small < d_big < d_huge
     assert u_big < 0.5 * 2.0 ** -17
+
+
+# ---------------------------------------------------------------- round 2: L1-rule Q search
+
+def test_max_q_l1_rule_all_ones_801():
+    """All-ones 801-tap kernel: k~ = Q * 1 at K_q = Q (Eq. (2), ||k||_inf = 1), so the L1 rule
+    R = S_q ||k~||_1 = 801 Q^2 coincides with Eq. (3).  By hand: Table 1's 97,667
+    admits 801*11^2 = 96,921 but not 801*12^2 = 115,344 -> Q = 11 (S:401's value); the dyadic
+    3-digit bound 131,071 (C4) admits 115,344 but not 801*13^2 = 135,369 -> Q = 12; the dyadic
+    2-digit bound 67,108,863 admits 801*289^2 = 66,900,321 but not 801*290^2 = 67,364,100."""
+    kp = np.ones(801)
+    for rule in (O.RMAX_L1, O.RMAX_PAPER):
+        assert O.max_q_under_bound(kp, 801, O.SYM, O.EPS_PAPER, rule) == 11
+        assert O.max_q_under_bound(kp, 801, O.SYM, O.EPS_POW2, rule) == 12
+        assert O.max_q_under_bound(kp, 801, O.ASYM3, O.EPS_POW2, rule) == 12
+        assert O.max_q_under_bound(kp, 801, O.ASYM2, O.EPS_POW2, rule) == 289
+
+
+def test_max_q_l1_rule_three_tap_hand_example():
+    """k = [0.5, -1, 0.25]: c_k = Q, k~ = [[0.5 Q]], -Q, [[0.25 Q]] (round half away, C5).
+    L1 rule R(Q) = Q (Q + [[Q/2]] + [[Q/4]]) against the dyadic 3-digit bound 131,071:
+      Q = 273: 273 (273 + 137 + 68) = 130,494 <= 131,071
+      Q = 274: 274 (274 + 137 + 69) = 131,520 >  131,071   -> Q = 273.
+    The PAPER rule R = N' Q^2 = 3 Q^2 gives 3*209^2 = 131,043 <= bound < 3*210^2 = 132,300 -> 209,
+    so a search that silently used Eq. (3) instead of the L1 rule fails."""
+    kp = np.array([0.5, -1.0, 0.25])
+    assert O.max_q_under_bound(kp, 3, O.SYM, O.EPS_POW2, O.RMAX_L1) == 273
+    assert O.max_q_under_bound(kp, 3, O.SYM, O.EPS_POW2, O.RMAX_PAPER) == 209
+    # the straddling values themselves, by hand
+    assert O.companding_range(3, 273, 273, O.compand(kp, 273)[0], O.RMAX_L1) == 130494
+    assert O.companding_range(3, 274, 274, O.compand(kp, 274)[0], O.RMAX_L1) == 131520
+
+
+def test_max_q_l1_rule_scale_invariant_and_monotone():
+    """Companding divides by ||k||_inf (Eq. (2)), so scaling k by any power of two leaves
+    k~ and hence Q unchanged; a zero tap appended (C13) changes neither ||k~||_1 nor Q."""
+    kp = np.array([0.5, -1.0, 0.25])
+    for scale in (2.0 ** -7, 1.0, 2.0 ** 9):
+        assert O.max_q_under_bound(kp * scale, 3, O.SYM, O.EPS_POW2, O.RMAX_L1) == 273
+    assert O.max_q_under_bound(np.append(kp, 0.0), 4, O.SYM, O.EPS_POW2, O.RMAX_L1) == 273
+
+
+def test_flop_model_frequency_forms_structure():
+    """Table 1's frequency-domain FLOP cells are three FFTs of Franchetti's
+    5 n log2 n ([13]) at the Table's transform length plus a linear term:
+      full  n = 3N+1:      15 n log2 n + n
+      sym   same n:        half of full's transform flops + 5N + 1
+      asym2 n = 2N+1:      15 n log2 n + 6.5 (3N+1)
+      asym3 n = 5N/3+1:    15 n log2 n + (62N + 21) / 3
+    A wrong coefficient or transform length in any cell breaks one of these."""
+    for N in (3, 32, 800, 8192):
+        n_full, n_a2, n_a3 = 3 * N + 1, 2 * N + 1, 5.0 * N / 3.0 + 1
+        full = O.flop_count(O.FULL, "freq", N)
+        assert math.isclose(full, 15 * n_full * math.log2(n_full) + n_full, rel_tol=1e-12)
+        sym = O.flop_count(O.SYM, "freq", N)
+        assert math.isclose(sym - (5 * N + 1), 0.5 * (full - n_full), rel_tol=1e-12)
+        a2 = O.flop_count(O.ASYM2, "freq", N)
+        assert math.isclose(a2, 15 * n_a2 * math.log2(n_a2) + 6.5 * (3 * N + 1), rel_tol=1e-12)
+        a3 = O.flop_count(O.ASYM3, "freq", N)
+        assert math.isclose(a3, 15 * n_a3 * math.log2(n_a3) + (62 * N + 21) / 3.0, rel_tol=1e-12)
+    # P:127: "symmetric packing is expected to be the fastest method under both ... domains"
+    for N in (32, 800, 8192):
+        f = {m: O.flop_count(m, "freq", N) for m in (O.FULL, O.SYM, O.ASYM2, O.ASYM3)}
+        assert f[O.SYM] == min(f.values())
