@@ -38,10 +38,13 @@ enum {
   PC_OK = 0,
   PC_E_CONFIG = 2,          /* invalid geometry / arguments ("config error")        */
   PC_E_BOUND = 3,           /* R_max exceeds the packing's bound under STRICT      */
-  PC_E_BACKEND = 4,         /* backend validation failure                          */
+  PC_E_BACKEND = 4,         /* backend validation failure: the FFT core's
+                               worst-case last-digit error, x4, exceeds 0.5 LSB    */
   PC_E_CUDA = 5,            /* a CUDA runtime call failed / no device                     */
   PC_W_UNPACK_MARGIN = 6,   /* warning: digit residual exceeded 0.25 LSB (FFT core)        */
-  PC_E_STATE = 7            /* call order violated (e.g. execute before set_kernel)        */
+  PC_E_STATE = 7,           /* call order violated (e.g. execute before set_kernel)        */
+  PC_E_WATCHDOG = 8         /* a persistent kernel's internal wait timed out (4 s) and the
+                               launch abandoned its work: its outputs are invalid          */
 };
 
 /* ---- enumerations -------------------------------------------------------------------- */
@@ -59,38 +62,49 @@ enum { PC_CORE_DIRECT = 0, PC_CORE_FFT = 1 };              /* Tier-2 core
  * block, phases separated by barriers (also the form that serves conv_execute_debug). */
 enum { PC_EXEC_FUSED = 0, PC_EXEC_PERBLOCK = 1, PC_EXEC_TILED = 2 };
 
+/* Direct-core variants (conv_opts.core_variant).  AUTO = the FP64 tensor cores (DMMA,
+ * mma.sync m8n8k4 f64, tile 16) except symmetric packing with < 768 core taps and asym3 with
+ * < 256, which keep the FP64 FMA core (measured). */
+enum { PC_CORE_AUTO = 0, PC_CORE_FMA = 1, PC_CORE_DMMA = 2 };
+enum { PC_UNPACK_BALANCED = 0, PC_UNPACK_LITERAL = 1 };  /* C6; Eqs.(11)-(15) P:101-115    */
+
 /* Plan options.  conv_opts_default() fills: eps_rule POW2, rmax_rule PAPER, bound_policy
- * STRICT, core DIRECT, exec FUSED, K_q 0 (= Q), device -1 (current), u_sys 3.1193e-11. */
+ * STRICT, core DIRECT, exec FUSED, K_q 0 (= Q), device -1 (current), every tuning field 0
+ * (automatic), u_sys 3.1193e-11.  Packed results are bit-identical under every tuning
+ * setting and full precision is within 1e-12 (tested); the tuning fields exist for tests
+ * and measurements. */
 typedef struct conv_opts {
-  int32_t eps_rule;
-  int32_t rmax_rule;
-  int32_t bound_policy;
-  int32_t core;
-  int32_t exec;
+  int32_t eps_rule;         /* PC_EPS_*: Eq. (6), C2, C4                            */
+  int32_t rmax_rule;        /* PC_RMAX_*: Eq. (3) or the attainable L1 range (C3)   */
+  int32_t bound_policy;     /* PC_BOUND_*: refuse (STRICT) or flag (WARN) beyond the bound */
+  int32_t core;             /* PC_CORE_DIRECT / PC_CORE_FFT                  */
+  int32_t exec;             /* PC_EXEC_*                                                    */
   int32_t K_q;              /* kernel companding range; 0 means K_q = S_q = Q       */
   int32_t device;           /* CUDA device ordinal, -1 = current device                    */
-  int32_t reserved[9];      /* [0]: raw-block staging 0 auto/1 on/2 off (per-block kernel);
-                               [1]: force the persistent core tile (12/14/16; tests);
-                               [2]: direct core, 0 auto (the FP64 tensor cores -- DMMA, T = 16 --
-                                    except symmetric packing with < 768 core taps and asym3 with
-                                    < 256: FMA), 1 the FP64 FMA core (any T), 2 DMMA;
-                               [3]: force consumer warps per job (1, 2, 4; diagnostics);
-                               [4]: force the FFT size N (complex points, 1024..8192; 16384 =
-                                    the 32768-point real transform of the whole block, full
-                                    precision, W_block <= 16386, 2-CTA clusters);
-                               [5]: unpack form, 0 balanced digits (C6), 1 the literal
-                                    Eqs. (11)-(15) with the u_sys guard (symmetric packing,
-                                    direct core; exact for R_max < 89,524, reading C6);
-                               [6]: tiled-kernel producers: 1 = compand/pack with integer ops
-                                    (dyadic eps; bit-identical), else FP64 ops;
-                               [7]: >= 2: cap on the tiled kernel's stage-ring slots; < 0: the
-                                    producers claim job m only once consumers hold parts of
-                                    m + reserved[7] (diagnostics);
-                               [8]: 2 = compand/pack in a prepack kernel ahead of the tiled
-                                    launch instead of its producer warps (single-chunk plans,
-                                    W_block <= 25,600); rest 0.  Packed results are bit-identical
-                                    under every setting, full precision within 1e-12 (tested). */
-  double u_sys;             /* P:153; used only by the literal paper unpack form          */
+  int32_t raw_staging;      /* per-block kernel: raw block TMA-staged 0 auto / 1 on / 2 off */
+  int32_t core_tile;        /* persistent direct core: outputs per thread, 0 auto / 12/14/16 */
+  int32_t core_variant;     /* PC_CORE_AUTO / PC_CORE_FMA / PC_CORE_DMMA                    */
+  int32_t parts_per_job;    /* persistent direct core: consumer warps per job, 0 auto / 1,2,4 */
+  int32_t fft_n;            /* FFT core: complex points N, 0 auto / 1024..8192 (real transform
+                               2N); 16384 = the 32768-point real transform of the whole block
+                               (full precision, W_block <= 16386, 2-CTA clusters)          */
+  int32_t unpack_form;      /* PC_UNPACK_BALANCED, or PC_UNPACK_LITERAL: the literal
+                               Eqs. (11)-(15) with the u_sys guard (symmetric packing, direct
+                               core; exact for R_max < 89,524, reading C6)                 */
+  int32_t pack_alu;         /* persistent core producers: 1 = compand/pack with integer ops
+                               (dyadic eps; bit-identical), 0 FP64 ops                      */
+  int32_t stage_cap;        /* >= 2: cap on the persistent kernel's stage-ring slots; < 0: the
+                               producers claim job m only once consumers hold parts of
+                               m + stage_cap; 0 automatic                                   */
+  int32_t prepack;          /* 1: compand/pack in a prepack kernel ahead of the persistent
+                               launch instead of its producer warps (single-chunk plans,
+                               W_block <= 25,600); 0 in the producer warps                  */
+  int32_t early_fill;       /* 1: a persistent launch's pipeline fill may overlap the tail of
+                               the preceding launch on the stream when that launch does not
+                               write this launch's input (host-checked); 0 off              */
+  int32_t validate_trials;  /* FFT core: worst-case operand pairs of the backend validation
+                               run by conv_plan_set_kernel, 0 = 128             */
+  double u_sys;             /* P:153; used by the literal paper unpack form                */
 } conv_opts;
 
 /* Read-only plan description (conv_plan_query). */
@@ -117,6 +131,14 @@ typedef struct conv_plan_info {
   int32_t core_tile;        /* outputs per thread of the persistent core (12, 14 or 16)      */
   int32_t fft_n;            /* FFT core: complex points N (real transform length 2N), else 0 */
   int32_t core_mma;         /* 1: the tiled core runs on the FP64 tensor cores (DMMA), else 0  */
+  int32_t backend_ok;       /* FFT core: 1 if the backend validation passed (4 x resid <= 0.5
+                               LSB), 0 if it failed (WARN plans only), -1 not run           */
+  double backend_resid;     /* FFT core: worst last-digit residual (LSB) of the validation  */
+  double u_sys_cal;         /* FFT core: calibrated u_sys = 4 x that residual x the last
+                               digit's unit (absolute); 0 for the exact direct core */
+  int32_t device;           /* CUDA device ordinal the plan's memory lives on               */
+  int32_t exec_used;        /* the kernel conv_execute runs: PC_EXEC_TILED (persistent direct
+                               core), PC_EXEC_PERBLOCK (one CTA per block), -1 the FFT core   */
 } conv_plan_info;
 
 /* Per-block decision of conv_adapt_block. */
@@ -152,22 +174,34 @@ int conv_plan_create(conv_plan** out, int64_t L, int32_t N, int32_t W_block, int
  * ||k||_inf, c_k = K_q/||k||_inf, k~ = [[c_k k]] (Eq. (2)), R_max (Eq. (3) / C3), eps
  * (Eq. (6) / C2 / C4), bound check (Table 1), packed kernel (Eq. (5) under C1, or
  * k~ for asymmetric, Eq. (8)).  Synchronizes `stream` (one-time plan cost).
- * Returns PC_E_BOUND under STRICT when R_max exceeds the bound (kernel not installed). */
+ * Returns PC_E_BOUND under STRICT when R_max exceeds the bound (kernel not installed).
+ * FFT-core plans of a packed mode then validate the backend: the plan's own
+ * FFT kernel runs on validate_trials worst-case operand windows (every sample +-1, random signs,
+ * so every packed digit is +-S_q; the installed kernel, companded to +-K_q) and its last-digit
+ * residual monitor gives the worst deviation d (LSB) from the exact integers; u_sys_cal =
+ * 4 d x the digit unit.  If 4 d > 0.5 LSB the regime (N', R_max, fft_n) is unsafe: PC_E_BACKEND
+ * under STRICT (kernel not installed), recorded (backend_ok = 0) under WARN. */
 int conv_plan_set_kernel(conv_plan* plan, const double* k_dev, void* stream);
 
 /* Run the whole hot path on an L-sample device input, writing L_out device outputs:
  * r_out (Eq. (17)) for conv, or the valid cross-correlation lags c[j] = sum_n s[j+n] q[n],
- * 0 <= j <= L-N, for xcorr (C17). */
+ * 0 <= j <= L-N, for xcorr (C17).  s_dev and r_dev must not overlap.
+ * Returns PC_OK, or (FFT core) PC_W_UNPACK_MARGIN when a completed launch of this plan saw a
+ * last-digit residual above 0.25 LSB (the kernels raise a flag in host-mapped memory; it stays
+ * raised until conv_plan_residual(reset = 1); the launch of this call is enqueued either way),
+ * or PC_E_WATCHDOG when a completed launch of this plan abandoned its work (sticky likewise). */
 int conv_execute(conv_plan* plan, const double* s_dev, double* r_dev, void* stream);
 
 /* Same as conv_execute restricted to blocks [block_begin, block_end) -- the unit of
  * multi-GPU sharding.  s_dev holds global samples [s_offset, ...) (the
- * block range plus its N'+1-sample halo); r_dev receives global outputs [r_offset, ...). */
+ * block range plus its N'+1-sample halo); r_dev receives global outputs [r_offset, ...).
+ * Returns as conv_execute. */
 int conv_execute_blocks(conv_plan* plan, const double* s_dev, int64_t s_offset, double* r_dev,
                         int64_t r_offset, int64_t block_begin, int64_t block_end, void* stream);
 
 /* n_signals independent signals of L samples (row stride s_stride doubles) through the
- * same plan; outputs row stride r_stride doubles.  One launch over all blocks. */
+ * same plan; outputs row stride r_stride doubles.  One launch over all blocks.  Returns as
+ * conv_execute. */
 int conv_execute_batch(conv_plan* plan, const double* s_dev, int64_t n_signals, int64_t s_stride,
                        double* r_dev, int64_t r_stride, void* stream);
 
@@ -175,8 +209,26 @@ int conv_execute_batch(conv_plan* plan, const double* s_dev, int64_t n_signals, 
  * conv_execute, copies L_out doubles back to r_host, and synchronizes `stream`.  Plans of
  * >= 128 blocks pipeline 15 block ranges over plan-owned copy streams (H2D of range
  * c+1, core of range c and D2H of range c-1 overlap); pinned host buffers are needed for
- * the copies to overlap.  Results are identical to conv_execute. */
+ * the copies to overlap.  Results are identical to conv_execute; returns as conv_execute (it
+ * synchronizes, so the flags include this call's own launches). */
 int conv_execute_host(conv_plan* plan, const double* s_host, double* r_host, void* stream);
+
+/* conv_execute_host restricted to blocks [block_begin, block_end) (a rank's shard, SURVEY
+ * §8(e)): s_host holds global samples [s_offset, ...) -- at least the shard's input range
+ * conv_shard_range reports -- and r_host receives global outputs (conv) / lags (xcorr)
+ * [r_offset, ...) of the shard's output range.  Same pipeline and return codes; adaptive plans
+ * need the whole range (PC_E_CONFIG otherwise). */
+int conv_execute_host_blocks(conv_plan* plan, const double* s_host, int64_t s_offset, double* r_host,
+                             int64_t r_offset, int64_t block_begin, int64_t block_end, void* stream);
+
+/* Database winner of the music-matching score (reading C17): over n candidates --
+ * candidate i = (score_dev[i], lag_dev[i], first_index + i), or, if cand_dev is non-NULL, the
+ * rows {score, lag, index} of cand_dev (n x 3 doubles, e.g. the all-gathered winners of every
+ * rank) -- the largest score, ties to the smallest index.  Writes {score, lag, index} (3 doubles,
+ * lag and index exact integers) to best_dev.  Device pointers, stream-ordered, one launch (no
+ * plan needed). */
+int conv_best_match(const double* score_dev, const int64_t* lag_dev, const double* cand_dev, int64_t n,
+                    int64_t first_index, double* best_dev, void* stream);
 
 /* Many (signal, kernel) pairs, one kernel each -- the MPEG-7 stereo-descriptor regime of §IV.C
  * (SURVEY NEXT-3): block b of one channel cross-correlated with block b of the other.
@@ -208,9 +260,13 @@ int conv_xcorr_max(conv_plan* plan, const double* db_dev, int64_t n_signals, int
 /* Parity/debug run of the whole path that also dumps, per block w (row w of each array,
  * strides from conv_plan_info; any pointer may be NULL): packed words as the core sees
  * them (Eq. (4)/(7)), packed outputs (Eq. (9)/(8)), unpacked integers of the kept range
- * (Eqs. (12)-(15)), and c_s (Eq. (2)).  r_dev as in conv_execute (may be NULL). */
+ * (Eqs. (12)-(15)), and c_s (Eq. (2)).  r_dev as in conv_execute (may be NULL).
+ * max_residual_host (may be NULL): the largest distance of a decoded last digit from its
+ * integer over all blocks (LSB; exactly 0 under the dyadic eps, C4); synchronizes `stream`
+ * when non-NULL. */
 int conv_execute_debug(conv_plan* plan, const double* s_dev, double* r_dev, double* packed_dev,
-                       double* rbar_dev, int64_t* rint_dev, double* c_s_dev, void* stream);
+                       double* rbar_dev, int64_t* rint_dev, double* c_s_dev, double* max_residual_host,
+                       void* stream);
 
 /* SNR-constrained adaptation for ADAPTIVE plans: per block, the first
  * packing of {SYM, ASYM2} whose Eq. (19) prediction at its maximum Q under its bound
@@ -219,6 +275,14 @@ int conv_execute_debug(conv_plan* plan, const double* s_dev, double* r_dev, doub
  * Synchronizes `stream` only when out_host is non-NULL (otherwise stream-ordered). */
 int conv_adapt_block(conv_plan* plan, const double* s_dev, double snr_floor_db,
                      double calib_offset_db, conv_block_decision* out_host, void* stream);
+
+/* conv_adapt_block on a rank's blocks [block_begin, block_end): s_dev holds global
+ * samples [s_offset, ...) (the shard's input range); out_host receives block_end - block_begin
+ * decisions.  The next conv_execute_blocks over exactly this range runs one persistent launch per
+ * packing; executes of blocks outside the decided range return PC_E_STATE. */
+int conv_adapt_blocks(conv_plan* plan, const double* s_dev, int64_t s_offset, int64_t block_begin,
+                      int64_t block_end, double snr_floor_db, double calib_offset_db,
+                      conv_block_decision* out_host, void* stream);
 
 /* Single-point calibration of the Eq. (19) SNR model (Fig. 5: "calibrated via a single
  * measurement at the coarsest quantization (S_q = K_q = 8)"; reading C18).  Runs the plan's
@@ -255,9 +319,9 @@ int conv_shard_range(int64_t L, int32_t N, int32_t W_block, int32_t mode, int32_
  * hand-written FP64 FFT, so the packed outputs are approximate and exact integers are
  * recovered only while the error stays below half an LSB.  The kernels keep the largest
  * last-digit residual (in LSB) seen since the last reset; this call copies it to
- * *resid_host (synchronizes `stream`), resets it if `reset`, and returns
- * PC_W_UNPACK_MARGIN if it exceeded 0.25 LSB (SURVEY §5 unpack-residual monitor).
- * Direct-core plans are exact: *resid_host = 0, PC_OK. */
+ * *resid_host (synchronizes `stream`), resets it (and the margin flag conv_execute reports)
+ * if `reset`, and returns PC_W_UNPACK_MARGIN if it exceeded 0.25 LSB (SURVEY §5 unpack-residual
+ * monitor).  Direct-core plans are exact: *resid_host = 0, PC_OK. */
 int conv_plan_residual(conv_plan* plan, double* resid_host, int32_t reset, void* stream);
 
 int conv_plan_query(const conv_plan* plan, conv_plan_info* info);

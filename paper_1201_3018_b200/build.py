@@ -13,7 +13,8 @@ OUT = os.path.join(HERE, "libpackedconv.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 EXTRA = os.environ.get("PC_NVCC_EXTRA", "").split()
 FLAGS = EXTRA + ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v", "-cudart", "static"]
+         "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
+OBJ_DIR = os.path.join(HERE, "build")
 
 
 def up_to_date():
@@ -23,16 +24,33 @@ def up_to_date():
     return all(os.path.getmtime(d) <= t for d in DEPS)
 
 
+def _compile(src):
+    obj = os.path.join(OBJ_DIR, os.path.basename(src)[:-3] + ".o")
+    res = subprocess.run([NVCC] + FLAGS + ["-c", "-o", obj, src], capture_output=True, text=True)
+    return obj, res
+
+
 def build_library(force=False, verbose=False):
+    """nvcc -c of every source in parallel (one process each), then one shared-library link
+    with the static CUDA runtime."""
     if not force and up_to_date():
         return OUT
-    cmd = [NVCC] + FLAGS + ["-o", OUT] + SOURCES
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    from concurrent.futures import ThreadPoolExecutor
+    os.makedirs(OBJ_DIR, exist_ok=True)
+    with ThreadPoolExecutor(len(SOURCES)) as ex:
+        results = list(ex.map(_compile, SOURCES))
+    for obj, res in results:
+        if res.returncode != 0:
+            sys.stderr.write(res.stdout + res.stderr)
+            raise RuntimeError("nvcc failed: " + obj)
+        if verbose:
+            sys.stderr.write(res.stderr)
+    link = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static", "-o", OUT] + \
+        [obj for obj, _ in results]
+    res = subprocess.run(link, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed")
-    if verbose:
-        sys.stderr.write(res.stderr)
+        raise RuntimeError("nvcc link failed")
     return OUT
 
 

@@ -61,6 +61,7 @@ struct conv_plan {
   int* d_lists = nullptr;              // adaptive: per-packing ascending block lists [4][P]
   int* d_counts = nullptr;             // adaptive: their lengths [4]
   int adapt_ready = 0;
+  long long adapt_b0 = 0, adapt_b1 = 0;  // the block range the decisions (and lists) cover
   // host end-to-end staging
   double* d_in = nullptr;
   double* d_out = nullptr;
@@ -90,6 +91,12 @@ struct conv_plan {
   double2* d_tw2 = nullptr;            // exp(-2 pi i k / 2N), k <= N
   double2* d_H = nullptr;              // spectrum of the core taps, k <= N
   double* d_resid = nullptr;           // max last-digit residual (LSB)
+  int backend_ok = -1;                 // FFT backend validation: 1 pass, 0 fail (WARN), -1 not run
+  double backend_resid = 0.0, u_sys_cal = 0.0;
+  // flags the kernels raise in host-mapped pinned memory (pc::kStatusMargin / kStatusWatchdog)
+  int* h_status = nullptr;             // host view
+  int* d_status = nullptr;             // device view of the same memory
+  double* d_dbg_resid = nullptr;       // conv_execute_debug: max last-digit residual
 };
 
 namespace {
@@ -200,7 +207,7 @@ bool launch_shape(const conv_plan* p, const int* packs, int npacks, Shape* sh) {
   const size_t staged = base + (size_t)p->W_block * 8;
   const int by_regs = 65536 / (t * 64);
   auto ctas = [&](size_t sm) { return (int)(kSmemPerSM / (sm + 1024)); };
-  int mode = p->opts.reserved[0];   // 0 auto, 1 force staging, 2 never stage
+  int mode = p->opts.raw_staging;   // 0 auto, 1 force staging, 2 never stage
   bool stage = staged <= kMaxSmem && (mode == 1 || (mode == 0 && ctas(staged) >= (by_regs < ctas(base) ? by_regs : ctas(base))));
   if (stage) {
     sh->stage_raw = 1;
@@ -227,7 +234,7 @@ bool tiled_shape(const conv_plan* p, int packing, TShape* sh, bool taps_per_sign
   int mmax, mtyp;
   core_sizes(p, packing, &mmax, &mtyp);
   const int K = core_taps(p, packing);
-  const int force = p->opts.reserved[1];
+  const int force = p->opts.core_tile;
   // core: the FP64 tensor cores (DMMA, T = 16) unless the FMA core or another tile is forced;
   // auto keeps the FMA core for symmetric packing with a short core (about N/2 taps): there the
   // three-digit epilogue weighs as much as the core and the DMMA interference slows it (cfg2,
@@ -235,7 +242,7 @@ bool tiled_shape(const conv_plan* p, int packing, TShape* sh, bool taps_per_sign
   // taps on DMMA wins (1025: 429 vs 438 us, cfg4's 4097: 143.4 vs 160.0 ms); likewise asymmetric
   // M = 3 below 256 taps (129 taps: FMA 49.9
   // vs 55.1 us; 257: equal; 513: DMMA 82.6 vs 95); asym2 and full precision: DMMA at every length
-  const int core = p->opts.reserved[2];
+  const int core = p->opts.core_variant;
   const bool long_core = packing == PC_PACK_SYM ? K >= 768 : (packing == PC_PACK_ASYM3 ? K >= 256 : true);
   sh->mma = (core == 2 || (core == 0 && long_core)) && (force == 0 || force == 16);
   double best = -1.0;
@@ -244,7 +251,7 @@ bool tiled_shape(const conv_plan* p, int packing, TShape* sh, bool taps_per_sign
     if (sh->mma && T != 16) continue;
     const double speed = T == 16 ? 1.0 : (T == 14 ? 0.96 : 0.92);   // core-loop calibration (profiles)
     for (int npart : {4, 2, 1}) {
-      if (p->opts.reserved[3] > 0 && npart != p->opts.reserved[3]) continue;   // diagnostics: force G
+      if (p->opts.parts_per_job > 0 && npart != p->opts.parts_per_job) continue;   // diagnostics: force G
       const int G = 32 * npart;
       const long long groups = (mtyp + T - 1) / T;
       const long long tiles = (groups + G - 1) / G;
@@ -287,7 +294,7 @@ bool tiled_shape(const conv_plan* p, int packing, TShape* sh, bool taps_per_sign
   if (fixed + 2 * stage > kMaxSmem) return false;
   sh->nstages = (int)((kMaxSmem - fixed) / stage);
   if (sh->nstages > pc::kTiledMaxStages) sh->nstages = pc::kTiledMaxStages;
-  if (p->opts.reserved[7] >= 2 && sh->nstages > p->opts.reserved[7]) sh->nstages = p->opts.reserved[7];   // diagnostics
+  if (p->opts.stage_cap >= 2 && sh->nstages > p->opts.stage_cap) sh->nstages = p->opts.stage_cap;   // diagnostics
   sh->smem = fixed + (size_t)sh->nstages * stage;
   if (sh->smem < kMaxSmem / 2 + 4096) sh->smem = kMaxSmem / 2 + 4096;   // one CTA per SM
   return true;
@@ -331,7 +338,7 @@ int choose_fft_N(const conv_plan* p, int packing) {
   int mmax, mtyp;
   core_sizes(p, packing, &mmax, &mtyp);
   const int K = core_taps(p, packing);
-  const int force = p->opts.reserved[4];            // diagnostics: complex points N
+  const int force = p->opts.fft_n;                  // complex points N (0 = cost model)
   if (force == 1024 || force == 2048 || force == 4096 || force == 8192) return 2 * force - K >= 1 ? force : 0;
   // 32768-point real transform of the whole block (cfg3's configured full-precision core):
   // full precision, windows of at most 16384 real words (2-CTA cluster kernel)
@@ -397,7 +404,7 @@ bool small_core_plan(const conv_plan* p, const int* packs, int np) {
   return true;
 }
 bool forced_tiled(const conv_plan* p) {
-  return p->opts.reserved[1] != 0 || p->opts.reserved[3] != 0 || p->opts.reserved[5] == 1;
+  return p->opts.core_tile != 0 || p->opts.parts_per_job != 0 || p->opts.unpack_form == PC_UNPACK_LITERAL;
 }
 bool uses_tiled(const conv_plan* p) {
   if (p->opts.core != PC_CORE_DIRECT || p->packing == PC_PACK_ADAPTIVE) return false;
@@ -411,21 +418,20 @@ bool uses_tiled(const conv_plan* p) {
   return !(small_core_plan(p, packs, np) && launch_shape(p, packs, np, &sh));
 }
 
-// Tiled launches overlap (programmatic dependent launch): with PC_EARLY_FILL=1 in the environment
-// the next launch's pipeline fill may run before the preceding launch on the stream has finished
-// (early_fill) as long as it does not read what that launch writes.  Opt-in: measured no faster at
-// cfg2 (102.7 vs 102.1 us per step; the step is bound by each SM's own 8 jobs), and a foreign
-// kernel with its own programmatic trigger between two of ours could not be seen by this check.  Per (device, stream): the output address range of the last tiled
-// launch.  A kernel of anyone else in between has no programmatic trigger, so the tiled launch
-// after it starts only once it has completed -- the stale record can only make this check
-// conservative.
+// Tiled launches overlap (programmatic dependent launch): with opts.early_fill = 1 the next
+// launch's pipeline fill may run before the preceding launch on the stream has finished as long
+// as it does not read what that launch writes.  Opt-in: measured no faster at cfg2 (102.7 vs
+// 102.1 us per step; the step is bound by each SM's own 8 jobs), and a foreign kernel with its
+// own programmatic trigger between two of ours could not be seen by this check.  Per (device,
+// stream): the output address range of the last tiled launch.  A kernel of anyone else in
+// between has no programmatic trigger, so the tiled launch after it starts only once it has
+// completed -- the stale record can only make this check conservative.
 std::mutex g_streams_mu;
 std::map<std::pair<int, cudaStream_t>, std::pair<uintptr_t, uintptr_t>> g_last_out;
-bool early_fill_ok(int dev, cudaStream_t st, uintptr_t in_lo, uintptr_t in_hi) {
-  const char* ev = std::getenv("PC_EARLY_FILL");
-  if (!ev || ev[0] != '1') return false;
+bool early_fill_ok(const conv_plan* p, cudaStream_t st, uintptr_t in_lo, uintptr_t in_hi) {
+  if (p->opts.early_fill != 1) return false;
   std::lock_guard<std::mutex> lk(g_streams_mu);
-  auto it = g_last_out.find({dev, st});
+  auto it = g_last_out.find({p->device, st});
   return it == g_last_out.end() || in_hi <= it->second.first || it->second.second <= in_lo;
 }
 void record_out(int dev, cudaStream_t st, uintptr_t lo, uintptr_t hi) {
@@ -438,7 +444,9 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
               unsigned long long* timing = nullptr, int* grid_out = nullptr, double* xc_val = nullptr,
               long long* xc_lag = nullptr, bool pairs = false) {
   if (!p->kernel_set) return PC_E_STATE;
-  if (p->packing == PC_PACK_ADAPTIVE && !p->adapt_ready) return PC_E_STATE;
+  if (p->packing == PC_PACK_ADAPTIVE &&
+      (!p->adapt_ready || n_sig != 1 || b0 < p->adapt_b0 || b0 + nblk > p->adapt_b1))
+    return PC_E_STATE;                                  // execute only blocks with decisions
   if (nblk <= 0 || n_sig <= 0) return PC_OK;
   int packs[4];
   const int np = plan_packs(p, packs);
@@ -459,15 +467,16 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
   e.reg_path = per_block_ok ? sh.reg_path : 0;
   for (int i = 0; i < np; ++i) {
     fill_modep(p->ms[packs[i]], packs[i], &e.mp[packs[i]]);
-    if (p->opts.reserved[6] != 1) e.mp[packs[i]].alu_pack = 0;   // integer packing only when asked
+    if (p->opts.pack_alu != 1) e.mp[packs[i]].alu_pack = 0;   // integer packing only when asked
   }
-  if (p->opts.reserved[5] == 1) {                    // literal Eqs. (11)-(15) (SYM, tiled kernel)
+  if (p->opts.unpack_form == PC_UNPACK_LITERAL) {   // literal Eqs. (11)-(15) (SYM, tiled kernel)
     pc::ModeP& ms = e.mp[PC_PACK_SYM];
     ms.paper_unpack = 1;
     ms.R_safe = ms.R * (ms.eps + 1.0 + ms.eps_inv) + p->opts.u_sys * ms.eps_inv;   // P:103, oracle order
   }
   e.dec_pack = p->packing == PC_PACK_ADAPTIVE ? p->d_dec_pack : nullptr;
   e.nsig = n_sig;
+  e.status = p->d_status;
   const int launch_pack = p->packing == PC_PACK_ADAPTIVE ? -1 : p->packing;
   if (p->opts.core == PC_CORE_FFT) {
     if (dbg) return PC_E_CONFIG;                      // per-step dumps exist for the direct core
@@ -496,8 +505,8 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
   if (!dbg && !xc_val && !pairs && small_core && !forced && per_block_ok && p->opts.exec == PC_EXEC_FUSED)
     return cuda_status(pc::launch_fused(launch_pack, make_geo(p), e, nblk * n_sig, sh.threads, sh.smem, st));
   const bool tiled_ok = p->opts.exec == PC_EXEC_FUSED || p->opts.exec == PC_EXEC_TILED;
-  if (!dbg && p->packing == PC_PACK_ADAPTIVE && tiled_ok && n_sig == 1 && b0 == 0 &&
-      nblk == p->P && p->d_lists) {
+  if (!dbg && p->packing == PC_PACK_ADAPTIVE && tiled_ok && n_sig == 1 && b0 == p->adapt_b0 &&
+      b0 + nblk == p->adapt_b1 && p->d_lists) {
     // a8 -> a2..a7: one tiled launch per packing over its block list (pc_adapt_lists)
     TShape sh3[3];
     const int order[3] = {PC_PACK_ASYM2, PC_PACK_SYM, PC_PACK_FULL};
@@ -521,7 +530,7 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
         el.rows_s = t.rows_s;
         el.tiles0 = t.tiles0;
         el.tiles1 = t.tiles1;
-        el.jobs_per_sig = t.tiles0 + (p->P - 1) * t.tiles1;   // upper bound: grid size only
+        el.jobs_per_sig = (b0 == 0 ? t.tiles0 + (nblk - 1) * t.tiles1 : nblk * t.tiles1);   // upper bound: grid size
         el.mp[pk].K_pad = t.K_pad;
         int grid = 0;
         cudaError_t err = pc::launch_tiled(pk, t.T, t.mma, make_geo(p), el, el.jobs_per_sig, t.threads, t.smem, st, &grid);
@@ -541,7 +550,7 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
     e.sm_ctr = p->d_counter + (p->ctr_flip ? pc::kCtrDone + 1 : 0);   // alternate: see early_fill
     p->ctr_flip ^= 1;
     e.dbg_timing = timing;
-    e.lookahead = p->opts.reserved[7] < 0 ? -p->opts.reserved[7] : 0;   // diagnostics
+    e.lookahead = p->opts.stage_cap < 0 ? -p->opts.stage_cap : 0;   // diagnostics
     e.xc_val = xc_val;
     e.xc_lag = xc_lag;
     e.G = ts.G;
@@ -555,10 +564,10 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
     e.jobs_per_sig = (b0 == 0) ? ts.tiles0 + (nblk - 1) * ts.tiles1 : nblk * ts.tiles1;
     e.mp[p->packing].K_pad = ts.K_pad;
     const long long njobs = e.jobs_per_sig * n_sig;
-    // a2-a4 ahead of the DMMA-core launch (single-chunk packed plans, reserved[8] = 2): measured
+    // a2-a4 ahead of the DMMA-core launch (single-chunk packed plans, opts.prepack = 1): measured
     // slower than the fused producers at cfg2 (the separate pass costs ~26 us, the persistent
     // kernel's tail does not shrink), so off by default
-    if (ts.nchunks == 1 && p->packing != PC_PACK_FULL && p->opts.reserved[8] == 2 &&
+    if (ts.nchunks == 1 && p->packing != PC_PACK_FULL && p->opts.prepack == 1 &&
         (long long)p->W_block * 8 <= 200 * 1024) {
       const long long stride = ((long long)(ts.T + (ts.mma ? 4 : 1)) * ts.rows_s + 1) & ~1LL;   // stage_x of pc_tiled_kernel
       const long long need = njobs * stride + njobs;
@@ -577,7 +586,7 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
     // every address this launch may read as input / write as output (rows sig < n_sig)
     const uintptr_t in_lo = (uintptr_t)(s - s_off), in_hi = (uintptr_t)(s - s_off + (n_sig - 1) * s_stride + p->L);
     const uintptr_t out_lo = (uintptr_t)(r - r_off - p->N), out_hi = (uintptr_t)(r - r_off + (n_sig - 1) * r_stride + p->L + 2 * p->N);
-    e.early_fill = !timing && !e.pre_win && early_fill_ok(p->device, st, in_lo, in_hi);
+    e.early_fill = !timing && !e.pre_win && early_fill_ok(p, st, in_lo, in_hi);
     e.early_claim = 1;                                 // claims touch only this launch's queue array
     int grid = 0;
     cudaError_t err = pc::launch_tiled(p->packing, ts.T, ts.mma, make_geo(p), e, njobs, ts.threads, ts.smem, st, &grid);
@@ -589,6 +598,15 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
   if (pairs || xc_val) return PC_E_CONFIG;  // per-pair taps / fused scores exist only in the tiled kernel
   if (!per_block_ok) return PC_E_CONFIG;   // debug dumps / adaptive need the per-block kernel
   return cuda_status(pc::launch_fused(launch_pack, make_geo(p), e, nblk * n_sig, sh.threads, sh.smem, st));
+}
+
+// Status of an enqueue that succeeded: the sticky flags completed launches of the plan raised in
+// host-mapped memory (read without synchronizing).
+int plan_flags(const conv_plan* p, int rc) {
+  if (rc != PC_OK || !p->h_status) return rc;
+  if (reinterpret_cast<volatile int*>(p->h_status)[pc::kStatusWatchdog]) return PC_E_WATCHDOG;
+  if (reinterpret_cast<volatile int*>(p->h_status)[pc::kStatusMargin]) return PC_W_UNPACK_MARGIN;
+  return PC_OK;
 }
 
 }  // namespace
@@ -618,6 +636,7 @@ const char* conv_status_string(int s) {
     case PC_E_CUDA: return "CUDA error";
     case PC_W_UNPACK_MARGIN: return "unpack margin warning";
     case PC_E_STATE: return "invalid call order";
+    case PC_E_WATCHDOG: return "kernel watchdog timeout (launch abandoned)";
   }
   return "unknown status";
 }
@@ -666,6 +685,11 @@ int conv_plan_create(conv_plan** out, int64_t L, int32_t N, int32_t W_block, int
   if (e == cudaSuccess) e = cudaMalloc(&p->d_scal, sizeof(double) * 4);
   if (e == cudaSuccess) e = cudaMalloc(&p->d_counter, 2 * (pc::kCtrDone + 1) * sizeof(unsigned));   // two arrays
   if (e == cudaSuccess) e = cudaMemset(p->d_counter, 0, 2 * (pc::kCtrDone + 1) * sizeof(unsigned));
+  if (e == cudaSuccess) e = cudaHostAlloc(&p->h_status, 4 * sizeof(int), cudaHostAllocMapped);
+  if (e == cudaSuccess) {
+    std::memset(p->h_status, 0, 4 * sizeof(int));
+    e = cudaHostGetDevicePointer(&p->d_status, p->h_status, 0);
+  }
   if (e != cudaSuccess) {
     conv_plan_destroy(p);
     return PC_E_CUDA;
@@ -759,6 +783,8 @@ void conv_plan_destroy(conv_plan* p) {
   cudaFree(p->d_tw2);
   cudaFree(p->d_H);
   cudaFree(p->d_resid);
+  cudaFree(p->d_dbg_resid);
+  if (p->h_status) cudaFreeHost(p->h_status);
   delete p;
 }
 
@@ -856,6 +882,50 @@ int max_q(conv_plan* p, int packing, const double* k_dev, cudaStream_t st, int* 
   return PC_OK;
 }
 
+// Backend validation of an FFT-core plan (P:103, P:153 u_sys): the plan's own
+// FFT kernel on worst-case operand windows -- every sample +-1 with random signs, so every packed
+// digit is +-S_q, convolved with the installed kernel k~ -- over the first blocks of the plan's
+// geometry until `trials` jobs (transform windows) ran; the kernels' last-digit residual monitor
+// gives the worst deviation d (LSB) from the exact integers.  u_sys_cal = 4 d x the unit of the
+// last digit in the packed word (eps for symmetric and asym2, eps^2 for asym3).
+int validate_fft_backend(conv_plan* p, cudaStream_t st) {
+  FShape fs;
+  if (!fft_shape(p, p->packing, p->fft_N, &fs)) return PC_E_CONFIG;
+  const long long trials = p->opts.validate_trials > 0 ? p->opts.validate_trials : 128;
+  long long nb = 1, jobs = fs.parts0;
+  while (jobs < trials && nb < p->P) {
+    ++nb;
+    jobs += fs.parts1;
+  }
+  long long in_len = (nb - 1 == 0 ? 0 : (nb - 1) * (long long)p->W - 2) + p->W_block;
+  if (in_len > p->L) in_len = p->L;
+  const long long out_len = (long long)p->Np - 1 + nb * (long long)p->W + p->N;
+  double *x = nullptr, *y = nullptr;
+  cudaError_t e = cudaMalloc(&x, sizeof(double) * in_len);
+  if (e == cudaSuccess) e = cudaMalloc(&y, sizeof(double) * out_len);
+  if (e == cudaSuccess) e = pc::launch_fill_pm1(x, in_len, 0x5eed0000ull + (unsigned long long)p->Np, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(p->d_resid, 0, sizeof(double), st);
+  int rc = e == cudaSuccess ? PC_OK : PC_E_CUDA;
+  if (!rc) rc = run_exec(p, x, 0, 0, y, 0, 0, 0, nb, 1, nullptr, st);
+  double d = 0.0;
+  if (!rc) {
+    e = cudaMemcpyAsync(&d, p->d_resid, sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(p->d_resid, 0, sizeof(double), st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = PC_E_CUDA;
+  }
+  cudaFree(x);
+  cudaFree(y);
+  if (rc) return rc;
+  reinterpret_cast<volatile int*>(p->h_status)[pc::kStatusMargin] = 0;   // the validation's own flag
+  const ModeState& m = p->ms[p->packing];
+  const int last = p->packing == PC_PACK_ASYM3 ? 2 : 1;                  // power of eps of the last digit
+  p->backend_resid = d;
+  p->u_sys_cal = 4.0 * d * std::pow(m.eps, (double)last);
+  p->backend_ok = 4.0 * d <= 0.5 ? 1 : 0;
+  return PC_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -905,6 +975,15 @@ int conv_plan_set_kernel(conv_plan* p, const double* k_dev, void* stream) {
       cudaError_t e = pc::launch_fft_spectrum(p->fft_N, m.kr, m.K, p->d_tw, p->d_tw2, p->d_H, st);
       if (e == cudaSuccess) e = cudaStreamSynchronize(st);
       if (e != cudaSuccess) return PC_E_CUDA;
+      p->backend_ok = -1;
+      p->backend_resid = p->u_sys_cal = 0.0;
+      if (p->packing != PC_PACK_FULL) {                // validate the FFT regime
+        p->kernel_set = 1;                             // (run_exec needs an installed kernel)
+        rc = validate_fft_backend(p, st);
+        p->kernel_set = 0;
+        if (rc) return rc;
+        if (!p->backend_ok && p->opts.bound_policy == PC_BOUND_STRICT) return PC_E_BACKEND;
+      }
     }
   }
   p->kernel_set = 1;
@@ -914,7 +993,7 @@ int conv_plan_set_kernel(conv_plan* p, const double* k_dev, void* stream) {
 int conv_execute(conv_plan* p, const double* s, double* r, void* stream) {
   if (!p || !s || !r) return PC_E_CONFIG;
   if (cudaSetDevice(p->device) != cudaSuccess) return PC_E_CUDA;
-  return run_exec(p, s, 0, 0, r, 0, 0, 0, p->P, 1, nullptr, (cudaStream_t)stream);
+  return plan_flags(p, run_exec(p, s, 0, 0, r, 0, 0, 0, p->P, 1, nullptr, (cudaStream_t)stream));
 }
 
 int conv_execute_blocks(conv_plan* p, const double* s, int64_t s_offset, double* r, int64_t r_offset,
@@ -922,8 +1001,8 @@ int conv_execute_blocks(conv_plan* p, const double* s, int64_t s_offset, double*
   if (!p || !s || !r) return PC_E_CONFIG;
   if (block_begin < 0 || block_end > p->P || block_begin > block_end) return PC_E_CONFIG;
   if (cudaSetDevice(p->device) != cudaSuccess) return PC_E_CUDA;
-  return run_exec(p, s, s_offset, 0, r, r_offset, 0, block_begin, block_end - block_begin, 1, nullptr,
-                   (cudaStream_t)stream);
+  return plan_flags(p, run_exec(p, s, s_offset, 0, r, r_offset, 0, block_begin, block_end - block_begin, 1,
+                                nullptr, (cudaStream_t)stream));
 }
 
 int conv_execute_batch(conv_plan* p, const double* s, int64_t n_signals, int64_t s_stride, double* r,
@@ -931,56 +1010,70 @@ int conv_execute_batch(conv_plan* p, const double* s, int64_t n_signals, int64_t
   if (!p || !s || !r || n_signals < 0) return PC_E_CONFIG;
   if (p->packing == PC_PACK_ADAPTIVE && n_signals > 1) return PC_E_CONFIG;
   if (cudaSetDevice(p->device) != cudaSuccess) return PC_E_CUDA;
-  return run_exec(p, s, 0, s_stride, r, 0, r_stride, 0, p->P, n_signals, nullptr, (cudaStream_t)stream);
+  return plan_flags(p, run_exec(p, s, 0, s_stride, r, 0, r_stride, 0, p->P, n_signals, nullptr, (cudaStream_t)stream));
 }
 
 int conv_execute_host(conv_plan* p, const double* s_host, double* r_host, void* stream) {
+  if (!p) return PC_E_CONFIG;
+  return conv_execute_host_blocks(p, s_host, 0, r_host, 0, 0, p->P, stream);
+}
+
+int conv_execute_host_blocks(conv_plan* p, const double* s_host, int64_t s_offset, double* r_host, int64_t r_offset,
+                             int64_t B0, int64_t B1, void* stream) {
   if (!p || !s_host || !r_host) return PC_E_CONFIG;
+  if (B0 < 0 || B1 > p->P || B0 > B1) return PC_E_CONFIG;
   if (cudaSetDevice(p->device) != cudaSuccess) return PC_E_CUDA;
+  if (B0 == B1) return PC_OK;
+  if (p->packing == PC_PACK_ADAPTIVE && (B0 != 0 || B1 != p->P)) return PC_E_CONFIG;   // decisions: whole input
   cudaStream_t st = (cudaStream_t)stream;
   const long long L_out = p->mode == PC_MODE_XCORR ? p->L - p->N + 1 : p->L + p->N - 1;
+  // device buffers addressed by global sample / output index (a shard uses its own range)
   if (!p->d_in && cudaMalloc(&p->d_in, sizeof(double) * p->L) != cudaSuccess) return PC_E_CUDA;
   if (!p->d_out && cudaMalloc(&p->d_out, sizeof(double) * L_out) != cudaSuccess) return PC_E_CUDA;
-  // Adaptive plans (decisions belong to one device input) and small plans: one pass.
+  // input read by blocks [B0, b1) and outputs written by them (reading C7, Eq. (17)), as
+  // conv_shard_range
+  const long long W = p->W, Wb = p->W_block, Np = p->Np;
+  auto in_end_of = [&](long long b1) {
+    const long long last = b1 - 1;
+    const long long e = (last == 0 ? 0 : last * W - 2) + Wb;
+    return e < p->L ? e : p->L;
+  };
+  auto out_end_of = [&](long long b1) {
+    long long o = (b1 == p->P) ? p->L + p->N - 1 : Np - 1 + b1 * W;
+    if (o > p->L + p->N - 1) o = p->L + p->N - 1;
+    if (p->mode == PC_MODE_XCORR) {                                   // lag j = gg - (N-1)
+      const long long lo = p->N - 1, hi = p->L;
+      o = (o < lo ? lo : (o > hi ? hi : o)) - lo;
+    }
+    return o;
+  };
+  const long long in_begin = B0 == 0 ? 0 : B0 * W - 2;
+  const long long out_begin = B0 == 0 ? 0 : out_end_of(B0);
+  // Adaptive plans (decisions belong to one device input) and small ranges: one pass.
   // Chunk weights: small first and last ranges shorten the pipeline ramp (the first H2D and
   // the last D2H are not overlapped).  (Zero-copy was measured and dropped: the tiled kernel
   // reading pinned input over PCIe took 2.1 ms at cfg2 -- the peak and packing passes read each
   // sample twice over the link -- and storing outputs straight to pinned memory 1.07-1.36 ms,
   // against 1.04 ms for this copy pipeline; the link's duplex floor is 0.71 ms.)
   // (15 ranges 1:1:2:..:2:1:1 measured 0.98-1.00 ms at cfg2 against 1.04-1.05 for 1:2:4:4:4:4:4:2:1
-  // and 1.01-1.02 for 16 equal ranges; PC_HOST_WEIGHTS="w0,w1,..." overrides, diagnostics)
+  // and 1.01-1.02 for 16 equal ranges)
   static const int kW[15] = {1, 1, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2, 1, 1};
-  int nchunk = (p->packing == PC_PACK_ADAPTIVE || p->P < 128) ? 1 : 15;
-  long long cum[33] = {0};
+  const int nchunk = (p->packing == PC_PACK_ADAPTIVE || B1 - B0 < 128) ? 1 : 15;
+  long long cum[16] = {0};
   for (int i = 0; i < 15; ++i) cum[i + 1] = cum[i] + kW[i];
-  if (const char* ev = std::getenv("PC_HOST_CHUNKS")) {         // diagnostics: n equal ranges
-    const int n = std::atoi(ev);
-    if (n >= 1 && n <= 16 && nchunk > 1) {            // (16 event pairs)
-      nchunk = n;
-      for (int i = 0; i <= n; ++i) cum[i] = i;
-    }
-  }
-  if (const char* ev = std::getenv("PC_HOST_WEIGHTS")) {        // diagnostics: "w0,w1,..." (<= 16)
-    int n = 0;
-    long long acc = 0;
-    for (const char* q = ev; *q && n < 16 && nchunk > 1;) {
-      const long long w = std::atoll(q);
-      if (w <= 0) break;
-      acc += w;
-      cum[++n] = acc;
-      while (*q && *q != ',') ++q;
-      if (*q == ',') ++q;
-    }
-    if (n >= 1 && nchunk > 1) nchunk = n;
-  }
+  const long long nb = B1 - B0;
   if (nchunk <= 1) {
-    if (cudaMemcpyAsync(p->d_in, s_host, sizeof(double) * p->L, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    const long long i1 = in_end_of(B1), o1 = out_end_of(B1);
+    if (cudaMemcpyAsync(p->d_in + in_begin, s_host + (in_begin - s_offset), sizeof(double) * (i1 - in_begin),
+                        cudaMemcpyHostToDevice, st) != cudaSuccess)
       return PC_E_CUDA;
-    int rc = run_exec(p, p->d_in, 0, 0, p->d_out, 0, 0, 0, p->P, 1, nullptr, st);
+    int rc = run_exec(p, p->d_in, 0, 0, p->d_out, 0, 0, B0, nb, 1, nullptr, st);
     if (rc) return rc;
-    if (cudaMemcpyAsync(r_host, p->d_out, sizeof(double) * L_out, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    if (o1 > out_begin && cudaMemcpyAsync(r_host + (out_begin - r_offset), p->d_out + out_begin,
+                                          sizeof(double) * (o1 - out_begin), cudaMemcpyDeviceToHost,
+                                          st) != cudaSuccess)
       return PC_E_CUDA;
-    return cuda_status(cudaStreamSynchronize(st));
+    return plan_flags(p, cuda_status(cudaStreamSynchronize(st)));
   }
   // Pipeline over block ranges: the H2D of chunk c+1, the core of chunk c and the D2H of
   // chunk c-1 overlap (two copy engines + the SMs).  Each input sample and each output is
@@ -998,25 +1091,13 @@ int conv_execute_host(conv_plan* p, const double* s_host, double* r_host, void* 
   if (e == cudaSuccess) e = cudaStreamWaitEvent(p->st_h2d, p->ev_out, 0);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(p->st_d2h, p->ev_out, 0);
   if (e != cudaSuccess) return PC_E_CUDA;
-  const long long W = p->W, Wb = p->W_block, Np = p->Np;
-  long long in_done = 0, out_done = 0;
+  long long in_done = in_begin, out_done = out_begin;
   for (int c = 0; c < nchunk; ++c) {
-    const long long b0 = p->P * cum[c] / cum[nchunk], b1 = p->P * cum[c + 1] / cum[nchunk];
+    const long long b0 = B0 + nb * cum[c] / cum[nchunk], b1 = B0 + nb * cum[c + 1] / cum[nchunk];
     if (b1 <= b0) continue;
-    const long long last = b1 - 1;
-    long long in_end = (last == 0 ? 0 : last * W - 2) + Wb;            // block `last` reads up to here
-    if (in_end > p->L) in_end = p->L;
-    if (c == nchunk - 1) in_end = p->L;
-    long long out_end = (b1 == p->P) ? p->L + p->N - 1 : Np - 1 + b1 * W;   // conv outputs of blocks < b1
-    if (p->mode == PC_MODE_XCORR) {
-      out_end -= p->N - 1;                                              // lags j = gg - (N-1)
-      if (out_end > L_out) out_end = L_out;
-      if (out_end < 0) out_end = 0;
-    } else if (out_end > L_out) {
-      out_end = L_out;
-    }
+    const long long in_end = in_end_of(b1), out_end = out_end_of(b1);
     if (in_end > in_done) {
-      e = cudaMemcpyAsync(p->d_in + in_done, s_host + in_done, sizeof(double) * (in_end - in_done),
+      e = cudaMemcpyAsync(p->d_in + in_done, s_host + (in_done - s_offset), sizeof(double) * (in_end - in_done),
                           cudaMemcpyHostToDevice, p->st_h2d);
       if (e != cudaSuccess) return PC_E_CUDA;
       in_done = in_end;
@@ -1028,22 +1109,27 @@ int conv_execute_host(conv_plan* p, const double* s_host, double* r_host, void* 
     if ((e = cudaEventRecord(p->ev_done[c], st)) != cudaSuccess) return PC_E_CUDA;
     if ((e = cudaStreamWaitEvent(p->st_d2h, p->ev_done[c], 0)) != cudaSuccess) return PC_E_CUDA;
     if (out_end > out_done) {
-      e = cudaMemcpyAsync(r_host + out_done, p->d_out + out_done, sizeof(double) * (out_end - out_done),
+      e = cudaMemcpyAsync(r_host + (out_done - r_offset), p->d_out + out_done, sizeof(double) * (out_end - out_done),
                           cudaMemcpyDeviceToHost, p->st_d2h);
       if (e != cudaSuccess) return PC_E_CUDA;
       out_done = out_end;
     }
   }
-  if (out_done != L_out) return PC_E_CONFIG;   // geometry bug guard
+  if (out_done != out_end_of(B1)) return PC_E_CONFIG;   // geometry bug guard
   if ((e = cudaEventRecord(p->ev_out, p->st_d2h)) != cudaSuccess) return PC_E_CUDA;
   if ((e = cudaStreamWaitEvent(st, p->ev_out, 0)) != cudaSuccess) return PC_E_CUDA;
-  return cuda_status(cudaStreamSynchronize(st));
+  return plan_flags(p, cuda_status(cudaStreamSynchronize(st)));
 }
 
 int conv_execute_debug(conv_plan* p, const double* s, double* r, double* packed, double* rbar, int64_t* rint,
-                       double* c_s, void* stream) {
+                       double* c_s, double* max_residual, void* stream) {
   if (!p || !s) return PC_E_CONFIG;
   if (cudaSetDevice(p->device) != cudaSuccess) return PC_E_CUDA;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (max_residual) {
+    if (!p->d_dbg_resid && cudaMalloc(&p->d_dbg_resid, sizeof(double)) != cudaSuccess) return PC_E_CUDA;
+    if (cudaMemsetAsync(p->d_dbg_resid, 0, sizeof(double), st) != cudaSuccess) return PC_E_CUDA;
+  }
   conv_plan_info info;
   conv_plan_query(p, &info);
   Exec d;
@@ -1055,7 +1141,12 @@ int conv_execute_debug(conv_plan* p, const double* s, double* r, double* packed,
   d.dbg_rint = reinterpret_cast<long long*>(rint);
   d.dbg_rint_stride = info.rint_stride;
   d.dbg_cs = c_s;
-  return run_exec(p, s, 0, 0, r, 0, 0, 0, p->P, 1, &d, (cudaStream_t)stream);
+  d.dbg_resid = max_residual ? p->d_dbg_resid : nullptr;
+  const int rc = run_exec(p, s, 0, 0, r, 0, 0, 0, p->P, 1, &d, st);
+  if (rc || !max_residual) return rc;
+  if (cudaMemcpyAsync(max_residual, p->d_dbg_resid, sizeof(double), cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    return PC_E_CUDA;
+  return cuda_status(cudaStreamSynchronize(st));
 }
 
 int conv_plan_set_kernels(conv_plan* p, const double* q_dev, int64_t n, int64_t q_stride, void* stream) {
@@ -1120,8 +1211,8 @@ int conv_xcorr_pairs(conv_plan* p, const double* x_dev, int64_t n, int64_t x_str
   int rc = run_exec(p, x_dev, 0, x_stride, p->d_xc_pval, 0, n_lags, 0, p->P, n, nullptr, st, nullptr, nullptr,
                     p->d_xc_pval, p->d_xc_plag, true);
   if (rc) return rc;
-  return cuda_status(pc::launch_xcorr_reduce(p->d_xc_pval, p->d_xc_plag, n, n_part, score,
-                                             reinterpret_cast<long long*>(lag), st));
+  return plan_flags(p, cuda_status(pc::launch_xcorr_reduce(p->d_xc_pval, p->d_xc_plag, n, n_part, score,
+                                                           reinterpret_cast<long long*>(lag), st)));
 }
 
 int conv_xcorr_max(conv_plan* p, const double* db, int64_t n_signals, int64_t s_stride, double* score,
@@ -1155,7 +1246,7 @@ int conv_xcorr_max(conv_plan* p, const double* db, int64_t n_signals, int64_t s_
     if (rc) return rc;
     cudaError_t e = pc::launch_xcorr_reduce(p->d_xc_pval, p->d_xc_plag, n_signals, n_part, score,
                                             reinterpret_cast<long long*>(lag), st);
-    return cuda_status(e);
+    return plan_flags(p, cuda_status(e));
   }
   long long chunk = (1LL << 28) / n_lags;    // <= 2 GiB of lag scratch
   if (chunk < 1) chunk = 1;
@@ -1176,7 +1267,7 @@ int conv_xcorr_max(conv_plan* p, const double* db, int64_t n_signals, int64_t s_
                                          reinterpret_cast<long long*>(lag) + s0, st);
     if (e != cudaSuccess) return PC_E_CUDA;
   }
-  return PC_OK;
+  return plan_flags(p, PC_OK);
 }
 
 int conv_snr_calibrate(conv_plan* p, const double* s, const double* k, int32_t Q, double* offset_db,
@@ -1238,12 +1329,19 @@ int conv_snr_calibrate(conv_plan* p, const double* s, const double* k, int32_t Q
 
 int conv_adapt_block(conv_plan* p, const double* s, double snr_floor_db, double calib_offset_db,
                      conv_block_decision* out, void* stream) {
+  if (!p) return PC_E_CONFIG;
+  return conv_adapt_blocks(p, s, 0, 0, p->P, snr_floor_db, calib_offset_db, out, stream);
+}
+
+int conv_adapt_blocks(conv_plan* p, const double* s, int64_t s_offset, int64_t B0, int64_t B1, double snr_floor_db,
+                      double calib_offset_db, conv_block_decision* out, void* stream) {
   if (!p || !s) return PC_E_CONFIG;
   if (p->packing != PC_PACK_ADAPTIVE) return PC_E_CONFIG;
+  if (B0 < 0 || B1 > p->P || B0 >= B1) return PC_E_CONFIG;
   if (!p->kernel_set) return PC_E_STATE;
   if (cudaSetDevice(p->device) != cudaSuccess) return PC_E_CUDA;
   cudaStream_t st = (cudaStream_t)stream;
-  const long long P = p->P;
+  const long long P = p->P, nb = B1 - B0;
   cudaError_t e = cudaSuccess;
   if (!p->d_dec_pack) {
     e = cudaMalloc(&p->d_dec_pack, sizeof(int) * P);
@@ -1273,28 +1371,28 @@ int conv_adapt_block(conv_plan* p, const double* s, double snr_floor_db, double 
       return PC_E_CUDA;
     p->cand_ok = 1;
   }
-  e = pc::launch_block_stats(make_geo(p), s, p->d_sigma, p->d_peak, st);
+  e = pc::launch_block_stats(make_geo(p), s - s_offset, p->d_sigma, p->d_peak, st, B0, nb);
   if (e == cudaSuccess)
-    e = pc::launch_adapt_decide(P, p->d_sigma, p->d_peak, p->k_sigma, p->k_peak, p->d_cand, p->d_cand + 4, nc, thr,
-                                p->d_dec_pack, p->d_dec_q, p->d_dec_snr, st);
-  if (e == cudaSuccess) e = pc::launch_adapt_lists(P, p->d_dec_pack, p->d_lists, p->d_counts, st);
+    e = pc::launch_adapt_decide(nb, p->d_sigma + B0, p->d_peak + B0, p->k_sigma, p->k_peak, p->d_cand, p->d_cand + 4,
+                                nc, thr, p->d_dec_pack + B0, p->d_dec_q + B0, p->d_dec_snr + B0, st);
+  if (e == cudaSuccess) e = pc::launch_adapt_lists(nb, p->d_dec_pack, p->d_lists, p->d_counts, st, B0, P);
   if (e != cudaSuccess) return PC_E_CUDA;
   if (out) {
-    int* hp = (int*)std::malloc(sizeof(int) * P * 2);
-    double* hs = (double*)std::malloc(sizeof(double) * P);
+    int* hp = (int*)std::malloc(sizeof(int) * nb * 2);
+    double* hs = (double*)std::malloc(sizeof(double) * nb);
     if (!hp || !hs) {
       std::free(hp);
       std::free(hs);
       return PC_E_CUDA;
     }
-    e = cudaMemcpyAsync(hp, p->d_dec_pack, sizeof(int) * P, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(hp + P, p->d_dec_q, sizeof(int) * P, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(hs, p->d_dec_snr, sizeof(double) * P, cudaMemcpyDeviceToHost, st);
+    e = cudaMemcpyAsync(hp, p->d_dec_pack + B0, sizeof(int) * nb, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hp + nb, p->d_dec_q + B0, sizeof(int) * nb, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hs, p->d_dec_snr + B0, sizeof(double) * nb, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e == cudaSuccess) {
-      for (long long w = 0; w < P; ++w) {
+      for (long long w = 0; w < nb; ++w) {
         out[w].packing = hp[w];
-        out[w].Q = hp[P + w];
+        out[w].Q = hp[nb + w];
         out[w].snr_lin = hs[w];
       }
     }
@@ -1303,6 +1401,8 @@ int conv_adapt_block(conv_plan* p, const double* s, double snr_floor_db, double 
     if (e != cudaSuccess) return PC_E_CUDA;
   }
   p->adapt_ready = 1;   // decisions live on the device: the next execute is stream-ordered
+  p->adapt_b0 = B0;
+  p->adapt_b1 = B1;
   return PC_OK;
 }
 
@@ -1316,6 +1416,7 @@ int conv_plan_residual(conv_plan* p, double* resid_host, int32_t reset, void* st
   if (e == cudaSuccess && reset) e = cudaMemsetAsync(p->d_resid, 0, sizeof(double), st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return PC_E_CUDA;
+  if (reset) reinterpret_cast<volatile int*>(p->h_status)[pc::kStatusMargin] = 0;   // after the sync: no launch pending
   return *resid_host > 0.25 ? PC_W_UNPACK_MARGIN : PC_OK;
 }
 
@@ -1411,7 +1512,19 @@ int conv_plan_query(const conv_plan* p, conv_plan_info* info) {
   info->core_tile = (p->packing != PC_PACK_ADAPTIVE && p->opts.core == PC_CORE_DIRECT && tiled_shape(p, pk, &ts)) ? ts.T : 0;
   info->fft_n = p->fft_N;
   info->core_mma = info->core_tile ? ts.mma : 0;
+  info->backend_ok = p->backend_ok;
+  info->backend_resid = p->backend_resid;
+  info->u_sys_cal = p->u_sys_cal;
+  info->device = p->device;
+  info->exec_used = p->opts.core == PC_CORE_FFT ? -1 : (uses_tiled(p) ? PC_EXEC_TILED : PC_EXEC_PERBLOCK);
   return PC_OK;
+}
+
+int conv_best_match(const double* score, const int64_t* lag, const double* cand, int64_t n, int64_t first_index,
+                    double* best, void* stream) {
+  if (!best || n < 1 || (!cand && (!score || !lag))) return PC_E_CONFIG;
+  return cuda_status(pc::launch_best_match(score, reinterpret_cast<const long long*>(lag), cand, n, first_index, best,
+                                           (cudaStream_t)stream));
 }
 
 }  // extern "C"

@@ -539,6 +539,8 @@ __global__ void __launch_bounds__(N / 16, (N <= 4096 ? PC_FFT_MINB : 1)) pc_fft_
     for (int o = 16; o > 0; o >>= 1) resid = fmax(resid, __shfl_xor_sync(0xffffffffu, resid, o));
     if ((tid & 31) == 0 && resid > 0.0)
       atomicMax(reinterpret_cast<unsigned long long*>(f.resid), (unsigned long long)__double_as_longlong(resid));
+    if ((tid & 31) == 0 && resid > 0.25 && e.status)    // the plan's host-mapped margin flag (conv_execute)
+      *reinterpret_cast<volatile int*>(e.status + kStatusMargin) = 1;
   }
   stamp(7);
 }
@@ -707,17 +709,15 @@ static cudaError_t launch_fft_N(int packing, const Geo& g, const Exec& e, const 
 #define PC_FFT_CASE(PK)                                                                                  \
   case PK: {                                                                                             \
     auto kfn = pc_fft_conv_kernel<PK, N>;                                                               \
-    static unsigned set = 0; /* attributes are per device: one bit each */                             \
-    int dev_ = 0;                                                                                        \
+    static LaunchAttrCache cache; /* per device, under a lock */                                       \
+    static std::once_flag carve;                                                                         \
+    int dev_ = 0, sms_ = 0;                                                                              \
     if ((err = cudaGetDevice(&dev_)) != cudaSuccess) return err;                                         \
-    if (!((set >> (dev_ & 31)) & 1u)) {                                                                  \
-      err = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);          \
-      if (err != cudaSuccess) return err;                                                                \
-      /* leave the rest of the 256 KB unified array to L1: the spectrum tables stay cached */           \
-      err = cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, PC_FFT_CARVEOUT);  \
-      if (err != cudaSuccess) return err;                                                                \
-      set |= 1u << (dev_ & 31);                                                                          \
-    }                                                                                                    \
+    if ((err = cache.ensure(kfn, dev_, smem, N / 16, &sms_)) != cudaSuccess) return err;                \
+    /* leave the rest of the 256 KB unified array to L1: the spectrum tables stay cached */             \
+    std::call_once(carve, [&] {                                                                          \
+      cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, PC_FFT_CARVEOUT);       \
+    });                                                                                                  \
     kfn<<<(unsigned)n_jobs, N / 16, smem, st>>>(g, e, f);                                              \
     break;                                                                                               \
   }
@@ -742,15 +742,11 @@ cudaError_t launch_fft_conv(int packing, int N, const Geo& g, const Exec& e, con
     case 16384: {                                         // full precision only (2-CTA clusters)
       if (packing != PACK_FULL) return cudaErrorInvalidValue;
       const size_t smem = (size_t)(kN32 + kN32 / 16 + 64 + kN32 / 64) * sizeof(double2);
-      static unsigned set = 0;                            // per device
-      int dev = 0;
-      if (cudaGetDevice(&dev) != cudaSuccess) return cudaErrorInvalidDevice;
-      if (!((set >> (dev & 31)) & 1u)) {
-        cudaError_t err = cudaFuncSetAttribute(pc_fft32k_full_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)smem);
-        if (err != cudaSuccess) return err;
-        set |= 1u << (dev & 31);
-      }
+      static LaunchAttrCache cache;                       // per device, under a lock
+      int dev = 0, sms = 0;
+      cudaError_t err = cudaGetDevice(&dev);
+      if (err == cudaSuccess) err = cache.ensure(pc_fft32k_full_kernel, dev, smem, kN32 / 16, &sms, false);
+      if (err != cudaSuccess) return err;
       pc_fft32k_full_kernel<<<(unsigned)(2 * n_jobs), kN32 / 16, smem, st>>>(g, e, f);
       return cudaGetLastError();
     }

@@ -268,6 +268,7 @@ __device__ __forceinline__ void fused_block(const Geo& g, const Exec& e, const M
   const double inv = dequant_scale(c_s, mp.c_k);   // Eq. (16)
   const long long gbase = b.g0 + b.o0;        // global index of kept output 0
   long long* dri = e.dbg_rint ? e.dbg_rint + dbg_row * e.dbg_rint_stride : nullptr;
+  double resid = 0.0;                         // debug: worst last-digit residual of this thread
   auto store = [&](int k, double rint_v, double val) {
     if (dri) dri[k] = (long long)rint_v;
     if (!r) return;
@@ -287,6 +288,10 @@ __device__ __forceinline__ void fused_block(const Geo& g, const Exec& e, const M
     for (int p = tid; p < npairs; p += nt) {
       const int m = p + moff;
       const Digits3 d = decode_sym(Rs[m], mp.eps, mp.eps_inv, mp.pow2);
+      if (e.dbg_resid) {                       // last digit B: distance from its integer (LSB)
+        const double rem = __dsub_rn(Rs[m], __dmul_rn(d.C, mp.eps_inv));
+        resid = fmax(resid, fabs(__dmul_rn(__dsub_rn(rem, d.A), mp.eps_inv) - d.B));
+      }
       const double Bp = (m >= 1) ? decode_sym_B(Rs[m - 1], mp.eps, mp.eps_inv, mp.pow2) : 0.0;
       const double ev = d.C + Bp, od = d.A;
       store(2 * p, ev, __dmul_rn(ev, inv));
@@ -299,6 +304,7 @@ __device__ __forceinline__ void fused_block(const Geo& g, const Exec& e, const M
 #pragma unroll
       for (int q = 0; q < M; ++q) {          // balanced digits, most significant first (C9)
         const double t = rint(v);
+        if (q == M - 1 && e.dbg_resid && q * b.S + m < b.n_out) resid = fmax(resid, fabs(v - t));
         if (q < M - 1) v = __dmul_rn(__dsub_rn(v, t), mp.eps_inv);
         const int k = q * b.S + m;
         if (k < b.n_out) store(k, t, __dmul_rn(t, inv));
@@ -306,6 +312,11 @@ __device__ __forceinline__ void fused_block(const Geo& g, const Exec& e, const M
     }
   } else {
     for (int m = tid; m < b.n_out; m += nt) store(m, 0.0, Rs[m]);
+  }
+  if (e.dbg_resid) {
+    for (int o = 16; o > 0; o >>= 1) resid = fmax(resid, __shfl_xor_sync(0xffffffffu, resid, o));
+    if ((tid & 31) == 0 && resid > 0.0)
+      atomicMax(reinterpret_cast<unsigned long long*>(e.dbg_resid), (unsigned long long)__double_as_longlong(resid));
   }
 }
 
@@ -337,11 +348,13 @@ __global__ void __launch_bounds__(kMaxThreads, 1) pc_fused_kernel(Geo g, Exec e)
 // once with every load in flight (the two-pass loop re-read it and was latency-bound:
 // 46 us for 134 MB at L = 2^24); longer blocks fall back to the loop.
 constexpr int kStatsThreads = 256, kStatsU = 16;
-__global__ void __launch_bounds__(kStatsThreads) pc_block_stats(Geo g, const double* __restrict__ s,
+// s is the global sample base (s[i] = sample i; a shard passes its slice minus its offset);
+// blocks b0 .. b0 + gridDim.x - 1.
+__global__ void __launch_bounds__(kStatsThreads) pc_block_stats(Geo g, const double* __restrict__ s, long long b0,
                                                                 double* __restrict__ sigma, double* __restrict__ peak_out) {
   __shared__ double red[32];
   __shared__ unsigned long long ired[32];
-  const long long w = blockIdx.x;
+  const long long w = b0 + blockIdx.x;
   const int tid = threadIdx.x, nt = blockDim.x;
   const long long g0 = (w == 0) ? 0 : w * (long long)g.W - 2;
   const long long avail = g.L - g0;
@@ -436,8 +449,10 @@ __global__ void pc_adapt_decide(long long P, const double* __restrict__ sigma, c
 // One CTA of 1024 threads, kListsPer consecutive blocks per thread per round (fewer rounds and
 // barriers): per-thread counts, a warp scan of them, a scan over warp totals per packing.
 constexpr int kListsPer = 4;
-__global__ void __launch_bounds__(1024) pc_adapt_lists(long long P, const int* __restrict__ dec_pack,
-                                                       int* __restrict__ lists, int* __restrict__ counts) {
+// Blocks b0 .. b0 + P - 1 (dec_pack indexed by block; list stride `stride`).
+__global__ void __launch_bounds__(1024) pc_adapt_lists(long long P, long long b0, long long stride,
+                                                       const int* __restrict__ dec_pack, int* __restrict__ lists,
+                                                       int* __restrict__ counts) {
   __shared__ int woff[4][32];   // per round: warp counts, then their exclusive offsets
   __shared__ int base[4];       // list lengths before the round
   __shared__ int rtot[4];       // round totals
@@ -448,7 +463,7 @@ __global__ void __launch_bounds__(1024) pc_adapt_lists(long long P, const int* _
 #pragma unroll
     for (int j = 0; j < kListsPer; ++j) {
       const long long w = r0 + (long long)kListsPer * tid + j;
-      d[j] = (w < P) ? dec_pack[w] : -1;
+      d[j] = (w < P) ? dec_pack[b0 + w] : -1;
 #pragma unroll
       for (int m = 0; m < 4; ++m) cnt[m] += (d[j] == m);
     }
@@ -483,7 +498,7 @@ __global__ void __launch_bounds__(1024) pc_adapt_lists(long long P, const int* _
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           if (q == m) pos = base[q] + woff[q][wid] + excl[q]++;
-        lists[(size_t)m * P + pos] = (int)(r0 + (long long)kListsPer * tid + j);
+        lists[(size_t)m * stride + pos] = (int)(b0 + r0 + (long long)kListsPer * tid + j);
       }
     }
     __syncthreads();
@@ -522,20 +537,77 @@ __global__ void pc_xcorr_max(const double* __restrict__ c, long long n_lags, lon
   }
 }
 
+// ------------------------------------------------------------------ database winner (a9)
+// One CTA: the largest score, ties to the smallest index (reading C17), over candidates
+// (score[i], lag[i], first + i) or the rows {score, lag, index} of cand.
+__global__ void __launch_bounds__(1024) pc_best_match(const double* __restrict__ score, const long long* __restrict__ lag,
+                                                      const double* __restrict__ cand, long long n, long long first,
+                                                      double* __restrict__ best) {
+  __shared__ double sv[32], sl[32], si[32];
+  double bv = -__longlong_as_double(0x7ff0000000000000LL), bl = 0.0, bi = -1.0;
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+    const double v = cand ? cand[3 * i] : score[i];
+    const double l = cand ? cand[3 * i + 1] : (double)lag[i];
+    const double x = cand ? cand[3 * i + 2] : (double)(first + i);
+    if (bi < 0.0 || v > bv || (v == bv && x < bi)) {
+      bv = v;
+      bl = l;
+      bi = x;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, bv, o), ol = __shfl_xor_sync(0xffffffffu, bl, o),
+                 oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (oi >= 0.0 && (bi < 0.0 || ov > bv || (ov == bv && oi < bi))) {
+      bv = ov;
+      bl = ol;
+      bi = oi;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sv[threadIdx.x >> 5] = bv;
+    sl[threadIdx.x >> 5] = bl;
+    si[threadIdx.x >> 5] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+      if (si[w] >= 0.0 && (bi < 0.0 || sv[w] > bv || (sv[w] == bv && si[w] < bi))) {
+        bv = sv[w];
+        bl = sl[w];
+        bi = si[w];
+      }
+    best[0] = bv;
+    best[1] = bl;
+    best[2] = bi;
+  }
+}
+
+// ------------------------------------------------------------------ backend validation input
+// x[i] = +-1 with the sign from a counter-based hash (splitmix64 of seed + i): every companded
+// sample is +-S_q, so every packed digit has full magnitude ("randomized worst-case packed
+// operands").
+__global__ void pc_fill_pm1(double* __restrict__ x, long long n, unsigned long long seed) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    unsigned long long z = seed + 0x9e3779b97f4a7c15ull * (unsigned long long)(i + 1);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    z ^= z >> 31;
+    x[i] = (z >> 63) ? -1.0 : 1.0;
+  }
+}
+
 // ------------------------------------------------------------------ host-side launchers
 template <int PACK>
 static cudaError_t launch_fused_t(const Geo& g, const Exec& e, long long n_jobs, int threads, size_t smem,
                                   cudaStream_t st) {
   auto kfn = pc_fused_kernel<PACK>;
-  // the >48 KB opt-in is a per-function attribute: set it once per size (host cost per launch)
-  static size_t set_for[64] = {0};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (smem > 49152 && (dev >= 64 || smem > set_for[dev])) {
-    cudaError_t err = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (err != cudaSuccess) return err;
-    if (dev < 64) set_for[dev] = smem;
-  }
+  // the >48 KB opt-in is a per-function attribute: raised once per device and size, under a lock
+  static LaunchAttrCache cache;
+  int dev = 0, sms = 0;
+  cudaError_t err = cudaGetDevice(&dev);
+  if (err == cudaSuccess) err = cache.ensure(kfn, dev, smem, threads, &sms);
+  if (err != cudaSuccess) return err;
   kfn<<<(unsigned)n_jobs, threads, smem, st>>>(g, e);
   return cudaGetLastError();
 }
@@ -566,8 +638,11 @@ cudaError_t launch_build_taps(const double* k_pad, const double* k_int, int Np, 
   return cudaGetLastError();
 }
 
-cudaError_t launch_block_stats(const Geo& g, const double* s, double* sigma, double* peak, cudaStream_t st) {
-  pc_block_stats<<<(unsigned)g.P, kStatsThreads, 0, st>>>(g, s, sigma, peak);
+cudaError_t launch_block_stats(const Geo& g, const double* s, double* sigma, double* peak, cudaStream_t st,
+                               long long b0, long long nb) {
+  if (nb < 0) nb = g.P - b0;
+  if (nb <= 0) return cudaSuccess;
+  pc_block_stats<<<(unsigned)nb, kStatsThreads, 0, st>>>(g, s, b0, sigma, peak);
   return cudaGetLastError();
 }
 
@@ -597,8 +672,9 @@ cudaError_t launch_build_taps_batch(const double* k_pad, const double* k_int, lo
   return cudaGetLastError();
 }
 
-cudaError_t launch_adapt_lists(long long P, const int* dec_pack, int* lists, int* counts, cudaStream_t st) {
-  pc_adapt_lists<<<1, 1024, 0, st>>>(P, dec_pack, lists, counts);
+cudaError_t launch_adapt_lists(long long P, const int* dec_pack, int* lists, int* counts, cudaStream_t st,
+                               long long b0, long long stride) {
+  pc_adapt_lists<<<1, 1024, 0, st>>>(P, b0, stride < 0 ? P : stride, dec_pack, lists, counts);
   return cudaGetLastError();
 }
 
@@ -697,6 +773,18 @@ cudaError_t launch_snr_sums(const double* ref, const double* x, long long n, con
 cudaError_t launch_xcorr_max(const double* c, long long n_signals, long long n_lags, long long stride,
                              double* score, long long* lag, cudaStream_t st) {
   pc_xcorr_max<<<(unsigned)n_signals, 1024, 0, st>>>(c, n_lags, stride, score, lag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_pm1(double* x, long long n, unsigned long long seed, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  pc_fill_pm1<<<592, 256, 0, st>>>(x, n, seed);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_best_match(const double* score, const long long* lag, const double* cand, long long n,
+                              long long first_index, double* best, cudaStream_t st) {
+  pc_best_match<<<1, 1024, 0, st>>>(score, lag, cand, n, first_index, best);
   return cudaGetLastError();
 }
 

@@ -2,10 +2,13 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <mutex>
+
 #include "pc_device.cuh"
 
 namespace pc {
 
+constexpr int kMaxDevices = 64;
 constexpr int kT = 8;              // outputs per thread of the per-block kernel's core
 constexpr int kMaxThreads = 1024;  // per-block kernel: threads per CTA; caps regs at 64
 constexpr int kTPChoices[3] = {16, 14, 12};   // tiled-kernel tiles instantiated; the plan picks
@@ -34,6 +37,37 @@ constexpr int kTiledThreads = 32 * (kTiledProdWarps + kTiledConsWarps);
 __host__ __device__ constexpr int tiled_cons_warps(int mma) { return mma ? PC_CONS_WARPS_MMA : kTiledConsWarps; }
 __host__ __device__ constexpr int tiled_threads(int mma) { return 32 * (kTiledProdWarps + tiled_cons_warps(mma)); }
 constexpr int kCtrDone = 256;     // sm_ctr[kCtrDone] counts retired CTAs; queues are sm_ctr[0, nsm)   // mbarrier + reduction scratch, keeps the rest 128B-aligned
+
+// Host: a kernel's launch attributes per device, raised once under a lock (launches from
+// several host threads / devices).  ensure() raises the maximum dynamic shared memory to at least
+// `need`, checks that one CTA of `threads` fits, and returns the device's SM count.
+struct LaunchAttrCache {
+  std::mutex mu;
+  size_t smem[kMaxDevices] = {};
+  int sms[kMaxDevices] = {};
+  template <class F>
+  cudaError_t ensure(F* kfn, int dev, size_t need, int threads, int* sms_out, bool check_occ = true) {
+    if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> lk(mu);
+    if (sms[dev] == 0) {
+      const cudaError_t err = cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
+      if (err != cudaSuccess) return err;
+    }
+    if (need > smem[dev] || smem[dev] == 0) {
+      cudaError_t err = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need);
+      if (err != cudaSuccess) return err;
+      if (check_occ) {                                 // (cluster kernels: checked at launch)
+        int occ = 0;
+        err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, threads, need);
+        if (err != cudaSuccess) return err;
+        if (occ < 1) return cudaErrorInvalidConfiguration;
+      }
+      smem[dev] = need;
+    }
+    *sms_out = sms[dev];
+    return cudaSuccess;
+  }
+};
 
 // Per-packing parameters of one launch (adaptive plans fill several).
 struct ModeP {
@@ -102,7 +136,13 @@ struct Exec {
   const double* pre_win;
   long long pre_stride;
   const double* pre_inv;
+  // plan flags in host-mapped pinned memory (conv_execute reads them without synchronizing):
+  // [kStatusMargin] an FFT-core launch saw a last-digit residual > 0.25 LSB, [kStatusWatchdog] a
+  // persistent-kernel wait timed out and the launch abandoned its work
+  int* status;
+  double* dbg_resid;    // conv_execute_debug: max last-digit residual (LSB, atomicMax on the bits)
 };
+constexpr int kStatusMargin = 0, kStatusWatchdog = 1;
 
 // FFT overlap-save core (pc_fft.cu).
 struct FftArgs {
@@ -138,15 +178,22 @@ cudaError_t launch_kernel_prep_batch(const double* k_in, long long k_stride, lon
 cudaError_t launch_build_taps_batch(const double* k_pad, const double* k_int, long long pad_stride, int Np,
                                     int packing, double eps_inv, int K, int K_pad, double* kr, long long kr_stride,
                                     long long n, cudaStream_t st);
-cudaError_t launch_block_stats(const Geo& g, const double* s, double* sigma, double* peak, cudaStream_t st);
+// s: global sample base; blocks [b0, b0 + nb) (nb < 0: to the end)
+cudaError_t launch_block_stats(const Geo& g, const double* s, double* sigma, double* peak, cudaStream_t st,
+                               long long b0 = 0, long long nb = -1);
 cudaError_t launch_adapt_decide(long long P, const double* sigma, const double* peak, double sig_k, double peak_k,
                                 const int* cand, const int* qmode, int ncand, double thr, int* dp, int* dq, double* ds,
                                 cudaStream_t st);
-cudaError_t launch_adapt_lists(long long P, const int* dec_pack, int* lists, int* counts, cudaStream_t st);
+// decisions of blocks [b0, b0 + P) into lists of row stride `stride` (< 0: P)
+cudaError_t launch_adapt_lists(long long P, const int* dec_pack, int* lists, int* counts, cudaStream_t st,
+                               long long b0 = 0, long long stride = -1);
 cudaError_t launch_xcorr_reduce(const double* val, const long long* lag, long long n_signals, long long n_part,
                                 double* score, long long* best, cudaStream_t st);
 cudaError_t launch_snr_sums(const double* ref, const double* x, long long n, const double* sigma, const double* peak,
                             long long P, double sig_k, double peak_k, double Q, double* out, cudaStream_t st);
+cudaError_t launch_best_match(const double* score, const long long* lag, const double* cand, long long n,
+                              long long first_index, double* best, cudaStream_t st);
+cudaError_t launch_fill_pm1(double* x, long long n, unsigned long long seed, cudaStream_t st);
 cudaError_t launch_xcorr_max(const double* c, long long n_signals, long long n_lags, long long stride,
                              double* score, long long* lag, cudaStream_t st);
 

@@ -298,8 +298,11 @@ __device__ __forceinline__ unsigned smid_() {
   asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
   return r;
 }
-// Watchdog wait (development safety net): a wait that has not completed after 4 s reports
-// where it is stuck and traps, so a scheduling bug fails the launch instead of hanging.
+// Watchdog waits: a wait that has not completed after 4 s (%globaltimer) is a scheduling fault.
+// Release builds raise the plan's host-mapped watchdog flag (conv_execute then returns
+// PC_E_WATCHDOG) and end the thread, so every other wait of the launch times out the same way
+// and the launch finishes without a sticky context error; PC_DEBUG_TRAP builds print where the
+// wait is stuck and trap.
 __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t phase) {
   uint32_t ok;
   asm volatile(
@@ -311,26 +314,36 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t phase) {
       : "memory");
   return ok != 0;
 }
-__device__ __noinline__ void mbar_stuck(int where, long long n, int st, uint32_t phase) {
+constexpr unsigned long long kWatchdogNs = 4000000000ull;
+__device__ __noinline__ void mbar_stuck(int* status, int where, long long n, int st, uint32_t phase) {
+#ifdef PC_DEBUG_TRAP
   printf("pc_tiled_kernel: wait %d stuck (block %d thread %d seq %lld slot %d parity %u)\n", where,
          (int)blockIdx.x, (int)threadIdx.x, n, st, phase);
   __trap();
+#else
+  (void)n;
+  (void)st;
+  (void)phase;
+  if (status) *reinterpret_cast<volatile int*>(status + kStatusWatchdog) = 1 + where;   // host-mapped
+  __threadfence_system();
+  asm volatile("exit;");
+#endif
 }
-// spin-wait step with the same watchdog (a scheduling bug traps with its location instead of
-// hanging the GPU): ~2^24 sleeps of >= 64 ns
-__device__ __forceinline__ void spin_wd(int& spins, unsigned ns, int where, long long n, int st) {
+// spin-wait step with the same 4-s watchdog (t0 = 0 before the first step)
+__device__ __forceinline__ void spin_wd(int* status, unsigned long long& t0, unsigned ns, int where, long long n,
+                                        int st) {
   __nanosleep(ns);
-  if (++spins > (1 << 24)) mbar_stuck(where, n, st, 0u);
+  const unsigned long long t = gtimer();
+  if (t0 == 0) t0 = t;
+  else if (t - t0 > kWatchdogNs) mbar_stuck(status, where, n, st, 0u);
 }
-__device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t phase, int where, long long n, int st) {
+__device__ __forceinline__ void mbar_wait_wd(int* status, uint64_t* bar, uint32_t phase, int where, long long n,
+                                             int st) {
   if (mbar_try(bar, phase)) return;
-  unsigned long long t0;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  const unsigned long long t0 = gtimer();
   for (;;) {
     if (mbar_try(bar, phase)) return;
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    if (t - t0 > 4000000000ull) mbar_stuck(where, n, st, phase);
+    if (gtimer() - t0 > kWatchdogNs) mbar_stuck(status, where, n, st, phase);
   }
 }
 
@@ -586,7 +599,7 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
     const long long nb = *e.blk_count;
     njobs = nb == 0 ? 0 : (e.blk_list[0] == 0 ? e.tiles0 + (nb - 1) * e.tiles1 : nb * e.tiles1);
     if (njobs == 0) {          // no block chose this packing: leave once the tap copy has landed
-      mbar_wait_wd(&ps->bar_taps, 0, 4, 0, 0);   // (every CTA leaves: the queues stay untouched)
+      mbar_wait_wd(e.status, &ps->bar_taps, 0, 4, 0, 0);   // (every CTA leaves: the queues stay untouched)
       return;
     }
   }
@@ -710,15 +723,15 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
       } else {
         long long j = -1;
         if (lane == 0) {
-          int sp = 0;
-          while (*reinterpret_cast<volatile long long*>(&ps->turn) != m) spin_wd(sp, 256, 5, m, 0);
+          unsigned long long sp = 0;
+          while (*reinterpret_cast<volatile long long*>(&ps->turn) != m) spin_wd(e.status, sp, 256, 5, m, 0);
           // bounded claim-ahead: a job claimed long before any warp can start it is work other
           // SMs can no longer steal (the launch's tail)
           // (sentinel sequences, after the first failed claim, are never held back)
           if (e.lookahead > 0)
             while (*reinterpret_cast<volatile long long*>(&ps->m_end) < 0 &&
                    m >= (long long)*reinterpret_cast<volatile int*>(&ps->mseq_hi) + e.lookahead)
-              spin_wd(sp, 128, 6, m, 0);
+              spin_wd(e.status, sp, 128, 6, m, 0);
           const long long me = *reinterpret_cast<volatile long long*>(&ps->m_end);
           j = (me >= 0) ? -1 : 0;
         }
@@ -762,11 +775,11 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
         if (n >= NS) {
           if (lane == 0)
           {
-            int sp = 0;
-            while (*reinterpret_cast<volatile long long*>(&ps->seq[st]) != n - NS) spin_wd(sp, 256, 7, n, st);
+            unsigned long long sp = 0;
+            while (*reinterpret_cast<volatile long long*>(&ps->seq[st]) != n - NS) spin_wd(e.status, sp, 256, 7, n, st);
           }
           __syncwarp();
-          mbar_wait_wd(&ps->empty[st], (uint32_t)(((n / NS) & 1) ^ 1), 1, n, st);
+          mbar_wait_wd(e.status, &ps->empty[st], (uint32_t)(((n / NS) & 1) ^ 1), 1, n, st);
         }
         if (prec && c == 0) t_sl = gtimer();
         if (job >= 0 && !(prepacked && c == 0) && !e.pre_win)
@@ -798,16 +811,15 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
   const int cw = ctid >> 5, lane = tid & 31;
   const int smsp = (tid >> 5) & 3;
   double* wbuf = wout + (size_t)cw * 32 * (T + 1);
-  mbar_wait_wd(&ps->bar_taps, 0, 4, 0, 0);
+  mbar_wait_wd(e.status, &ps->bar_taps, 0, 4, 0, 0);
   // A consumer warp may claim work up to NCW / npart jobs ahead of the producer, i.e. more than
   // one ring lap: a parity wait could then see the slot's previous lap; the sequence number
   // stamped by the producer tells the two apart.
   auto wait_full = [&](long long n, int st) {
-    for (int spin = 0;; ++spin) {
-      mbar_wait_wd(&ps->full[st], (uint32_t)((n / NS) & 1), 2, n, st);
+    for (unsigned long long sp = 0;;) {
+      mbar_wait_wd(e.status, &ps->full[st], (uint32_t)((n / NS) & 1), 2, n, st);
       if (*reinterpret_cast<volatile long long*>(&ps->seq[st]) == n) return;
-      if (spin > 20000000) mbar_stuck(3, n, st, (uint32_t)*reinterpret_cast<volatile long long*>(&ps->seq[st]));
-      __nanosleep(200);
+      spin_wd(e.status, sp, 200, 3, n, st);
     }
   };
   int njob = 0;
@@ -886,10 +898,10 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
       if (lane == 0)
         // while the SMSP's producer warp packs, one core slot: a second queued DMMA warp would
         // slow its loads and FP64 ops 3x (tools/dmma_interference.cu)
-        for (int sp = 0;
+        for (unsigned long long sp = 0;
              *reinterpret_cast<volatile int*>(&ps->core_serve[smsp]) +
                  (PC_PROD_YIELD && *reinterpret_cast<volatile int*>(&ps->prod_busy[smsp]) ? 1 : PC_CORE_SLOTS) <= cl;)
-          spin_wd(sp, 64, 8, cl, smsp);
+          spin_wd(e.status, sp, 64, 8, cl, smsp);
       if (wrec) wrec[0] |= ((gtimer() - wrec[1]) >> 4) << 32;   // diagnostics: token wait (16 ns units)
       __syncwarp();
     }
@@ -1161,17 +1173,11 @@ template <int PACK, int T, int PT>
 static cudaError_t launch_prepack_t(const Geo& g, const Exec& e, long long n_jobs, cudaStream_t st) {
   auto kfn = pc_prepack_kernel<PACK, T, PT>;
   const size_t smem = (size_t)g.W_block * sizeof(double);
-  static size_t c_smem = 0;                          // attribute set for (device, size): per device
-  static int c_dev = -1;
-  int dev = 0;
-  cudaError_t err0 = cudaGetDevice(&dev);
-  if (err0 != cudaSuccess) return err0;
-  if (smem > c_smem || dev != c_dev) {
-    cudaError_t err = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (err != cudaSuccess) return err;
-    c_smem = smem;
-    c_dev = dev;
-  }
+  static LaunchAttrCache cache;                      // per device, under a lock
+  int dev = 0, sms = 0;
+  cudaError_t err = cudaGetDevice(&dev);
+  if (err == cudaSuccess) err = cache.ensure(kfn, dev, smem, kPrepackThreads, &sms);
+  if (err != cudaSuccess) return err;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)n_jobs);
   cfg.blockDim = dim3(kPrepackThreads);
@@ -1212,24 +1218,11 @@ template <int PACK, int T, int MMA>
 static cudaError_t launch_tiled_t(const Geo& g, const Exec& e, long long n_jobs, int threads, size_t smem,
                                   cudaStream_t st, int* grid_out) {
   auto kfn = pc_tiled_kernel<PACK, T, MMA>;
-  static size_t c_smem = 0;
-  static int c_threads = 0, c_grid = 0, c_dev = -1, c_sms = 0;
-  int dev = 0;
+  static LaunchAttrCache cache;                      // per device, under a lock
+  int dev = 0, c_sms = 0;
   cudaError_t err = cudaGetDevice(&dev);
+  if (err == cudaSuccess) err = cache.ensure(kfn, dev, smem, threads, &c_sms);
   if (err != cudaSuccess) return err;
-  if (smem != c_smem || threads != c_threads || dev != c_dev) {
-    err = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (err != cudaSuccess) return err;
-    int occ = 0;
-    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, threads, smem);
-    if (err != cudaSuccess) return err;
-    cudaDeviceGetAttribute(&c_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (occ < 1) return cudaErrorInvalidConfiguration;
-    c_smem = smem;
-    c_threads = threads;
-    c_dev = dev;
-    c_grid = c_sms * occ;
-  }
   if (c_sms > kCtrDone) return cudaErrorInvalidConfiguration;
   Exec ex = e;
   ex.nsm = c_sms;

@@ -5,8 +5,9 @@ host-side exchanges.  The data path never crosses ranks:
   [P*g/G, P*(g+1)/G) of one long signal, reads its input range plus the N'+1-sample halo
   (`shard`), runs `conv_execute_blocks` and writes a disjoint output range;
 * signal sharding (config 4): rank g owns database signals [n*g/G, n*(g+1)/G), computes
-  per-signal (score, lag) with `conv_xcorr_max`, and only the scores are gathered
-  (`gather_best_match`, NCCL all_gather of 16 B/signal).
+  per-signal (score, lag) with `conv_xcorr_max`, reduces them to its winner on the device
+  (`conv_best_match`), and only the winners are gathered (`gather_best_match`, NCCL all_gather
+  of 24 B per rank).
 """
 from __future__ import annotations
 
@@ -22,36 +23,39 @@ def signal_range(n_signals, rank, world):
     return n_signals * rank // world, n_signals * (rank + 1) // world
 
 
-def gather_best_match(scores, lags, first_signal, group=None):
+def _device_best_match(out, n, scores=None, lags=None, cand=None, first=0):
+    binding.best_match(out, n, score_dev=scores, lag_dev=lags, cand_dev=cand, first_index=first)
+
+
+def gather_best_match(scores, lags, first_signal, group=None, reduce=None):
     """All ranks learn the database winner: the largest score, ties to the smallest global
-    signal index (reading C17).  `scores` (float64) / `lags` (int64) are this rank's
-    per-signal results for signals first_signal .. first_signal+len-1 (any device the
-    process group's backend supports).  Returns (signal, score, lag)."""
+    signal index (reading C17).  `scores` (float64) / `lags` (int64) are this rank's per-signal
+    results for signals first_signal .. first_signal+len-1.  Each rank reduces its own signals to
+    one candidate {score, lag, index} on the device (conv_best_match), the world's candidates are
+    all-gathered (NCCL: one 3-double tensor per rank) and reduced again by the same kernel:
+    stream-ordered, no host round trip until the caller reads the result.  `reduce` replaces the
+    device kernel (CPU / gloo tests of this host logic).  Returns the tensor {score, lag, index}."""
     import torch
     import torch.distributed as dist
 
+    red = reduce or _device_best_match
     world = dist.get_world_size(group)
     dev = scores.device
-    n = torch.tensor([scores.numel()], dtype=torch.int64, device=dev)
-    ns = [torch.zeros_like(n) for _ in range(world)]
-    dist.all_gather(ns, n, group=group)
-    m = int(max(int(x.item()) for x in ns))
-    pad = m - scores.numel()
-    packed = torch.stack([torch.cat([scores.double(), torch.full((pad,), float("-inf"), device=dev, dtype=torch.float64)]),
-                          torch.cat([lags.double(), torch.zeros(pad, device=dev, dtype=torch.float64)]),
-                          torch.cat([torch.arange(first_signal, first_signal + scores.numel(), device=dev,
-                                                  dtype=torch.float64),
-                                     torch.full((pad,), float("inf"), device=dev, dtype=torch.float64)])])
-    parts = [torch.zeros_like(packed) for _ in range(world)]
-    dist.all_gather(parts, packed, group=group)
-    allp = torch.cat(parts, dim=1).cpu()
-    best = float("-inf")
-    win = None
-    for j in range(allp.shape[1]):
-        sc, lg, idx = float(allp[0, j]), int(allp[1, j]), allp[2, j]
-        if idx == float("inf"):
-            continue
-        idx = int(idx)
-        if sc > best or (sc == best and win is not None and idx < win[0]):
-            best, win = sc, (idx, sc, lg)
-    return win
+    local = torch.empty(3, dtype=torch.float64, device=dev)
+    red(local, scores.numel(), scores=scores, lags=lags, first=first_signal)
+    if dist.get_backend(group) == "nccl":
+        cand = torch.empty(3 * world, dtype=torch.float64, device=dev)
+        dist.all_gather_into_tensor(cand, local, group=group)
+    else:
+        parts = [torch.empty_like(local) for _ in range(world)]
+        dist.all_gather(parts, local, group=group)
+        cand = torch.cat(parts)
+    best = torch.empty(3, dtype=torch.float64, device=dev)
+    red(best, world, cand=cand)
+    return best
+
+
+def best_match_tuple(best):
+    """(signal, score, lag) of a gather_best_match result (reads it back to the host)."""
+    b = best.cpu().tolist()
+    return int(b[2]), float(b[0]), int(b[1])

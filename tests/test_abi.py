@@ -44,26 +44,72 @@ def test_library_exports_every_declared_symbol(lib):
 
 
 def test_struct_layout_matches_c(lib):
+    """Every named field of the ctypes mirrors sits at the C offset (no magic reserved[] slots)."""
     from paper_1201_3018_b200 import binding as b
-    src = r'''
-#include <stdio.h>
-#include <stddef.h>
-#include "packedconv.h"
-int main(void) {
-  printf("%zu %zu %zu %zu %zu %zu\n", sizeof(conv_opts), offsetof(conv_opts, u_sys), sizeof(conv_plan_info),
-         offsetof(conv_plan_info, eps), offsetof(conv_plan_info, q_mode), sizeof(conv_block_decision));
-  return 0;
-}
-'''
+    structs = [("conv_opts", b.conv_opts), ("conv_plan_info", b.conv_plan_info), ("conv_shard", b.conv_shard),
+               ("conv_block_decision", b.conv_block_decision)]
+    lines, want = [], []
+    for cname, cls in structs:
+        lines.append(f'printf("%zu\\n", sizeof({cname}));')
+        want.append(C.sizeof(cls))
+        for fname, _ in cls._fields_:
+            lines.append(f'printf("%zu\\n", offsetof({cname}, {fname}));')
+            want.append(getattr(cls, fname).offset)
+    src = "#include <stdio.h>\n#include <stddef.h>\n#include \"packedconv.h\"\nint main(void) {\n" + \
+        "\n".join(lines) + "\nreturn 0;\n}\n"
     with tempfile.TemporaryDirectory() as d:
         c = os.path.join(d, "t.c")
         open(c, "w").write(src)
         exe = os.path.join(d, "t")
         subprocess.check_call(["gcc", "-I", os.path.dirname(HEADER), c, "-o", exe])
         vals = [int(v) for v in subprocess.check_output([exe]).split()]
-    want = [C.sizeof(b.conv_opts), b.conv_opts.u_sys.offset, C.sizeof(b.conv_plan_info), b.conv_plan_info.eps.offset,
-            b.conv_plan_info.q_mode.offset, C.sizeof(b.conv_block_decision)]
     assert vals == want
+    # the tuning knobs are named fields, not reserved slots
+    names = [f for f, _ in b.conv_opts._fields_]
+    for f in ("fft_n", "core_variant", "core_tile", "parts_per_job", "unpack_form", "validate_trials"):
+        assert f in names
+    assert "reserved" not in names
+
+
+def test_library_reads_no_environment(lib):
+    """Library behaviour is set through conv_opts only: no getenv in the sources."""
+    csrc = os.path.join(ROOT, "paper_1201_3018_b200", "csrc")
+    for f in os.listdir(csrc):
+        assert "getenv" not in open(os.path.join(csrc, f)).read(), f
+
+
+def test_release_kernels_do_not_trap(lib):
+    """The persistent kernel's watchdog raises a host-mapped flag and exits (PC_E_WATCHDOG) in
+    release builds; __trap (a sticky context error) exists only in PC_DEBUG_TRAP builds."""
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", lib._name], capture_output=True,
+                          text=True).stdout
+    assert "BPT.TRAP" not in sass
+
+
+def test_binding_rejects_bad_buffers():
+    """The C ABI takes no lengths: the binding checks dtype, contiguity, device and size."""
+    import torch
+    from paper_1201_3018_b200 import binding as b
+    info = {"device": 0, "L": 100, "N": 9, "Np": 9, "W": 30, "W_block": 40, "mode": b.MODE_CONV}
+    with pytest.raises(b.PcError) as ei:
+        b._dev(torch.zeros(100, dtype=torch.float64), 100, "w", "s", info)      # host tensor
+    assert ei.value.code == b.PC_E_CONFIG
+    with pytest.raises(b.PcError):
+        b._host(np_zeros(50), 100, "w", "s")                                     # too short
+    with pytest.raises(b.PcError):
+        b._host(np_zeros(200).astype("float32"), 100, "w", "s")                  # wrong dtype
+    with pytest.raises(b.PcError):
+        b._host(np_zeros(400)[::2], 100, "w", "s")                               # strided
+    assert b._host(np_zeros(100), 100, "w", "s")
+    assert b._dev(12345, 10**9, "w", "s", info) == 12345                         # raw pointer: caller-managed
+    # block spans (reading C7, Eq. (17)): blocks [0, 2) of L = 100, N' = 9, W = 30, W_block = 40
+    assert b._block_span(info, 0, 2) == (min(100, 30 - 2 + 40), 9 - 1 + 60)
+    assert b._block_span(info, 1, 4) == (100, 100 + 9 - 1)
+
+
+def np_zeros(n):
+    import numpy as np
+    return np.zeros(n)
 
 
 def test_status_strings_and_defaults(lib):

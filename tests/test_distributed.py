@@ -96,6 +96,17 @@ def test_gloo_block_sharded_pipeline_equals_single_run():
     assert q.get(timeout=10) is True
 
 
+def _cpu_best_match(out, n, scores=None, lags=None, cand=None, first=0):
+    """Stand-in for the conv_best_match kernel on CPU: the C17 rule written out."""
+    rows = cand.view(-1, 3).tolist() if cand is not None else \
+        [[float(scores[i]), float(lags[i]), float(first + i)] for i in range(n)]
+    best = None
+    for sc, lg, idx in rows[:n]:
+        if best is None or sc > best[0] or (sc == best[0] and idx < best[2]):
+            best = [sc, lg, idx]
+    out.copy_(torch.tensor(best, dtype=torch.float64))
+
+
 def _worker_gather(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -103,7 +114,8 @@ def _worker_gather(rank, world, port, q):
     a, b = D.signal_range(n, rank, world)
     scores = torch.tensor([float((i * 7) % 5) for i in range(a, b)], dtype=torch.float64)  # ties: max 4 at i=2,7
     lags = torch.tensor([100 + i for i in range(a, b)], dtype=torch.int64)
-    q.put((rank, D.gather_best_match(scores, lags, a)))
+    best = D.gather_best_match(scores, lags, a, reduce=_cpu_best_match)
+    q.put((rank, D.best_match_tuple(best)))
     dist.destroy_process_group()
 
 
@@ -119,3 +131,21 @@ def test_gloo_score_gather_ties_to_lowest_signal():
     assert all(p.exitcode == 0 for p in procs)
     res = dict(q.get(timeout=10) for _ in range(2))
     assert res[0] == res[1] == (2, 4.0, 102)
+
+
+@pytest.mark.slow
+def test_bench_launcher_relaunches_with_torchrun():
+    """bench.py --gpus 2 outside torchrun re-launches itself through torch.distributed.run (one
+    process per rank); the reference arm runs on rank 0 and reports n_gpus = the world size."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_PORT")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--gpus", "2",
+                          "--steps", "1", "--warmup", "1", "--workload", "cfg1"], capture_output=True, text=True,
+                         timeout=300, env=env, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(x) for x in out.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    assert lines[0]["impl"] == "reference" and lines[0]["n_gpus"] == 2

@@ -32,9 +32,9 @@ def dev(x):
 def gpu_run(s, k, W_block, packing, Q, mode=O.CONV, eps_rule=O.EPS_POW2, rmax_rule=O.RMAX_PAPER, debug=True,
             tile=0, npart=0, exec_=0, core=0):
     opts = pcb.opts_default(eps_rule=EPS[eps_rule], rmax_rule=rmax_rule, bound_policy=pcb.BOUND_WARN, exec=exec_)
-    opts.reserved[1] = tile
-    opts.reserved[2] = core     # direct core: 0 auto (FP64 tensor cores, T = 16), 1 FP64 FMA, 2 DMMA
-    opts.reserved[3] = npart
+    opts.core_tile = tile
+    opts.core_variant = core    # direct core: 0 auto (FP64 tensor cores, T = 16), 1 FP64 FMA, 2 DMMA
+    opts.parts_per_job = npart
     with pcb.Plan(len(s), len(k), W_block, mode, PK[packing], Q, opts=opts) as p:
         p.set_kernel(dev(k))
         info = p.info()
@@ -241,30 +241,32 @@ def test_bound_policy_strict():
         assert ei.value.code == pcb.PC_E_BOUND
 
 
-def test_execute_blocks_sharding_bit_identical():
-    """Block-range sharding: each 'rank' holds only its input slice plus the
-    N'+1 halo; the union of outputs is bit-identical to the single run, for G = 1,2,3,4,8."""
+@pytest.mark.parametrize("mode", [O.CONV, O.XCORR])
+def test_execute_blocks_sharding_bit_identical(mode):
+    """Block-range sharding: each 'rank' takes its shard from conv_shard_range,
+    holds only its input slice plus the N'+1 halo, and runs conv_execute_blocks; the union of
+    the shards' outputs is bit-identical to the single run, for G = 1, 2, 3, 4, 8."""
     rng = np.random.default_rng(2)
     L, N, W_block, Q = 200000, 64, 1024, 255
     s, k = rng.laplace(0, 0.2, L), rng.uniform(-1, 1, N)
-    ref = O.conv_pipeline(s, k, W_block, O.ASYM2, Q)
-    with pcb.Plan(L, N, W_block, pcb.MODE_CONV, pcb.PACK_ASYM2, Q) as p:
+    ref = O.conv_pipeline(s, k, W_block, O.ASYM2, Q, mode=mode)
+    with pcb.Plan(L, N, W_block, mode, pcb.PACK_ASYM2, Q) as p:
         p.set_kernel(dev(k))
         info = p.info()
-        P, W = info["P"], info["W"]
         for G in (1, 2, 3, 4, 8):
             out = np.full(info["L_out"], np.nan)
+            covered = 0
             for rank in range(G):
-                b0, b1 = P * rank // G, P * (rank + 1) // G
-                in0 = 0 if b0 == 0 else b0 * W - 2
-                in1 = min(L, (b1 - 1) * W - 2 + W_block) if b1 > 1 else min(L, W_block)
-                o0 = 0 if b0 == 0 else info["Np"] - 1 + b0 * W
-                o1 = min(info["L_out"], info["Np"] - 1 + b1 * W)
+                sh = pcb.shard_range(L, N, W_block, mode, rank, G)
+                in0, in1, o0, o1 = sh["in_begin"], sh["in_end"], sh["out_begin"], sh["out_end"]
                 s_slice = dev(s[in0:in1])
-                r_slice = torch.full((o1 - o0,), float("nan"), dtype=torch.float64, device=DEV)
-                p.execute_blocks(s_slice, in0, r_slice, o0, b0, b1)
+                r_slice = torch.full((max(1, o1 - o0),), float("nan"), dtype=torch.float64, device=DEV)
+                p.execute_blocks(s_slice, in0, r_slice, o0, sh["block_begin"], sh["block_end"])
                 torch.cuda.synchronize()
-                out[o0:o1] = r_slice.cpu().numpy()
+                assert np.isnan(out[o0:o1]).all()          # disjoint output ranges
+                out[o0:o1] = r_slice[:o1 - o0].cpu().numpy()
+                covered += o1 - o0
+            assert covered == info["L_out"]
             assert np.array_equal(out, ref.out), G
 
 
@@ -524,14 +526,14 @@ def test_fft_full_precision(case):
                                   (20_000, 4096, 16384)])
 def test_fft32k_configured_full_precision(case, mode):
     """cfg3's configured full-precision core: the block's linear convolution through a
-    32768-point real transform (conv_opts.reserved[4] = 16384), computed by 2-CTA clusters
+    32768-point real transform (conv_opts.fft_n = 16384), computed by 2-CTA clusters
     (parity classes, DSMEM combine).  Within 1e-12 normalized of the direct FP64 result,
     including block 0 (zero prefix skipped), ragged tails and xcorr placement."""
     L, N, W_block = case
     rng = np.random.default_rng(N + L)
     s, k = rng.laplace(0, 0.2, L), rng.normal(0, 1 / np.sqrt(N), N)
     opts = pcb.opts_default(core=1)
-    opts.reserved[4] = 16384
+    opts.fft_n = 16384
     with pcb.Plan(L, N, W_block, pcb.MODE_XCORR if mode == O.XCORR else pcb.MODE_CONV, pcb.PACK_FULL, 0,
                   opts=opts) as p:
         p.set_kernel(dev(k))
@@ -633,7 +635,7 @@ def test_execute_host_pipelined(mode, packing):
 @pytest.mark.parametrize("mode", [O.CONV, O.XCORR])
 @pytest.mark.parametrize("case", [(50_000, 65, 1024, 20), (120_000, 129, 2048, 20), (60_000, 33, 512, 35)])
 def test_literal_paper_unpack(mode, case):
-    """conv_opts.reserved[5] = 1: the symmetric unpack follows the literal Eqs. (11)-(15) with
+    """conv_opts.unpack_form = UNPACK_LITERAL: the symmetric unpack follows the literal Eqs. (11)-(15) with
     the u_sys guard (PAPER eps, reading C6: exact for R_max < 89,524).  Its integers equal the
     exact integer convolution, so the output equals the oracle's literal-form pipeline and the
     balanced-digit output bit for bit."""
@@ -645,7 +647,7 @@ def test_literal_paper_unpack(mode, case):
     ref = O.conv_pipeline(s, k, W_block, O.SYM, Q, mode=mode, eps_rule=O.EPS_PAPER, unpack_form="paper")
     assert ref.mismatches == 0
     opts = pcb.opts_default(eps_rule=EPS[O.EPS_PAPER], rmax_rule=O.RMAX_PAPER, bound_policy=pcb.BOUND_WARN)
-    opts.reserved[5] = 1
+    opts.unpack_form = pcb.UNPACK_LITERAL
     with pcb.Plan(L, N, W_block, pcb.MODE_XCORR if mode == O.XCORR else pcb.MODE_CONV, pcb.PACK_SYM, Q,
                   opts=opts) as p:
         p.set_kernel(dev(k))
@@ -720,8 +722,8 @@ def test_xcorr_pairs_per_pair_kernels(packing, Q):
 @pytest.mark.parametrize("mode", [O.CONV, O.XCORR])
 def test_dmma_core_variants(opt, packing, mode):
     """The DMMA-core kernel's alternative schedules give bit-identical results: a2-a4 in a
-    prepack kernel ahead of it (conv_opts.reserved[8] = 2), a bounded producer claim-ahead
-    (reserved[7] = -2), integer-pipe companding and packing (reserved[6] = 1), and the auto
+    prepack kernel ahead of it (conv_opts.prepack = 1), a bounded producer claim-ahead
+    (stage_cap = -2), integer-pipe companding and packing (pack_alu = 1), and the auto
     core choice (DMMA, FMA for symmetric packing)."""
     L, N, W_block, Q = 90_000, 301, 4096, 31
     rng = np.random.default_rng(packing * 7 + mode)
@@ -730,11 +732,11 @@ def test_dmma_core_variants(opt, packing, mode):
     ref = O.conv_pipeline(s, k, W_block, packing, Q, mode=mode)
     opts = pcb.opts_default(bound_policy=pcb.BOUND_WARN, exec=2)
     if opt == "prepack":
-        opts.reserved[2], opts.reserved[8] = 2, 2
+        opts.core_variant, opts.prepack = 2, 1
     elif opt == "lookahead":
-        opts.reserved[2], opts.reserved[7] = 2, -2
+        opts.core_variant, opts.stage_cap = 2, -2
     elif opt == "alu_pack":
-        opts.reserved[2], opts.reserved[6] = 2, 1
+        opts.core_variant, opts.pack_alu = 2, 1
     with pcb.Plan(L, N, W_block, mode, PK[packing], Q, opts=opts) as p:
         p.set_kernel(dev(k))
         info = p.info()
@@ -770,19 +772,20 @@ def test_snr_calibration_matches_oracle(sig, mode):
 
 @pytest.mark.parametrize("early", ["1", "0"])
 @pytest.mark.parametrize("packing", [O.ASYM2, O.FULL])
-def test_back_to_back_launches_early_fill(packing, early, monkeypatch):
+def test_back_to_back_launches_early_fill(packing, early):
     """Consecutive tiled launches on one stream overlap (programmatic dependent launch): a
     launch's pipeline fill may start before the preceding one finished unless it reads what that
     one writes.  Chained (the second convolves the first's output, no sync in between): the
     host check must hold the fill back; independent inputs: it may run early.  Both bit-exact
     (full precision: the same bits as the unchained run)."""
-    monkeypatch.setenv("PC_EARLY_FILL", early)        # opt-in overlap of a launch's fill
     L, N, W_block, Q = 60_000, 129, 2048, 63
     rng = np.random.default_rng(17)
     s, k = np.clip(rng.laplace(0, 0.3, L), -1, 1), rng.uniform(-1, 1, N)
     Q = 0 if packing == O.FULL else Q
-    with pcb.Plan(L, N, W_block, O.CONV, PK[packing], Q, opts=pcb.opts_default(exec=2)) as p1, \
-            pcb.Plan(L + N - 1, N, W_block, O.CONV, PK[packing], Q, opts=pcb.opts_default(exec=2)) as p2:
+    ef = int(early)                                   # opt-in overlap of a launch's fill
+    with pcb.Plan(L, N, W_block, O.CONV, PK[packing], Q, opts=pcb.opts_default(exec=2, early_fill=ef)) as p1, \
+            pcb.Plan(L + N - 1, N, W_block, O.CONV, PK[packing], Q,
+                     opts=pcb.opts_default(exec=2, early_fill=ef)) as p2:
         p1.set_kernel(dev(k))
         p2.set_kernel(dev(k))
         s_d = dev(s)
@@ -874,7 +877,7 @@ def test_fft_core_backend_validation_worst_case(packing, Q):
 @pytest.mark.parametrize("packing,N,mma", [(O.SYM, 513, 0), (O.SYM, 2049, 1), (O.ASYM3, 129, 0), (O.ASYM3, 513, 1),
                                            (O.ASYM2, 129, 1), (O.FULL, 129, 1)])
 def test_auto_core_choice(packing, N, mma):
-    """The auto core rule (conv_opts.reserved[2] = 0): DMMA except short symmetric (< 768 core taps)
+    """The auto core rule (conv_opts.core_variant = 0): DMMA except short symmetric (< 768 core taps)
     and asym3 (< 256) cores, which keep the FMA loop -- the measured crossovers."""
     W_block = 8192
     with pcb.Plan(100_000, N, W_block, pcb.MODE_CONV, PK[packing], 0 if packing == O.FULL else 3,
@@ -882,3 +885,138 @@ def test_auto_core_choice(packing, N, mma):
         p.set_kernel(dev(np.linspace(-1, 1, N)))
         info = p.info()
         assert info["core_mma"] == mma and info["core_tile"] in (12, 14, 16)
+
+
+# --------------------------------------------------------------------- round 2: boundary (§8(b))
+def fft_plan(L, k, packing, Q, policy, fft_n=0, W_block=16384, mode=O.CONV):
+    opts = pcb.opts_default(core=pcb.CORE_FFT, rmax_rule=pcb.RMAX_L1, bound_policy=policy, fft_n=fft_n)
+    p = pcb.Plan(L, len(k), W_block, mode, PK[packing], Q, opts=opts)
+    try:
+        p.set_kernel(dev(k))
+    except Exception:
+        p.close()
+        raise
+    return p
+
+
+def test_fft_backend_validation_at_set_kernel():
+    """conv_plan_set_kernel validates FFT-core plans: at the cfg3 geometry
+    asym2 up to Q = 191 (~8.6 bits) passes -- 4 x the worst last-digit residual <= 0.5 LSB --
+    with a calibrated u_sys; asym2 Q = 285, within its R_max bound (L1 rule), has a worst-case
+    residual near 0.3-0.4 LSB and is refused under STRICT (PC_E_BACKEND, kernel not installed)
+    and accepted under WARN (backend_ok = 0), where executing worst-case data makes the runtime
+    monitor fire (PC_W_UNPACK_MARGIN from conv_execute and conv_plan_residual)."""
+    s, k = WL.cfg3(seed=0, L=1 << 18)
+    for Q in (63, 127, 191):
+        with fft_plan(len(s), k, O.ASYM2, Q, pcb.BOUND_STRICT) as p:
+            info = p.info()
+            assert info["bound_ok"] == 1 and info["backend_ok"] == 1
+            assert 0.0 < info["backend_resid"] <= 0.125 and info["u_sys_cal"] > 0.0
+            print(f"validated asym2 Q={Q}: resid {info['backend_resid']:.4g} LSB, u_sys {info['u_sys_cal']:.4g}")
+    with pytest.raises(pcb.PcError) as ei:
+        fft_plan(len(s), k, O.ASYM2, 285, pcb.BOUND_STRICT, fft_n=4096)
+    assert ei.value.code == pcb.PC_E_BACKEND
+    L = 1 << 20
+    with fft_plan(L, k, O.ASYM2, 285, pcb.BOUND_WARN, fft_n=4096) as p:
+        info = p.info()
+        assert info["bound_ok"] == 1 and info["backend_ok"] == 0 and info["backend_resid"] > 0.125
+        x = dev(np.where(np.random.default_rng(1).random(L) < 0.5, -1.0, 1.0))
+        r = torch.empty(info["L_out"], dtype=torch.float64, device=DEV)
+        p.execute(x, r)
+        torch.cuda.synchronize()
+        with pytest.warns(pcb.UnpackMarginWarning):
+            rc = p.execute(x, r)                  # the completed launch raised the host-mapped flag
+        assert rc == pcb.PC_W_UNPACK_MARGIN
+        torch.cuda.synchronize()
+        res, rc = p.residual(reset=True)
+        assert rc == pcb.PC_W_UNPACK_MARGIN and res > 0.25
+        assert p.execute(x * 0.0, r) == pcb.PC_OK  # flag cleared by the reset
+
+
+def test_direct_plans_skip_backend_validation():
+    s, k = WL.cfg2(seed=0, L=1 << 16)
+    with pcb.Plan(len(s), len(k), 4096, pcb.MODE_CONV, pcb.PACK_ASYM2, 511, rmax_rule=pcb.RMAX_L1) as p:
+        p.set_kernel(dev(k))
+        info = p.info()
+        assert info["backend_ok"] == -1 and info["u_sys_cal"] == 0.0
+
+
+@pytest.mark.parametrize("eps_rule,exact", [(O.EPS_POW2, True), (O.EPS_PAPER, False)])
+def test_debug_max_residual(eps_rule, exact):
+    """conv_execute_debug's max_residual (§8(b)): exactly 0 under the dyadic eps (C4: every
+    packed product exact); under the paper's eps (Eq. (6)) a rounding residual below 0.5 LSB."""
+    rng = np.random.default_rng(9)
+    L, N, W_block, Q = 30000, 65, 1024, 20
+    s, k = np.clip(rng.laplace(0, 0.3, L), -1, 1), rng.uniform(-1, 1, N)
+    opts = pcb.opts_default(eps_rule=EPS[eps_rule], bound_policy=pcb.BOUND_WARN, exec=pcb.EXEC_PERBLOCK)
+    ref = O.conv_pipeline(s, k, W_block, O.SYM, Q, eps_rule=eps_rule)
+    with pcb.Plan(L, N, W_block, pcb.MODE_CONV, pcb.PACK_SYM, Q, opts=opts) as p:
+        p.set_kernel(dev(k))
+        r = torch.empty(p.info()["L_out"], dtype=torch.float64, device=DEV)
+        res = p.execute_debug(dev(s), r, max_residual=True)
+        assert np.array_equal(r.cpu().numpy(), ref.out)
+    if exact:
+        assert res == 0.0
+    else:
+        assert 0.0 < res < 0.5
+
+
+def test_binding_rejects_bad_device_buffers():
+    """No lengths cross the C ABI, so the binding refuses wrong dtype / short / strided / host
+    buffers before any launch (PC_E_CONFIG)."""
+    s, k = WL.cfg1(seed=0, L=8192)
+    with pcb.Plan(len(s), len(k), 1024, pcb.MODE_CONV, pcb.PACK_ASYM2, 127) as p:
+        p.set_kernel(dev(k))
+        Lo = p.info()["L_out"]
+        good_s, good_r = dev(s), torch.empty(Lo, dtype=torch.float64, device=DEV)
+        bad = [(good_s.float(), good_r), (good_s[:-1], good_r), (good_s, good_r[:-1]),
+               (torch.empty(2 * len(s), dtype=torch.float64, device=DEV)[::2], good_r),
+               (torch.from_numpy(s), good_r)]
+        for a, b in bad:
+            with pytest.raises(pcb.PcError) as ei:
+                p.execute(a, b)
+            assert ei.value.code == pcb.PC_E_CONFIG
+        with pytest.raises(pcb.PcError):
+            p.execute(good_s, good_s)                 # in place: s and r overlap
+        with pytest.raises(pcb.PcError):
+            p.set_kernel(dev(k[:-1]))
+        assert p.execute(good_s, good_r) == pcb.PC_OK
+
+
+@pytest.mark.parametrize("floor", [35.0, 65.0])      # sym + asym2 blocks; asym2 + full blocks
+def test_adaptive_block_lists_many_blocks(floor):
+    """pc_adapt_lists' compaction across warps and rounds (P > 4096 blocks, two packings
+    interleaved per floor): every output is written (NaN-filled buffer) and equals the oracle's adaptive
+    pipeline (packed blocks bit-exact, full-precision blocks within 1e-12)."""
+    rng = np.random.default_rng(11)
+    N, W_block = 33, 128                              # W = 94: P = 5200 blocks
+    P = 5200
+    L = P * 94
+    scale = np.repeat(10.0 ** rng.uniform(-2, 0, P + 1), 94)[:L]
+    s = rng.laplace(0, 1.0, L) * scale
+    k = rng.normal(0, 1 / np.sqrt(N), N)
+    y_ref, dec_ref, qmode = O.adaptive_pipeline(s, k, W_block, floor)
+    modes = {m for m, _, _ in dec_ref}
+    assert len(modes) >= 2, modes
+    with pcb.Plan(L, N, W_block, pcb.MODE_CONV, pcb.PACK_ADAPTIVE, 0, rmax_rule=pcb.RMAX_L1) as p:
+        p.set_kernel(dev(k))
+        info = p.info()
+        assert info["P"] > 4096
+        s_d = dev(s)
+        dec = p.adapt_block(s_d, floor)
+        assert [(d[0], d[1]) for d in dec] == [(PK[m], q) for m, q, _ in dec_ref]
+        r = torch.full((info["L_out"],), float("nan"), dtype=torch.float64, device=DEV)
+        p.execute(s_d, r)
+        torch.cuda.synchronize()
+        got = r.cpu().numpy()
+    assert not np.isnan(got).any()
+    geom = O.Geometry(L, N, W_block)
+    for w, (m, q, _) in enumerate(dec_ref):
+        g0 = geom.block_start(w)
+        o0, n_out = geom.kept(w)
+        lo, hi = g0 + o0, min(g0 + o0 + n_out, geom.L_out)
+        if m == O.FULL:
+            scl = max(np.max(np.abs(y_ref[lo:hi])), 1e-300)
+            assert np.max(np.abs(got[lo:hi] - y_ref[lo:hi])) / scl < 1e-12, w
+        else:
+            assert np.array_equal(got[lo:hi], y_ref[lo:hi]), w

@@ -1,7 +1,7 @@
 """Per-CTA timeline of the tiled persistent kernel (conv_execute_profile): how many CTAs are
 resident per SM over time, per-job core durations, fill, and consumer cycle split.
     python tools/tiled_timeline.py [workload=cfg2] [L] > out.json
-    PC_OPT="2=1,3=4" sets conv_opts.reserved[i] = v (e.g. 2=1: the FP64 FMA core)"""
+    PC_OPT="core_variant=1,parts_per_job=4" sets named conv_opts fields (e.g. core_variant=1: the FP64 FMA core)"""
 import json
 import os
 import sys
@@ -37,8 +37,8 @@ out = {}
 for name, (pk, Q, rm) in points.items():
     o = pcb.opts_default(rmax_rule=rm)
     for kv in filter(None, os.environ.get("PC_OPT", "").split(",")):
-        i, v = kv.split("=")
-        o.reserved[int(i)] = int(v)
+        f, v = kv.split("=")
+        setattr(o, f, int(v))
     with pcb.Plan(len(s), len(k), W_block, 0, pk, Q, opts=o) as p:
         p.set_kernel(torch.from_numpy(k).to(dev))
         for _ in range(3):
