@@ -1020,3 +1020,76 @@ def test_adaptive_block_lists_many_blocks(floor):
             assert np.max(np.abs(got[lo:hi] - y_ref[lo:hi])) / scl < 1e-12, w
         else:
             assert np.array_equal(got[lo:hi], y_ref[lo:hi]), w
+
+
+@pytest.mark.parametrize("mode", [O.CONV, O.XCORR])
+def test_execute_host_blocks_shards(mode):
+    """conv_execute_host_blocks (a rank's shard through host buffers): the shards'
+    host outputs assemble to the oracle's output bit for bit (pipelined and one-pass ranges)."""
+    rng = np.random.default_rng(21)
+    L, N, W_block, Q = 300_000, 129, 1024, 127
+    s, k = rng.laplace(0, 0.2, L), rng.uniform(-1, 1, N)
+    ref = O.conv_pipeline(s, k, W_block, O.ASYM2, Q, mode=mode)
+    with pcb.Plan(L, N, W_block, mode, pcb.PACK_ASYM2, Q) as p:
+        p.set_kernel(dev(k))
+        info = p.info()
+        for G in (1, 2, 5):
+            out = np.full(info["L_out"], np.nan)
+            for rank in range(G):
+                sh = pcb.shard_range(L, N, W_block, mode, rank, G)
+                sh_h = torch.from_numpy(s[sh["in_begin"]:sh["in_end"]].copy()).pin_memory()
+                rh = torch.full((max(1, sh["out_end"] - sh["out_begin"]),), float("nan"), dtype=torch.float64)
+                assert p.execute_host_blocks(sh_h, sh["in_begin"], rh, sh["out_begin"], sh["block_begin"],
+                                             sh["block_end"]) == pcb.PC_OK
+                out[sh["out_begin"]:sh["out_end"]] = rh.numpy()[:sh["out_end"] - sh["out_begin"]]
+            assert np.array_equal(out, ref.out), G
+
+
+def test_adapt_blocks_shards_equal_whole():
+    """conv_adapt_blocks + conv_execute_blocks on block-range shards (cfg5's multi-GPU split):
+    every shard's decisions equal the whole-signal decisions of its blocks, and the assembled
+    output is bit-identical to the single adaptive run."""
+    s, k = WL.cfg5(seed=2, L=1 << 18, N=1024)
+    W_block, floor = 4096, 40.0
+    L, N = len(s), len(k)
+    with pcb.Plan(L, N, W_block, pcb.MODE_CONV, pcb.PACK_ADAPTIVE, 0, rmax_rule=pcb.RMAX_L1) as p:
+        p.set_kernel(dev(k))
+        info = p.info()
+        s_d = dev(s)
+        whole = p.adapt_block(s_d, floor)
+        r = torch.empty(info["L_out"], dtype=torch.float64, device=DEV)
+        p.execute(s_d, r)
+        torch.cuda.synchronize()
+        want = r.cpu().numpy()
+        for G in (2, 3):
+            out = np.full(info["L_out"], np.nan)
+            for rank in range(G):
+                sh = pcb.shard_range(L, N, W_block, 0, rank, G)
+                xs = dev(s[sh["in_begin"]:sh["in_end"]])
+                dec = p.adapt_blocks(xs, sh["in_begin"], sh["block_begin"], sh["block_end"], floor, want=True)
+                assert dec == whole[sh["block_begin"]:sh["block_end"]]
+                n = sh["out_end"] - sh["out_begin"]
+                rs = torch.full((max(1, n),), float("nan"), dtype=torch.float64, device=DEV)
+                p.execute_blocks(xs, sh["in_begin"], rs, sh["out_begin"], sh["block_begin"], sh["block_end"])
+                torch.cuda.synchronize()
+                out[sh["out_begin"]:sh["out_end"]] = rs.cpu().numpy()[:n]
+                with pytest.raises(pcb.PcError) as ei:       # blocks outside the decided range
+                    p.execute(s_d, r)
+                assert ei.value.code == pcb.PC_E_STATE
+            assert np.array_equal(out, want), G
+
+
+def test_best_match_kernel():
+    """conv_best_match (the database winner, C17): largest score, ties to the smallest index,
+    over per-signal arrays and over gathered candidate rows."""
+    rng = np.random.default_rng(4)
+    n = 3000
+    sc = np.round(rng.normal(0, 1, n), 1)                  # many ties
+    lg = rng.integers(0, 1 << 20, n)
+    best = torch.empty(3, dtype=torch.float64, device=DEV)
+    pcb.best_match(best, n, score_dev=dev(sc), lag_dev=dev(lg), first_index=77)
+    i = int(np.flatnonzero(sc == sc.max())[0])
+    assert best.cpu().tolist() == [sc[i], float(lg[i]), float(77 + i)]
+    cand = np.array([[1.0, 5, 9], [2.0, 6, 4], [2.0, 7, 3], [-1.0, 8, 0]])
+    pcb.best_match(best, 4, cand_dev=dev(cand.reshape(-1)))
+    assert best.cpu().tolist() == [2.0, 7.0, 3.0]

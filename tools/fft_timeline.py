@@ -1,6 +1,6 @@
 """Per-job phase times of the FFT core (conv_execute_profile on an FFT plan): median us of
 peak, packing, forward FFT, spectrum product, inverse FFT, unpack+store.
-    python tools/fft_timeline.py [L]"""
+    python tools/fft_timeline.py [L] [fft_n ...]"""
 import json
 import sys
 
@@ -17,8 +17,11 @@ dev = torch.device("cuda")
 S, R = torch.from_numpy(s).to(dev), torch.empty(len(s) + len(k) - 1, dtype=torch.float64, device=dev)
 rec = torch.zeros(8 * 4096 + 64, dtype=torch.int64, device=dev)
 out = {}
-for name, (pk, Q, rm) in {"asym2_9b": (2, 255, 1), "full": (0, 0, 0)}.items():
-    opts = pcb.opts_default(rmax_rule=rm, core=1)
+sizes = [int(x) for x in sys.argv[2:]] or [0]
+cases = {f"{nm}_n{n}": (pk, Q, rm, n) for n in sizes for nm, (pk, Q, rm) in
+         {"asym2_q191": (2, 191, 1), "full": (0, 0, 0)}.items()}
+for name, (pk, Q, rm, fn) in cases.items():
+    opts = pcb.opts_default(rmax_rule=rm, core=1, fft_n=fn)
     with pcb.Plan(len(s), len(k), 16384, 0, pk, Q, opts=opts) as p:
         p.set_kernel(torch.from_numpy(k).to(dev))
         for _ in range(3):
@@ -28,6 +31,7 @@ for name, (pk, Q, rm) in {"asym2_9b": (2, 255, 1), "full": (0, 0, 0)}.items():
         torch.cuda.synchronize()
         n = min(g, 4096)
         a = rec[:8 * n].view(n, 8).cpu().numpy().astype(np.int64)
+        a = a[a[:, 7] != 0]                                  # records of jobs that exist
         fft_n = p.info()["fft_n"]
     d = np.diff(a[:, 1:], axis=1) / 1e3
     t0 = a[:, 1].min()
