@@ -97,6 +97,8 @@ struct conv_plan {
   int* h_status = nullptr;             // host view
   int* d_status = nullptr;             // device view of the same memory
   double* d_dbg_resid = nullptr;       // conv_execute_debug: max last-digit residual
+  double* d_blkpeak = nullptr;         // block peaks ahead of the persistent kernel [n_sig][P]
+  long long blkpeak_cap = 0;
 };
 
 namespace {
@@ -518,6 +520,9 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
         const TShape& t = sh3[i];
         Exec el = e;
         el.dec_pack = nullptr;
+        el.blk_peak = p->d_peak;                        // a2 done by pc_block_stats (same max|x|)
+        el.peak_stride = 0;
+        el.early_fill = 0;
         el.blk_list = p->d_lists + (size_t)pk * p->P;
         el.blk_count = p->d_counts + pk;
         el.sm_ctr = p->d_counter;
@@ -583,10 +588,31 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
       e.pre_inv = p->d_pre + njobs * stride;
       if (pc::launch_prepack(p->packing, ts.T, ts.mma, make_geo(p), e, njobs, st) != cudaSuccess) return PC_E_CUDA;
     }
+    // a2 ahead (PC_PEAK_AHEAD builds): the block peaks of this launch's blocks in one bandwidth-bound
+    // pass, so the producers only compand and pack (their peak pass runs 3-6x slower next to the
+    // DMMA warps).  Peaks for free: adaptive plans (pc_block_stats), below.
+#ifndef PC_PEAK_AHEAD
+#define PC_PEAK_AHEAD 0   // measured: the extra pass costs more per step (cfg2 asym2 100.6 vs 95.1 us) than it
+#endif                    // saves in the persistent kernel (89.3 vs 92.6 us); adaptive plans reuse pc_block_stats'
+    if (PC_PEAK_AHEAD && p->packing != PC_PACK_FULL && !e.pre_win) {
+      const long long need = n_sig * p->P;
+      if (need > p->blkpeak_cap) {
+        cudaFree(p->d_blkpeak);
+        p->d_blkpeak = nullptr;
+        p->blkpeak_cap = 0;
+        if (cudaMalloc(&p->d_blkpeak, sizeof(double) * need) != cudaSuccess) return PC_E_CUDA;
+        p->blkpeak_cap = need;
+      }
+      if (pc::launch_block_peak(make_geo(p), s, s_off, s_stride, b0, nblk, n_sig, p->d_blkpeak, p->P, st) !=
+          cudaSuccess)
+        return PC_E_CUDA;
+      e.blk_peak = p->d_blkpeak;
+      e.peak_stride = p->P;
+    }
     // every address this launch may read as input / write as output (rows sig < n_sig)
     const uintptr_t in_lo = (uintptr_t)(s - s_off), in_hi = (uintptr_t)(s - s_off + (n_sig - 1) * s_stride + p->L);
     const uintptr_t out_lo = (uintptr_t)(r - r_off - p->N), out_hi = (uintptr_t)(r - r_off + (n_sig - 1) * r_stride + p->L + 2 * p->N);
-    e.early_fill = !timing && !e.pre_win && early_fill_ok(p, st, in_lo, in_hi);
+    e.early_fill = !timing && !e.pre_win && !e.blk_peak && early_fill_ok(p, st, in_lo, in_hi);
     e.early_claim = 1;                                 // claims touch only this launch's queue array
     int grid = 0;
     cudaError_t err = pc::launch_tiled(p->packing, ts.T, ts.mma, make_geo(p), e, njobs, ts.threads, ts.smem, st, &grid);
@@ -784,6 +810,7 @@ void conv_plan_destroy(conv_plan* p) {
   cudaFree(p->d_H);
   cudaFree(p->d_resid);
   cudaFree(p->d_dbg_resid);
+  cudaFree(p->d_blkpeak);
   if (p->h_status) cudaFreeHost(p->h_status);
   delete p;
 }

@@ -537,6 +537,65 @@ __global__ void pc_xcorr_max(const double* __restrict__ c, long long n_lags, lon
   }
 }
 
+// ------------------------------------------------------------------ a2 ahead of the tiled core
+// One CTA per (signal, block): p_w = max |x| over the block's W_block samples (reading C7),
+// every load in flight at once, integer max of the |x| bits (non-negative doubles order like
+// their bit patterns).  Lets the persistent kernel's producers skip the peak pass, which ran 3-6x
+// slower next to the DMMA warps (profiles/r01_dmma_interference.log).  Triggers dependent launches
+// at entry: the tiled kernel's prologue overlaps it and its griddepcontrol.wait covers the peaks.
+constexpr int kPeakThreads = 256, kPeakU = 8;
+__global__ void __launch_bounds__(kPeakThreads) pc_block_peak(Geo g, const double* __restrict__ s, long long s_off,
+                                                              long long s_stride, long long b0, long long nblk,
+                                                              double* __restrict__ peak, long long peak_stride) {
+  __shared__ unsigned long long ired[kPeakThreads / 32];
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const long long sig = blockIdx.x / nblk, w = b0 + blockIdx.x % nblk;
+  const long long g0 = (w == 0) ? 0 : w * (long long)g.W - 2;
+  const long long avail = g.L - g0;
+  const int n_valid = (int)(avail < 0 ? 0 : (avail > g.W_block ? g.W_block : avail));
+  const double* src = s + sig * s_stride + (g0 - s_off);
+  const int tid = threadIdx.x;
+  unsigned long long m = 0ull;
+  if ((reinterpret_cast<uintptr_t>(src) & 15u) == 0) {
+    const double2* s2 = reinterpret_cast<const double2*>(src);
+    const int n2 = n_valid / 2;
+    for (int i0 = tid; i0 < n2; i0 += kPeakU * kPeakThreads) {
+      double2 v[kPeakU];
+#pragma unroll
+      for (int u = 0; u < kPeakU; ++u) {
+        const int i = i0 + u * kPeakThreads;
+        v[u] = (i < n2) ? __ldg(s2 + i) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < kPeakU; ++u) {
+        const unsigned long long a = (unsigned long long)__double_as_longlong(v[u].x) & 0x7fffffffffffffffull;
+        const unsigned long long b = (unsigned long long)__double_as_longlong(v[u].y) & 0x7fffffffffffffffull;
+        m = a > m ? a : m;
+        m = b > m ? b : m;
+      }
+    }
+    if ((n_valid & 1) && tid == 0) {
+      const unsigned long long a = (unsigned long long)__double_as_longlong(src[n_valid - 1]) & 0x7fffffffffffffffull;
+      m = a > m ? a : m;
+    }
+  } else {
+    for (int i = tid; i < n_valid; i += kPeakThreads) {
+      const unsigned long long a = (unsigned long long)__double_as_longlong(__ldg(src + i)) & 0x7fffffffffffffffull;
+      m = a > m ? a : m;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long x = __shfl_xor_sync(0xffffffffu, m, o);
+    m = x > m ? x : m;
+  }
+  if ((tid & 31) == 0) ired[tid >> 5] = m;
+  __syncthreads();
+  if (tid == 0) {
+    for (int i = 1; i < kPeakThreads / 32; ++i) m = ired[i] > m ? ired[i] : m;
+    peak[sig * peak_stride + w] = __longlong_as_double((long long)m);
+  }
+}
+
 // ------------------------------------------------------------------ database winner (a9)
 // One CTA: the largest score, ties to the smallest index (reading C17), over candidates
 // (score[i], lag[i], first + i) or the rows {score, lag, index} of cand.
@@ -785,6 +844,13 @@ cudaError_t launch_fill_pm1(double* x, long long n, unsigned long long seed, cud
 cudaError_t launch_best_match(const double* score, const long long* lag, const double* cand, long long n,
                               long long first_index, double* best, cudaStream_t st) {
   pc_best_match<<<1, 1024, 0, st>>>(score, lag, cand, n, first_index, best);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_block_peak(const Geo& g, const double* s, long long s_off, long long s_stride, long long b0,
+                              long long nblk, long long n_sig, double* peak, long long peak_stride, cudaStream_t st) {
+  if (nblk <= 0 || n_sig <= 0) return cudaSuccess;
+  pc_block_peak<<<(unsigned)(nblk * n_sig), kPeakThreads, 0, st>>>(g, s, s_off, s_stride, b0, nblk, peak, peak_stride);
   return cudaGetLastError();
 }
 

@@ -22,7 +22,14 @@ constexpr int kTiledProdWarps = PC_PROD_WARPS;   // tiled kernel: producer warps
 #ifndef PC_FILL_JOBS
 #define PC_FILL_JOBS 4
 #endif
-constexpr int kTiledFillJobs = PC_FILL_JOBS;   // tiled kernel: jobs packed by all warps before the consumers start
+constexpr int kTiledFillJobs = PC_FILL_JOBS;   // tiled kernel: fill groups (warps split into this many job packers)
+#ifndef PC_FILL_MAX
+#define PC_FILL_MAX 4
+#endif
+// tiled kernel: jobs packed by all warps before the consumers start (up to the ring's stages and
+// the CTA's share of the launch): a launch of <= NS jobs per SM never runs producers next to
+// DMMA warps (whose issue slowed producers 3-6x, profiles/r01_dmma_interference.log)
+constexpr int kTiledFillMax = PC_FILL_MAX;
 #ifndef PC_CONS_WARPS
 #define PC_CONS_WARPS 12
 #endif
@@ -45,8 +52,10 @@ struct LaunchAttrCache {
   std::mutex mu;
   size_t smem[kMaxDevices] = {};
   int sms[kMaxDevices] = {};
+  int occ[kMaxDevices] = {};             // resident CTAs per SM at the largest `need` seen
   template <class F>
-  cudaError_t ensure(F* kfn, int dev, size_t need, int threads, int* sms_out, bool check_occ = true) {
+  cudaError_t ensure(F* kfn, int dev, size_t need, int threads, int* sms_out, bool check_occ = true,
+                     int* occ_out = nullptr) {
     if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
     std::lock_guard<std::mutex> lk(mu);
     if (sms[dev] == 0) {
@@ -57,14 +66,16 @@ struct LaunchAttrCache {
       cudaError_t err = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need);
       if (err != cudaSuccess) return err;
       if (check_occ) {                                 // (cluster kernels: checked at launch)
-        int occ = 0;
-        err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, threads, need);
+        int o = 0;
+        err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kfn, threads, need);
         if (err != cudaSuccess) return err;
-        if (occ < 1) return cudaErrorInvalidConfiguration;
+        if (o < 1) return cudaErrorInvalidConfiguration;
+        occ[dev] = o;
       }
       smem[dev] = need;
     }
     *sms_out = sms[dev];
+    if (occ_out) *occ_out = occ[dev] > 0 ? occ[dev] : 1;
     return cudaSuccess;
   }
 };
@@ -141,6 +152,10 @@ struct Exec {
   // persistent-kernel wait timed out and the launch abandoned its work
   int* status;
   double* dbg_resid;    // conv_execute_debug: max last-digit residual (LSB, atomicMax on the bits)
+  // tiled kernel: block peaks max|x| computed ahead (pc_block_peak, or pc_block_stats for adaptive
+  // plans) at blk_peak[sig * peak_stride + w]; nullptr: the producers compute them
+  const double* blk_peak;
+  long long peak_stride;
 };
 constexpr int kStatusMargin = 0, kStatusWatchdog = 1;
 
@@ -193,6 +208,10 @@ cudaError_t launch_snr_sums(const double* ref, const double* x, long long n, con
                             long long P, double sig_k, double peak_k, double Q, double* out, cudaStream_t st);
 cudaError_t launch_best_match(const double* score, const long long* lag, const double* cand, long long n,
                               long long first_index, double* best, cudaStream_t st);
+// Per-block peak max|x| of blocks [b0, b0 + nblk) of n_sig signals (rows s + sig * s_stride, global
+// sample base s - s_off) into peak[sig * peak_stride + w].
+cudaError_t launch_block_peak(const Geo& g, const double* s, long long s_off, long long s_stride, long long b0,
+                              long long nblk, long long n_sig, double* peak, long long peak_stride, cudaStream_t st);
 cudaError_t launch_fill_pm1(double* x, long long n, unsigned long long seed, cudaStream_t st);
 cudaError_t launch_xcorr_max(const double* c, long long n_signals, long long n_lags, long long stride,
                              double* score, long long* lag, cudaStream_t st);

@@ -250,6 +250,13 @@ __device__ __forceinline__ double block_cs(const ModeP& mp, const double* gsrc, 
   return (peak == 0.0) ? 1.0 : mp.Q / peak;
 }
 
+// c_s from a block peak computed ahead (pc_block_peak / pc_block_stats): the same IEEE division.
+template <int PACK>
+__device__ __forceinline__ double cs_from_peak(const ModeP& mp, double peak) {
+  if (PACK == PACK_FULL) return 1.0;
+  return (peak == 0.0) ? 1.0 : mp.Q / peak;
+}
+
 // The same for one warp (producer warps work on different jobs): shuffles only.
 template <int PACK>
 __device__ __forceinline__ double warp_cs(const ModeP& mp, const double* gsrc, int n_valid, int lane) {
@@ -573,7 +580,7 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
     const long long nq_ = nj / PC_QUEUE_MIN;
     const long long nq = nq_ < 1 ? 1 : (nq_ > (long long)gridDim.x ? (long long)gridDim.x : nq_);
     const long long q = blockIdx.x % nq, lo = nj * q / nq, hi = nj * (q + 1) / nq;
-    for (long long jb = lo; jb < hi && jb < lo + kTiledFillJobs; ++jb) {
+    for (long long jb = lo; jb < hi && jb < lo + kTiledFillMax; ++jb) {
       const JobPos jp = job_pos(e, jb);
       const Blk b = block_info<PACK>(g, mp.K, jp.w);
       const long long avail = g.L - b.g0;
@@ -634,12 +641,12 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
     }
   };
 
-  // Pipeline fill: the first nf jobs (one per producer warp when a job is one stage) are
-  // claimed in parallel (before griddepcontrol.wait: only this launch's queue array is touched),
-  // then companded and packed by all 16 warps, four per job.
+  // Pipeline fill: the first nf jobs (up to the ring's stages and the CTA's share) are claimed in
+  // parallel (before griddepcontrol.wait: only this launch's queue array is touched), then
+  // companded and packed by all 16 warps in four groups of four warps.
   // (never more than a CTA's share of the launch: small launches spread over all CTAs)
   const long long share = (njobs + gridDim.x - 1) / gridDim.x;
-  const int nf = e.pre_win ? 0 : (nch == 1) ? (int)min((long long)min(kTiledFillJobs, NS), share < 1 ? 1 : share) : 1;
+  const int nf = e.pre_win ? 0 : (nch == 1) ? (int)min((long long)min(kTiledFillMax, NS), share < 1 ? 1 : share) : 1;
   const int lane_ = tid & 31, warp_ = tid >> 5;
   if (warp_ < nf) {
     const long long j = claim_job(e, njobs, lane_);
@@ -672,7 +679,8 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
                                      : nullptr;
       if (frec) frec[0] = gtimer();
       double* xs_f = stg + (size_t)((f * nch) % NS) * stage_words;
-      const double cs = block_cs<PACK>(mp, gsrc, n_valid, ps->red + 8 * gq, gtid, GW * 32, 1 + gq);
+      const double cs = e.blk_peak ? cs_from_peak<PACK>(mp, e.blk_peak[jp.sig * e.peak_stride + jp.w])
+                                   : block_cs<PACK>(mp, gsrc, n_valid, ps->red + 8 * gq, gtid, GW * 32, 1 + gq);
       if (frec) frec[1] = gtimer();
       pack_window<PACK, T, 1, PT>(g, b, mp, gsrc, n_valid, cs, jp.t * G * T - front * T, rows_s, xs_f, gtid,
                                   GW * 32);
@@ -763,7 +771,8 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
         const long long blk_id = jp.sig * g.P + jp.w;
         if (blk_id != cur_blk_w && !e.pre_win) {
           cur_blk_w = blk_id;
-          c_s_w = warp_cs<PACK>(mp, gsrc, n_valid, lane);   // a2/a3 (Eq. (2))
+          c_s_w = e.blk_peak ? cs_from_peak<PACK>(mp, e.blk_peak[jp.sig * e.peak_stride + jp.w])
+                             : warp_cs<PACK>(mp, gsrc, n_valid, lane);   // a2/a3 (Eq. (2))
           inv_w = dequant_scale(c_s_w, e.scal_sig ? e.scal_sig[3 * jp.sig + 1] : mp.c_k);   // Eq. (16)
         }
       }
