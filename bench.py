@@ -617,7 +617,7 @@ def ncu_traffic(kname_prefix, prof_names):
         if not os.path.exists(path):
             continue
         for recd in json.load(open(path)).get("ncu_full", []):
-            if recd["kernel"].startswith(kname_prefix):
+            if kname_prefix in recd["kernel"]:
                 mult = {"Mbyte": 1e6, "Kbyte": 1e3, "Gbyte": 1e9, "byte": 1.0}
                 rd, wr = recd["dram__bytes_read.sum"].split(), recd["dram__bytes_write.sum"].split()
                 return float(rd[0]) * mult[rd[1]] + float(wr[0]) * mult[wr[1]], f"profiles/{prof} (ncu --set full)"

@@ -146,6 +146,19 @@ struct TwSmem2 {
   const double2* hi;
   __device__ __forceinline__ double2 operator()(int m) const { return cmul(hi[m >> 6], lo[m & 63]); }
 };
+// The real-FFT split/merge twiddle W_k = exp(-2 pi i k / 2N), k <= N, from the N-point table:
+// even k = 2m is w^m; odd k = 2m + 1 is w^m * exp(-pi i / N) (one more product).  Replaces a
+// global-table load per pair (the product phase was bound by its table loads).
+struct TwHalf {
+  TwSmem2 t;
+  double2 c1;                                        // exp(-pi i / N), correctly rounded
+  int N;
+  __device__ __forceinline__ double2 operator()(int k) const {
+    if (k >= N) return make_double2(-1.0, 0.0);       // k = N: exp(-pi i)
+    const double2 w = t(k >> 1);
+    return (k & 1) ? cmul(w, c1) : w;
+  }
+};
 
 }  // namespace
 
@@ -268,7 +281,7 @@ __device__ void spectrum_product(double2* s, const double2* __restrict__ H, cons
       Zk[u] = s[pidx(kk)];
       Zkp[u] = s[pidx(kp)];
       Wk[u] = tw2(kk);                                // exp(-2 pi i k / 2N)
-      Wkp[u] = tw2(kp);
+      Wkp[u] = make_double2(-Wk[u].x, Wk[u].y);       // exp(-2 pi i (N-k) / 2N) = -conj(W_k)
       Hk[u] = __ldg(H + kk);
       Hkp[u] = __ldg(H + kp);
     }
@@ -482,7 +495,7 @@ __global__ void __launch_bounds__(N / 16, (N <= 4096 ? PC_FFT_MINB : 1)) pc_fft_
   const TwSmem2 tws{tw_lo, tw_hi};
   fft_smem<N, -1>(sm, tws);                                         // a5: forward
   stamp(4);
-  spectrum_product<N>(sm, f.H, TwGlobal{f.tw2});
+  spectrum_product<N>(sm, f.H, TwHalf{tws, __ldg(f.tw2 + 1), N});
   stamp(5);
   fft_smem<N, +1>(sm, tws);                                         // a5: inverse
   stamp(6);
