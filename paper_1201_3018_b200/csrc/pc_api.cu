@@ -1083,11 +1083,15 @@ int conv_execute_host_blocks(conv_plan* p, const double* s_host, int64_t s_offse
   // sample twice over the link -- and storing outputs straight to pinned memory 1.07-1.36 ms,
   // against 1.04 ms for this copy pipeline; the link's duplex floor is 0.71 ms.)
   // (15 ranges 1:1:2:..:2:1:1 measured 0.98-1.00 ms at cfg2 against 1.04-1.05 for 1:2:4:4:4:4:4:2:1
-  // and 1.01-1.02 for 16 equal ranges)
-  static const int kW[15] = {1, 1, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2, 1, 1};
-  const int nchunk = (p->packing == PC_PACK_ADAPTIVE || B1 - B0 < 128) ? 1 : 15;
-  long long cum[16] = {0};
-  for (int i = 0; i < 15; ++i) cum[i + 1] = cum[i] + kW[i];
+  // and 1.01-1.02 for 16 equal ranges; round 2, another box: 1.04 ms against 1.03 for 1:2:3:3:2:1,
+  // 1.03 for 1:3:3:1, 1.07 for 1:2:..:2:1 (8), 1.12 for 12 equal -- the copy engines' duplex floor
+  // for the 64 MB is 0.71 ms, profiles/r02/pcie_e2e.log)
+  static const int kW[] = {1, 1, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2, 2, 1, 1};
+  constexpr int kNW = (int)(sizeof(kW) / sizeof(kW[0]));
+  static_assert(kNW <= 16, "event pairs");
+  const int nchunk = (p->packing == PC_PACK_ADAPTIVE || B1 - B0 < 128) ? 1 : kNW;
+  long long cum[17] = {0};
+  for (int i = 0; i < kNW; ++i) cum[i + 1] = cum[i] + kW[i];
   const long long nb = B1 - B0;
   if (nchunk <= 1) {
     const long long i1 = in_end_of(B1), o1 = out_end_of(B1);
