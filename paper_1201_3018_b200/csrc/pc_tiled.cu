@@ -53,6 +53,7 @@ namespace {
 struct TSmem {
   uint64_t bar_taps, full[kTiledMaxStages], empty[kTiledMaxStages];
   long long job[kTiledMaxStages];   // -1: sentinel (no more work)
+  unsigned long long jpos[kTiledMaxStages];   // the job's position (pack_pos): sig << 40 | w << 8 | t
   long long seq[kTiledMaxStages];   // stage sequence number the slot holds
   double inv[kTiledMaxStages];      // (c_s c_k)^-1 of the stage's block (Eq. (16))
   int smsp_ctr[4];                  // consumer warp-job claim counters, one per SM sub-partition
@@ -73,6 +74,16 @@ struct JobPos {
   int t;
 };
 
+__device__ __forceinline__ unsigned long long pack_pos(const JobPos& p) {
+  return ((unsigned long long)p.sig << 40) | ((unsigned long long)p.w << 8) | (unsigned long long)p.t;
+}
+__device__ __forceinline__ JobPos unpack_pos(unsigned long long v) {
+  JobPos p;
+  p.sig = (long long)(v >> 40);
+  p.w = (long long)((v >> 8) & 0xffffffffull);
+  p.t = (int)(v & 0xffull);
+  return p;
+}
 __device__ __forceinline__ JobPos job_pos(const Exec& e, long long job) {
   JobPos p;
   if (e.blk_list) {                                  // adaptive: this launch's blocks, ascending
@@ -145,8 +156,63 @@ __device__ __forceinline__ void pack_window(const Geo& g, const Blk& b, const Mo
     return (i < 0 || i >= n_valid) ? 0.0 : (SRC_SMEM ? gsrc[i] : __ldg(gsrc + i));
   };
   const bool alu = mp.alu_pack;                              // warp-uniform (per plan)
+  // window words [ilo, ihi) whose core word is inside the block's input (cw in [pre, xlen)) and
+  // whose samples are all inside the block's valid samples: there, no per-sample / per-word range
+  // checks (the checks were a fifth of the producers' instructions)
+  int ilo, ihi;
+  {
+    constexpr int MS = (PACK == PACK_ASYM3) ? 3 : 2;
+    if (PACK == PACK_SYM) {
+      ilo = max(0, b.pre - cw0);
+      ihi = min(words, b.xlen - cw0);
+      ihi = n_valid >= 2 ? min(ihi, ((n_valid - 2) >> 1) + b.pre - cw0 + 1) : 0;
+    } else {
+      const int base = b.o0 - (g.Np - 1) + cw0;
+      const int span = (PACK == PACK_FULL) ? 0 : (MS - 1) * b.S;
+      ilo = max(0, max(-cw0, -base));
+      ihi = min(words, min(b.xlen - cw0, n_valid - base - span));
+    }
+  }
   for (int i0 = ptid; i0 < words; i0 += UW * nprod) {
     double v[UW];
+    if (!alu && i0 >= ilo && i0 + (UW - 1) * nprod < ihi) {   // interior: unchecked
+      if (PACK == PACK_SYM) {
+        double x0[UW], x1[UW];
+#pragma unroll
+        for (int u = 0; u < UW; ++u) {
+          const int j = cw0 + i0 + u * nprod - b.pre;
+          x0[u] = SRC_SMEM ? gsrc[2 * j] : __ldg(gsrc + 2 * j);
+          x1[u] = SRC_SMEM ? gsrc[2 * j + 1] : __ldg(gsrc + 2 * j + 1);
+        }
+#pragma unroll
+        for (int u = 0; u < UW; ++u) v[u] = pack_sym(compand1(c_s, x0[u]), compand1(c_s, x1[u]), mp.eps);
+      } else if (PACK == PACK_ASYM2 || PACK == PACK_ASYM3) {
+        constexpr int M = (PACK == PACK_ASYM2) ? 2 : 3;
+        double x[M][UW];
+        const double* src = gsrc + (b.o0 - (g.Np - 1) + cw0 + i0);
+#pragma unroll
+        for (int u = 0; u < UW; ++u)
+#pragma unroll
+          for (int q = 0; q < M; ++q) x[q][u] = SRC_SMEM ? src[q * b.S + u * nprod] : __ldg(src + q * b.S + u * nprod);
+#pragma unroll
+        for (int u = 0; u < UW; ++u) {
+          double a = compand1(c_s, x[M - 1][u]);         // Horner, oracle order
+#pragma unroll
+          for (int q = M - 2; q >= 0; --q) a = __dadd_rn(compand1(c_s, x[q][u]), __dmul_rn(mp.eps, a));
+          v[u] = a;
+        }
+      } else {
+        const double* src = gsrc + (b.o0 - (g.Np - 1) + cw0 + i0);
+#pragma unroll
+        for (int u = 0; u < UW; ++u) v[u] = SRC_SMEM ? src[u * nprod] : __ldg(src + u * nprod);
+      }
+#pragma unroll
+      for (int u = 0; u < UW; ++u) {
+        const int i = i0 + u * nprod;
+        xs[(i / T) * PT + i % T] = v[u];
+      }
+      continue;
+    }
     if (PACK == PACK_SYM) {
       double x0[UW], x1[UW];
 #pragma unroll
@@ -336,21 +402,31 @@ __device__ __noinline__ void mbar_stuck(int* status, int where, long long n, int
   asm volatile("exit;");
 #endif
 }
-// spin-wait step with the same 4-s watchdog (t0 = 0 before the first step)
-__device__ __forceinline__ void spin_wd(int* status, unsigned long long& t0, unsigned ns, int where, long long n,
-                                        int st) {
+// spin-wait step with the same 4-s watchdog; the timer is read every 64th step only (the spin
+// loops of waiting warps were ~13% of the kernel's issued instructions with a read per step,
+// profiles/r02_ncu_cfg2_asym2.json), competing for issue with the DMMA warps
+struct Spin {
+  unsigned n = 0;
+  unsigned long long t0 = 0;
+};
+__device__ __forceinline__ void spin_wd(int* status, Spin& sp, unsigned ns, int where, long long n, int st) {
   __nanosleep(ns);
-  const unsigned long long t = gtimer();
-  if (t0 == 0) t0 = t;
-  else if (t - t0 > kWatchdogNs) mbar_stuck(status, where, n, st, 0u);
+  if ((++sp.n & 63u) == 0u) {
+    const unsigned long long t = gtimer();
+    if (sp.t0 == 0) sp.t0 = t;
+    else if (t - sp.t0 > kWatchdogNs) mbar_stuck(status, where, n, st, 0u);
+  }
 }
 __device__ __forceinline__ void mbar_wait_wd(int* status, uint64_t* bar, uint32_t phase, int where, long long n,
                                              int st) {
-  if (mbar_try(bar, phase)) return;
-  const unsigned long long t0 = gtimer();
-  for (;;) {
-    if (mbar_try(bar, phase)) return;
-    if (gtimer() - t0 > kWatchdogNs) mbar_stuck(status, where, n, st, phase);
+  unsigned long long t0 = 0;
+  for (unsigned i = 1;; ++i) {
+    if (mbar_try(bar, phase)) return;                 // (suspends up to kSuspendHintNs per try)
+    if ((i & 63u) == 0u) {
+      const unsigned long long t = gtimer();
+      if (t0 == 0) t0 = t;
+      else if (t - t0 > kWatchdogNs) mbar_stuck(status, where, n, st, phase);
+    }
   }
 }
 
@@ -623,6 +699,7 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
   auto publish = [&](long long n, int st, int c, long long job, double inv, int ptid) {
     if (ptid == 0) {
       ps->job[st] = job;
+      if (job >= 0) ps->jpos[st] = pack_pos(job_pos(e, job));   // consumers skip the 64-bit divisions
       ps->inv[st] = (job >= 0 && e.pre_win) ? e.pre_inv[job] : inv;
       ps->seq[st] = n;
     }
@@ -731,7 +808,7 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
       } else {
         long long j = -1;
         if (lane == 0) {
-          unsigned long long sp = 0;
+          Spin sp;
           while (*reinterpret_cast<volatile long long*>(&ps->turn) != m) spin_wd(e.status, sp, 256, 5, m, 0);
           // bounded claim-ahead: a job claimed long before any warp can start it is work other
           // SMs can no longer steal (the launch's tail)
@@ -784,7 +861,7 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
         if (n >= NS) {
           if (lane == 0)
           {
-            unsigned long long sp = 0;
+            Spin sp;
             while (*reinterpret_cast<volatile long long*>(&ps->seq[st]) != n - NS) spin_wd(e.status, sp, 256, 7, n, st);
           }
           __syncwarp();
@@ -825,7 +902,7 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
   // one ring lap: a parity wait could then see the slot's previous lap; the sequence number
   // stamped by the producer tells the two apart.
   auto wait_full = [&](long long n, int st) {
-    for (unsigned long long sp = 0;;) {
+    for (Spin sp;;) {
       mbar_wait_wd(e.status, &ps->full[st], (uint32_t)((n / NS) & 1), 2, n, st);
       if (*reinterpret_cast<volatile long long*>(&ps->seq[st]) == n) return;
       spin_wd(e.status, sp, 200, 3, n, st);
@@ -870,7 +947,7 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
       break;
     }
     const double inv = ps->inv[st];
-    const JobPos jp = job_pos(e, job);
+    const JobPos jp = unpack_pos(ps->jpos[st]);
     const Blk b = block_info<PACK>(g, mp.K, jp.w);
     const int ngroups = (b.M_out + T - 1) / T;
     // FMA core: part p = groups [32 p, 32 p + 32) of the tile, one per lane.  DMMA core: the
@@ -907,10 +984,10 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
       if (lane == 0)
         // while the SMSP's producer warp packs, one core slot: a second queued DMMA warp would
         // slow its loads and FP64 ops 3x (tools/dmma_interference.cu)
-        for (unsigned long long sp = 0;
+        for (Spin sp;
              *reinterpret_cast<volatile int*>(&ps->core_serve[smsp]) +
                  (PC_PROD_YIELD && *reinterpret_cast<volatile int*>(&ps->prod_busy[smsp]) ? 1 : PC_CORE_SLOTS) <= cl;)
-          spin_wd(e.status, sp, 64, 8, cl, smsp);
+          spin_wd(e.status, sp, 128, 8, cl, smsp);
       if (wrec) wrec[0] |= ((gtimer() - wrec[1]) >> 4) << 32;   // diagnostics: token wait (16 ns units)
       __syncwarp();
     }
@@ -997,10 +1074,18 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
     };
     auto flush = [&](double* dst, int step, long long jlo, long long jhi) {
       __syncwarp();
+      if (jlo <= 0 && jhi >= 32 * T) {                      // the whole run is valid (most runs)
 #pragma unroll
-      for (int it = 0; it < T; ++it) {
-        const int j = lane + 32 * it;
-        if (j >= jlo && j < jhi) score_or_store(dst, (long long)step * j, wbuf[(j / T) * (T + 1) + j % T]);
+        for (int it = 0; it < T; ++it) {
+          const int j = lane + 32 * it;
+          score_or_store(dst, (long long)step * j, wbuf[(j / T) * (T + 1) + j % T]);
+        }
+      } else {
+#pragma unroll
+        for (int it = 0; it < T; ++it) {
+          const int j = lane + 32 * it;
+          if (j >= jlo && j < jhi) score_or_store(dst, (long long)step * j, wbuf[(j / T) * (T + 1) + j % T]);
+        }
       }
       __syncwarp();
     };
@@ -1064,10 +1149,18 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
         jlo = max(jlo, 0LL);
         jhi = min(jhi, (long long)((min(pgn, 16 * h + 16) - 16 * h) * V2));   // the part's groups only
         double* dst = rsig + gbase + k0;
+        if (jlo <= 0 && jhi >= 32 * T) {
 #pragma unroll
-        for (int it = 0; it < T; ++it) {
-          const int j = lane + 32 * it;
-          if (j >= jlo && j < jhi) score_or_store(dst, j, wbuf[(j / V2) * (V2 + 1) + j % V2]);
+          for (int it = 0; it < T; ++it) {
+            const int j = lane + 32 * it;
+            score_or_store(dst, j, wbuf[(j / V2) * (V2 + 1) + j % V2]);
+          }
+        } else {
+#pragma unroll
+          for (int it = 0; it < T; ++it) {
+            const int j = lane + 32 * it;
+            if (j >= jlo && j < jhi) score_or_store(dst, j, wbuf[(j / V2) * (V2 + 1) + j % V2]);
+          }
         }
         __syncwarp();
       }
