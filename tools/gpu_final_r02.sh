@@ -1,0 +1,15 @@
+# Round-2 end-of-round GPU pass: every GPU test, smoke, the driver's bench command, every workload's
+# bench line, the torchrun launch path (1 rank) and the reference arm.
+mkdir -p gpurun_out/r02f
+P=gpurun_out/r02f
+python -c "import __graft_entry__ as g; g.build()" > $P/build.log 2>&1
+timeout 900 python -m pytest tests -m gpu -q > $P/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $P/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $P/smoke.log 2>&1; echo "smoke rc=$?" >> $P/smoke.log
+timeout 600 python bench.py --gpus 1 --steps 20 --warmup 5 > $P/bench_default.json 2> $P/bench_default.err
+for w in cfg1 cfg3 cfg5; do
+  timeout 600 python bench.py --workload $w --steps 20 --warmup 5 --no-cpu-baseline > $P/bench_$w.json 2> $P/bench_$w.err
+done
+timeout 900 python bench.py --workload cfg4 --steps 5 --warmup 3 > $P/bench_cfg4.json 2> $P/bench_cfg4.err
+timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29517 bench.py --gpus 1 --steps 10 --warmup 3 --no-cpu-baseline --no-sub > $P/bench_torchrun.json 2> $P/bench_torchrun.err
+timeout 300 python bench.py --impl reference --steps 2 --warmup 3 > $P/bench_reference.json 2> $P/bench_reference.err
+echo done
