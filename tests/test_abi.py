@@ -146,3 +146,29 @@ def test_library_has_sm100a_code_and_tma(lib):
                                        text=True).stdout
     assert "DFMA" in sass
     assert "UBLKCP" in sass           # cp.async.bulk (TMA bulk copy) staging of blocks/taps
+
+
+def _build_c_example(lib, out):
+    src = os.path.join(ROOT, "examples", "conv_example.c")
+    libdir = os.path.dirname(lib._name)
+    subprocess.check_call(["gcc", "-O2", "-I", os.path.join(ROOT, "include"), src, "-o", out,
+                           "-L", "/usr/local/cuda/lib64", "-lcudart", "-L", libdir, "-lpackedconv",
+                           f"-Wl,-rpath,{libdir}", "-Wl,-rpath,/usr/local/cuda/lib64", "-lm"])
+
+
+def test_c_example_builds_against_the_abi(lib):
+    """A plain C program (examples/conv_example.c) compiles and links against include/packedconv.h
+    and the library alone -- the boundary needs no Python."""
+    with tempfile.TemporaryDirectory() as d:
+        _build_c_example(lib, os.path.join(d, "conv_example"))
+
+
+@pytest.mark.gpu
+def test_c_example_runs(lib):
+    """The C example runs the packed path end to end through host buffers and meets 40 dB."""
+    with tempfile.TemporaryDirectory() as d:
+        exe = os.path.join(d, "conv_example")
+        _build_c_example(lib, exe)
+        out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+        assert out.returncode == 0, out.stdout + out.stderr
+        assert "SNR vs full precision" in out.stdout
