@@ -1368,8 +1368,9 @@ int conv_adapt_blocks(conv_plan* p, const double* s, int64_t s_offset, int64_t B
                       double calib_offset_db, conv_block_decision* out, void* stream) {
   if (!p || !s) return PC_E_CONFIG;
   if (p->packing != PC_PACK_ADAPTIVE) return PC_E_CONFIG;
-  if (B0 < 0 || B1 > p->P || B0 >= B1) return PC_E_CONFIG;
+  if (B0 < 0 || B1 > p->P || B0 > B1) return PC_E_CONFIG;
   if (!p->kernel_set) return PC_E_STATE;
+  if (B0 == B1) return PC_OK;                          // an empty shard (more ranks than blocks)
   if (cudaSetDevice(p->device) != cudaSuccess) return PC_E_CUDA;
   cudaStream_t st = (cudaStream_t)stream;
   const long long P = p->P, nb = B1 - B0;
