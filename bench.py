@@ -369,7 +369,7 @@ def measure_split(name, sel, head, args, D, dev, L_global, clocks=False, N_overr
             sampler_summary = sampler.summary()
         kern_ms = ms / args.steps
         if adaptive:                                   # the blocks each packing ran on this shard
-            dec = plan.adapt_blocks(S[(args.steps - 1) % n_buf], i0, b0, b1, Q, calib, want=True)
+            dec = plan.adapt_blocks(S[(args.steps - 1) % n_buf], i0, b0, b1, Q, calib, want=True) or []
             fma = sum(core_fma_blocks(info, pk, 0, 0, [b0 + w for w, d in enumerate(dec) if d[0] == pk])
                       for pk in (FULL, SYM, ASYM2))
             counts = D.sum(*[sum(1 for d in dec if d[0] == pk) for pk in (FULL, SYM, ASYM2)])
