@@ -1093,3 +1093,65 @@ def test_best_match_kernel():
     cand = np.array([[1.0, 5, 9], [2.0, 6, 4], [2.0, 7, 3], [-1.0, 8, 0]])
     pcb.best_match(best, 4, cand_dev=dev(cand.reshape(-1)))
     assert best.cpu().tolist() == [2.0, 7.0, 3.0]
+
+
+# --------------------------------------------------------------------- randomized geometry sweep
+def _random_case(rng):
+    """A random valid geometry and operating point: N in [1, 700] (odd and even), W_block from
+    the smallest valid (W = 2N') to 8x that, L from one sample to ~30 blocks, every packing, the
+    largest Q its bound allows (or a smaller random one), both companding-range rules and both
+    modes; signals of several distributions (Laplace, uniform, sparse, constant runs)."""
+    N = int(rng.integers(1, 700))
+    Np = N | 1
+    W = 2 * Np + 2 * int(rng.integers(0, 4 * Np))
+    W_block = W + Np + 1
+    L = int(rng.integers(1, 30 * W))
+    mode = int(rng.integers(0, 2))
+    if mode == O.XCORR and L < N:
+        L = N + int(rng.integers(0, W))
+    packing = [O.SYM, O.ASYM2, O.ASYM3][int(rng.integers(0, 3))]
+    rmax = [O.RMAX_PAPER, O.RMAX_L1][int(rng.integers(0, 2))]
+    kind = int(rng.integers(0, 4))
+    if kind == 0:
+        s = np.clip(rng.laplace(0, 0.3, L), -1, 1)
+    elif kind == 1:
+        s = rng.uniform(-1, 1, L)
+    elif kind == 2:
+        s = rng.normal(0, 1, L) * (rng.random(L) < 0.05)
+    else:
+        s = np.repeat(rng.uniform(-1, 1, L // 64 + 1), 64)[:L]
+    k = rng.normal(0, 1, N) if rng.random() < 0.5 else rng.uniform(-1, 1, N)
+    kp = np.zeros(Np)
+    kp[:N] = k[::-1] if mode == O.XCORR else k
+    qmax = O.max_q_under_bound(kp, Np, packing, O.EPS_POW2, rmax, q_cap=4096)
+    Q = qmax if rng.random() < 0.6 else max(1, int(rng.integers(1, qmax + 1)))
+    return s, k, W_block, packing, Q, rmax, mode
+
+
+@pytest.mark.parametrize("seed", range(96))
+def test_randomized_geometries_bit_exact(seed):
+    """96 random (L, N, W_block, packing, Q, range rule, mode, signal) cases through the
+    production path (auto core and execution form) and, for every third case, the forced FMA
+    core / per-block kernel: the dequantized outputs equal the oracle's bit for bit, and the
+    integers are exact (the oracle's own self-check)."""
+    rng = np.random.default_rng(1000 + seed)
+    s, k, W_block, packing, Q, rmax, mode = _random_case(rng)
+    if Q < 1:
+        pytest.skip("no Q meets the bound")
+    ref = O.conv_pipeline(s, k, W_block, packing, Q, mode=mode, rmax_rule=rmax)
+    assert ref.mismatches == 0
+    variants = [dict()]
+    if seed % 3 == 0:
+        variants += [dict(core_variant=pcb.CORE_FMA, exec=pcb.EXEC_TILED), dict(exec=pcb.EXEC_PERBLOCK)]
+    for v in variants:
+        opts = pcb.opts_default(rmax_rule=rmax, **v)
+        try:
+            with pcb.Plan(len(s), len(k), W_block, mode, PK[packing], Q, opts=opts) as p:
+                p.set_kernel(dev(k))
+                r = torch.full((p.info()["L_out"],), float("nan"), dtype=torch.float64, device=DEV)
+                p.execute(dev(s), r)
+                torch.cuda.synchronize()
+        except pcb.PcError as ex:                      # a forced form may not fit (shared memory)
+            assert ex.code == pcb.PC_E_CONFIG and v, ex
+            continue
+        assert np.array_equal(r.cpu().numpy(), ref.out), (seed, v, len(s), len(k), W_block, packing, Q, rmax, mode)

@@ -1,5 +1,2 @@
 mkdir -p gpurun_out/r02
-for v in s3 q4; do
-PC_LIB_PATH=tools/variants/$v.so timeout 300 python bench.py --no-sub --no-cpu-baseline --steps 20 --warmup 5 --points asym2_10b,asym3_8b,full > gpurun_out/r02/bench_v_$v.json 2>&1
-done
-timeout 300 python bench.py --no-sub --no-cpu-baseline --steps 20 --warmup 5 --points asym2_10b,asym3_8b,full > gpurun_out/r02/bench_v_base.json 2>&1
+timeout 900 python -m pytest tests -m gpu -q -k "randomized or c_example" > gpurun_out/r02/pytest_rand.log 2>&1; echo "rc=$?" >> gpurun_out/r02/pytest_rand.log
