@@ -291,8 +291,11 @@ bool tiled_shape(const conv_plan* p, int packing, TShape* sh, bool taps_per_sign
   sh->tiles1 = (g1 + sh->G - 1) / sh->G;
   const int PT = sh->mma ? T + 4 : T + 1, TH = sh->mma ? 16 : 0;   // as pc_tiled_kernel
   const size_t stage = (size_t)((PT * sh->rows_s + 1) & ~1) * 8 + (sh->taps_resident ? 0 : (size_t)(sh->KC + 2 * TH) * 8);
+  // per-warp output staging rows: the FMA core and symmetric packing only (the DMMA core's
+  // asymmetric / full epilogue decodes from its fragments, so those rows become ring stages)
+  const bool staging = !sh->mma || packing == PC_PACK_SYM;
   const size_t fixed = pc::kTiledHeader + (sh->taps_resident ? (size_t)(sh->K_pad + 2 * TH) * 8 : 0) +
-                       (size_t)pc::tiled_cons_warps(sh->mma) * 32 * (T + 1) * 8;
+                       (staging ? (size_t)pc::tiled_cons_warps(sh->mma) * 32 * (T + 1) * 8 : 0);
   if (fixed + 2 * stage > kMaxSmem) return false;
   sh->nstages = (int)((kMaxSmem - fixed) / stage);
   if (sh->nstages > pc::kTiledMaxStages) sh->nstages = pc::kTiledMaxStages;

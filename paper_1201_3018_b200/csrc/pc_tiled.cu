@@ -620,6 +620,7 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
   const int front = (PACK == PACK_SYM) ? 1 : 0;   // one row before the tile: the extra word
   const int rows_s = e.rows_s;
   constexpr int PT = MMA ? T + 4 : T + 1;           // stage window pitch (conflict-free for the core)
+  constexpr bool FRAG_EPI = MMA && PACK != PACK_SYM;  // epilogue from the DMMA fragments (no staging rows)
   constexpr int TH = MMA ? 16 : 0;                  // DMMA core: zero / neighbour taps on both sides
   const int stage_x = (PT * rows_s + 1) & ~1;       // doubles of a stage's word window (16B-aligned end)
   const int stage_words = stage_x + (e.taps_resident ? 0 : KC + 2 * TH);
@@ -1023,7 +1024,10 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
       __syncwarp();
       if (lane == 0) mbar_arrive(&ps->empty[st]);
     }
-    if (MMA) {                                               // fragments -> group-major rows -> acc[T]
+    if (MMA && FRAG_EPI) {
+      __syncwarp();
+      if (lane == 0) atomicAdd(&ps->core_serve[smsp], 1);   // hand the DMMA pipe to the next claim
+    } else if (MMA) {                                        // fragments -> group-major rows -> acc[T]
       __syncwarp();
       if (lane == 0) atomicAdd(&ps->core_serve[smsp], 1);   // hand the DMMA pipe to the next claim
       const int r = lane >> 2, k2 = 2 * (lane & 3);
@@ -1163,6 +1167,41 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
           }
         }
         __syncwarp();
+      }
+    } else if (FRAG_EPI) {
+      // DMMA core, asymmetric / full: every digit is an elementwise function of its packed output
+      // (balanced digits, C9), so decode straight from the accumulator fragments -- lane (g, t)
+      // holds outputs (8 mt + g) T + 8 nt + 2 t + h of the warp's run -- and store them from there
+      // (no shared-memory transpose or staging: the kernel's stages take that space)
+      constexpr int M = (PACK == PACK_ASYM2) ? 2 : (PACK == PACK_ASYM3 ? 3 : 1);
+      const int seg = (PACK == PACK_FULL) ? b.n_out : b.S;   // outputs per digit segment
+      const int gq = lane >> 2, tq = lane & 3;
+#pragma unroll
+      for (int q = 0; q < M; ++q) {
+        const long long k0 = (long long)q * seg + mw;          // output k = k0 + j
+        long long jhi = min((long long)seg - mw, (long long)b.n_out - k0);
+        jhi = min(jhi, g_hi - gbase - k0);
+        jhi = min(jhi, (long long)(pgn * T));
+        const long long jlo = max(0LL, g_lo - gbase - k0);
+        double* dst = rsig + gbase + k0;
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+          for (int nt2 = 0; nt2 < 2; ++nt2)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int j = (8 * mt + gq) * T + 8 * nt2 + 2 * tq + h;
+              const double v = fr[mt][nt2][h];
+              double o;
+              if (PACK == PACK_FULL) {
+                o = v;
+              } else {
+                const double t = rint_fast(v);
+                o = __dmul_rn(t, inv);
+                if (q < M - 1) fr[mt][nt2][h] = __dmul_rn(__dsub_rn(v, t), mp.eps_inv);
+              }
+              if (j >= jlo && j < jhi) score_or_store(dst, j, o);
+            }
       }
     } else {
       constexpr int M = (PACK == PACK_ASYM2) ? 2 : (PACK == PACK_ASYM3 ? 3 : 1);
