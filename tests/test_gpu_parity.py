@@ -577,6 +577,42 @@ def test_fft_multi_part_blocks_and_xcorr(packing):
             assert rc == pcb.PC_OK and np.array_equal(got, ref.out)
 
 
+@pytest.mark.parametrize("packing,Q", [(O.ASYM2, 63), (O.SYM, 3)])
+def test_fft_batch_and_block_ranges(packing, Q):
+    """FFT core with block peaks computed ahead (pc_block_peak): a 3-signal batch with padded
+    strides (the peak buffer grows past the plan's one-signal size) and block ranges starting
+    past block 0 (peaks indexed by absolute block), bit-exact against the oracle."""
+    rng = np.random.default_rng(11)
+    L, N, W_block = 70000, 700, 16384
+    k = rng.uniform(-1, 1, N)
+    S = rng.laplace(0, 0.3, (3, L))
+    refs = [O.conv_pipeline(S[i], k, W_block, packing, Q, rmax_rule=O.RMAX_L1).out for i in range(3)]
+    opts = pcb.opts_default(core=pcb.CORE_FFT, rmax_rule=O.RMAX_L1, bound_policy=pcb.BOUND_WARN)
+    with pcb.Plan(L, N, W_block, pcb.MODE_CONV, PK[packing], Q, opts=opts) as p:
+        p.set_kernel(dev(k))
+        info = p.info()
+        Lo = info["L_out"]
+        Sd = torch.zeros((3, L + 5), dtype=torch.float64, device=DEV)
+        Sd[:, :L] = dev(S)
+        R = torch.full((3, Lo + 7), float("nan"), dtype=torch.float64, device=DEV)
+        p.execute_batch(Sd, 3, L + 5, R, Lo + 7)
+        torch.cuda.synchronize()
+        for i in range(3):
+            assert np.array_equal(R[i, :Lo].cpu().numpy(), refs[i]), i
+        P = info["P"]
+        out = np.full(Lo, np.nan)
+        s_d = dev(S[1])
+        for b0, b1 in [(0, 1), (1, P // 2), (P // 2, P)]:
+            r = torch.full((Lo,), float("nan"), dtype=torch.float64, device=DEV)
+            p.execute_blocks(s_d, 0, r, 0, b0, b1)
+            torch.cuda.synchronize()
+            got = r.cpu().numpy()
+            sel = ~np.isnan(got)
+            assert sel.any()
+            out[sel] = got[sel]
+        assert np.array_equal(out, refs[1])
+
+
 def test_fft_residual_monitor_flags_overflowing_precision():
     """Fault injection: symmetric packing past its FFT precision (WARN policy) -> the monitor
     reports a residual above 0.25 LSB (PC_W_UNPACK_MARGIN) instead of silently passing."""
