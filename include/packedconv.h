@@ -81,7 +81,8 @@ typedef struct conv_opts {
   int32_t exec;             /* PC_EXEC_*                                                    */
   int32_t K_q;              /* kernel companding range; 0 means K_q = S_q = Q       */
   int32_t device;           /* CUDA device ordinal, -1 = current device                    */
-  int32_t raw_staging;      /* per-block kernel: raw block TMA-staged 0 auto / 1 on / 2 off */
+  int32_t raw_staging;      /* raw block TMA-staged in shared memory (per-block kernel; the
+                               persistent kernel's producers): 0 auto / 1 on / 2 off         */
   int32_t core_tile;        /* persistent direct core: outputs per thread, 0 auto / 12/14/16 */
   int32_t core_variant;     /* PC_CORE_AUTO / PC_CORE_FMA / PC_CORE_DMMA                    */
   int32_t parts_per_job;    /* persistent direct core: consumer warps per job, 0 auto / 1,2,4 */

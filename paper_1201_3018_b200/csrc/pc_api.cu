@@ -229,6 +229,7 @@ bool launch_shape(const conv_plan* p, const int* packs, int npacks, Shape* sh) {
 // stage-ring slots as shared memory holds (2..8) after the per-warp output staging rows.
 struct TShape {
   int T, mma, threads, G, KC, nchunks, taps_resident, rows_s, K_pad, nstages;
+  int raw_slots, raw_stride;   // raw-staged producers: raw block slots in smem (0: global loads)
   long long tiles0, tiles1;
   size_t smem;
 };
@@ -294,9 +295,36 @@ bool tiled_shape(const conv_plan* p, int packing, TShape* sh, bool taps_per_sign
   // per-warp output staging rows: the FMA core and symmetric packing only (the DMMA core's
   // asymmetric / full epilogue decodes from its fragments, so those rows become ring stages)
   const bool staging = !sh->mma || packing == PC_PACK_SYM;
-  const size_t fixed = pc::kTiledHeader + (sh->taps_resident ? (size_t)(sh->K_pad + 2 * TH) * 8 : 0) +
-                       (staging ? (size_t)pc::tiled_cons_warps(sh->mma) * 32 * (T + 1) * 8 : 0);
+  size_t fixed = pc::kTiledHeader + (sh->taps_resident ? (size_t)(sh->K_pad + 2 * TH) * 8 : 0) +
+                 (staging ? (size_t)pc::tiled_cons_warps(sh->mma) * 32 * (T + 1) * 8 : 0);
   if (fixed + 2 * stage > kMaxSmem) return false;
+  // Raw-staged producers (single-chunk plans; opts.raw_staging 0 auto / 1 on / 2 off): the job's
+  // raw block (W_block samples) arrives by one TMA bulk copy into a shared-memory slot, two slots
+  // (the next job's copy in flight) when the ring keeps >= PC_RAW_MIN_STAGES stages, else one.
+#ifndef PC_RAW_PROD
+#define PC_RAW_PROD 1
+#endif
+#ifndef PC_RAW_MIN_STAGES
+#define PC_RAW_MIN_STAGES 5
+#endif
+  sh->raw_slots = 0;
+  sh->raw_stride = 0;
+  // (auto: asymmetric M = 2 and symmetric packing; measured at cfg2: asym2 93.2 -> 88.5 us, sym 73.8
+  // -> 72.7, while asym3 80.0 vs 78.5 and full precision -- no peak, plain copies -- 158 vs 144 lose)
+  if (PC_RAW_PROD && sh->nchunks == 1 && p->opts.raw_staging != 2 &&
+      (packing == PC_PACK_ASYM2 || packing == PC_PACK_SYM || p->opts.raw_staging == 1)) {
+    const size_t rs = (size_t)((p->W_block + 3) & ~1);   // doubles per slot (head offset, even)
+    for (int k = 2; k >= 1; --k) {
+      const size_t f2 = fixed + (size_t)k * rs * 8;
+      const int nst = f2 + 2 * stage <= kMaxSmem ? (int)((kMaxSmem - f2) / stage) : 0;
+      if (nst >= (p->opts.raw_staging == 1 ? 2 : PC_RAW_MIN_STAGES - (2 - k))) {
+        sh->raw_slots = k;
+        sh->raw_stride = (int)rs;
+        fixed = f2;
+        break;
+      }
+    }
+  }
   sh->nstages = (int)((kMaxSmem - fixed) / stage);
   if (sh->nstages > pc::kTiledMaxStages) sh->nstages = pc::kTiledMaxStages;
   if (p->opts.stage_cap >= 2 && sh->nstages > p->opts.stage_cap) sh->nstages = p->opts.stage_cap;   // diagnostics
@@ -535,6 +563,8 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
         el.KC = t.KC;
         el.nchunks = t.nchunks;
         el.taps_resident = t.taps_resident;
+        el.raw_slots = t.raw_slots;
+        el.raw_stride = t.raw_stride;
         el.rows_s = t.rows_s;
         el.tiles0 = t.tiles0;
         el.tiles1 = t.tiles1;
@@ -566,6 +596,8 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
     e.KC = ts.KC;
     e.nchunks = ts.nchunks;
     e.taps_resident = ts.taps_resident;
+    e.raw_slots = e.lookahead > 0 ? 0 : ts.raw_slots;   // (the claim-ahead diagnostics use the warp producers)
+    e.raw_stride = ts.raw_stride;
     e.rows_s = ts.rows_s;
     e.tiles0 = ts.tiles0;
     e.tiles1 = ts.tiles1;
@@ -590,6 +622,7 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
       e.pre_stride = stride;
       e.pre_inv = p->d_pre + njobs * stride;
       if (pc::launch_prepack(p->packing, ts.T, ts.mma, make_geo(p), e, njobs, st) != cudaSuccess) return PC_E_CUDA;
+      e.raw_slots = 0;                                 // the producers only move prepacked windows
     }
     // a2 ahead (PC_PEAK_AHEAD builds): the block peaks of this launch's blocks in one bandwidth-bound
     // pass, so the producers only compand and pack (their peak pass runs 3-6x slower next to the

@@ -116,6 +116,7 @@ struct Exec {
   int G;                        // consumer threads = groups per tile
   int KC, nchunks;              // taps per chunk (multiple of T), chunks per job
   int nstages;                  // stage ring slots (2 .. kTiledMaxStages)
+  int raw_slots, raw_stride;    // raw-staged producers: raw block slots after the staging rows (0: global loads), doubles each
   int lookahead;                // > 0: claim job sequence m only once consumers have claimed parts of m - lookahead
   int early_fill;               // 1: the pipeline fill runs before griddepcontrol.wait (see pc_tiled_kernel)
   int early_claim;              // 1: the fill's job claims run before griddepcontrol.wait (alternating queue arrays)

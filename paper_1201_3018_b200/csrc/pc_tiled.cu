@@ -64,6 +64,8 @@ struct TSmem {
   long long fjob[16];               // pipeline fill: jobs of sequences 0 .. nf-1
   double fcs[16], finv[16];         // their c_s and (c_s c_k)^-1
   long long m_end;                  // first job sequence whose claim failed (-1: not yet)
+  uint64_t rawbar[2];               // raw-staged producers: TMA arrival of raw slot k
+  long long pjob[2];                // raw-staged producers: claimed job of sequence m (slot m & 1)
   double red[32];
   long long cyc[4];   // diagnostics (consumer thread 0): wait, core, unpack/store cycles; clock mark
 };
@@ -84,6 +86,15 @@ __device__ __forceinline__ JobPos unpack_pos(unsigned long long v) {
   p.t = (int)(v & 0xffull);
   return p;
 }
+// 64-bit quotient / remainder through the 32-bit divide when both operands fit (the usual
+// case; a 64-bit division is a ~70-instruction subroutine, expensive for warps that share their
+// sub-partition with DMMA-issuing warps)
+__device__ __forceinline__ long long qdiv(long long a, long long b) {
+  return (((unsigned long long)a | (unsigned long long)b) >> 31) == 0 ? (long long)((unsigned)a / (unsigned)b) : a / b;
+}
+__device__ __forceinline__ long long qmod(long long a, long long b) {
+  return (((unsigned long long)a | (unsigned long long)b) >> 31) == 0 ? (long long)((unsigned)a % (unsigned)b) : a % b;
+}
 __device__ __forceinline__ JobPos job_pos(const Exec& e, long long job) {
   JobPos p;
   if (e.blk_list) {                                  // adaptive: this launch's blocks, ascending
@@ -95,12 +106,12 @@ __device__ __forceinline__ JobPos job_pos(const Exec& e, long long job) {
       return p;
     }
     const long long r = first0 ? job - e.tiles0 : job;
-    p.w = e.blk_list[(first0 ? 1 : 0) + r / e.tiles1];
-    p.t = (int)(r % e.tiles1);
+    p.w = e.blk_list[(first0 ? 1 : 0) + qdiv(r, e.tiles1)];
+    p.t = (int)qmod(r, e.tiles1);
     return p;
   }
-  p.sig = job / e.jobs_per_sig;
-  long long r = job % e.jobs_per_sig;
+  p.sig = qdiv(job, e.jobs_per_sig);
+  long long r = job - p.sig * e.jobs_per_sig;
   if (e.b0 == 0) {                                   // block 0 (if in range) has tiles0 tiles
     if (r < e.tiles0) {
       p.w = 0;
@@ -108,11 +119,12 @@ __device__ __forceinline__ JobPos job_pos(const Exec& e, long long job) {
       return p;
     }
     r -= e.tiles0;
-    p.w = 1 + r / e.tiles1;
-    p.t = (int)(r % e.tiles1);
+    p.w = 1 + qdiv(r, e.tiles1);
+    p.t = (int)(r - (p.w - 1) * e.tiles1);
   } else {
-    p.w = e.b0 + r / e.tiles1;
-    p.t = (int)(r % e.tiles1);
+    const long long q = qdiv(r, e.tiles1);
+    p.w = e.b0 + q;
+    p.t = (int)(r - q * e.tiles1);
   }
   return p;
 }
@@ -175,7 +187,7 @@ __device__ __forceinline__ void pack_window(const Geo& g, const Blk& b, const Mo
   }
   for (int i0 = ptid; i0 < words; i0 += UW * nprod) {
     double v[UW];
-    if (!alu && i0 >= ilo && i0 + (UW - 1) * nprod < ihi) {   // interior: unchecked
+    if (i0 >= ilo && i0 + (UW - 1) * nprod < ihi) {   // interior: unchecked
       if (PACK == PACK_SYM) {
         double x0[UW], x1[UW];
 #pragma unroll
@@ -184,8 +196,16 @@ __device__ __forceinline__ void pack_window(const Geo& g, const Blk& b, const Mo
           x0[u] = SRC_SMEM ? gsrc[2 * j] : __ldg(gsrc + 2 * j);
           x1[u] = SRC_SMEM ? gsrc[2 * j + 1] : __ldg(gsrc + 2 * j + 1);
         }
+        if (alu) {
 #pragma unroll
-        for (int u = 0; u < UW; ++u) v[u] = pack_sym(compand1(c_s, x0[u]), compand1(c_s, x1[u]), mp.eps);
+          for (int u = 0; u < UW; ++u) {
+            const long long n = round_away_alu(__dmul_rn(c_s, x0[u])) * (1LL << mp.b) + round_away_alu(__dmul_rn(c_s, x1[u]));
+            v[u] = i2d_scaled_alu(n, mp.b);
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < UW; ++u) v[u] = pack_sym(compand1(c_s, x0[u]), compand1(c_s, x1[u]), mp.eps);
+        }
       } else if (PACK == PACK_ASYM2 || PACK == PACK_ASYM3) {
         constexpr int M = (PACK == PACK_ASYM2) ? 2 : 3;
         double x[M][UW];
@@ -194,12 +214,22 @@ __device__ __forceinline__ void pack_window(const Geo& g, const Blk& b, const Mo
         for (int u = 0; u < UW; ++u)
 #pragma unroll
           for (int q = 0; q < M; ++q) x[q][u] = SRC_SMEM ? src[q * b.S + u * nprod] : __ldg(src + q * b.S + u * nprod);
+        if (alu) {                                           // integer Horner (dyadic eps), same bits
 #pragma unroll
-        for (int u = 0; u < UW; ++u) {
-          double a = compand1(c_s, x[M - 1][u]);         // Horner, oracle order
+          for (int u = 0; u < UW; ++u) {
+            long long n = round_away_alu(__dmul_rn(c_s, x[0][u]));
 #pragma unroll
-          for (int q = M - 2; q >= 0; --q) a = __dadd_rn(compand1(c_s, x[q][u]), __dmul_rn(mp.eps, a));
-          v[u] = a;
+            for (int q = 1; q < M; ++q) n = n * (1LL << mp.b) + round_away_alu(__dmul_rn(c_s, x[q][u]));
+            v[u] = i2d_scaled_alu(n, (M - 1) * mp.b);
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < UW; ++u) {
+            double a = compand1(c_s, x[M - 1][u]);         // Horner, oracle order
+#pragma unroll
+            for (int q = M - 2; q >= 0; --q) a = __dadd_rn(compand1(c_s, x[q][u]), __dmul_rn(mp.eps, a));
+            v[u] = a;
+          }
         }
       } else {
         const double* src = gsrc + (b.o0 - (g.Np - 1) + cw0 + i0);
@@ -313,6 +343,33 @@ __device__ __forceinline__ double block_cs(const ModeP& mp, const double* gsrc, 
   double peak = 0.0;
   for (int wi = 0; wi < nprod / 32; ++wi) peak = fmax(peak, red[wi]);
   named_bar(bar_id, nprod);
+  return (peak == 0.0) ? 1.0 : mp.Q / peak;
+}
+
+// a2/a3 from the raw block in shared memory (raw-staged producers): the same max |x| (integer
+// order of the absolute-value bits) and the same IEEE division as block_cs.
+template <int PACK>
+__device__ __forceinline__ double smem_cs(const ModeP& mp, const double* raw, int n_valid, double* red, int ptid,
+                                          int nprod, int bar_id) {
+  if (PACK == PACK_FULL) return 1.0;
+  constexpr int U = 4;
+  unsigned long long m[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) m[u] = 0ull;
+  for (int i0 = ptid; i0 < n_valid; i0 += U * nprod) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * nprod;
+      if (i < n_valid) m[u] = umax64(m[u], abs_bits(raw[i]));
+    }
+  }
+#pragma unroll
+  for (int u = 1; u < U; ++u) m[0] = umax64(m[0], m[u]);
+  for (int o = 16; o > 0; o >>= 1) m[0] = umax64(m[0], __shfl_xor_sync(0xffffffffu, m[0], o));
+  if ((ptid & 31) == 0) red[ptid >> 5] = __longlong_as_double((long long)m[0]);
+  named_bar(bar_id, nprod);
+  double peak = 0.0;
+  for (int wi = 0; wi < nprod / 32; ++wi) peak = fmax(peak, red[wi]);
   return (peak == 0.0) ? 1.0 : mp.Q / peak;
 }
 
@@ -454,7 +511,7 @@ __device__ __forceinline__ long long claim_job(const Exec& e, long long njobs, i
   const int s = (int)(blockIdx.x % (unsigned)nq);
   long long job = -1;
   if (lane == 0) {
-    const long long lo = njobs * s / nq, hi = njobs * (s + 1) / nq;
+    const long long lo = qdiv(njobs * s, nq), hi = qdiv(njobs * (s + 1), nq);
     if (lo < hi) {
       const unsigned n = atomicAdd(ctr + s, 1u);
       if (lo + n < hi) job = lo + n;
@@ -464,7 +521,7 @@ __device__ __forceinline__ long long claim_job(const Exec& e, long long njobs, i
   if (job >= 0 || PC_NO_STEAL) return job;
   for (int base = 1; base < nq; base += 32) {
     const int t = (s + base + lane) % nq;
-    const long long lo = njobs * t / nq, hi = njobs * (t + 1) / nq;
+    const long long lo = qdiv(njobs * t, nq), hi = qdiv(njobs * (t + 1), nq);
     const bool has = (base + lane < nq) && lo + (long long)*(volatile unsigned*)(ctr + t) < hi;
     unsigned mask = __ballot_sync(0xffffffffu, has);
     while (mask) {
@@ -627,11 +684,14 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
   double* kr_res = reinterpret_cast<double*>(smem + kTiledHeader) + TH;     // resident taps
   double* stg = kr_res + (e.taps_resident ? mp.K_pad + TH : -TH);           // NS stages
   double* wout = stg + (size_t)NS * stage_words;                            // per consumer warp: 32 (T+1)
+  double* raw_base = wout + (FRAG_EPI ? (size_t)0 : (size_t)NCW * 32 * (T + 1));   // raw slots (e.raw_slots)
   const int tid = threadIdx.x;
   const int nprod = kTiledProdWarps * 32;
 
   if (tid == 0) {
     mbar_init(&ps->bar_taps, 1);
+    mbar_init(&ps->rawbar[0], 1);
+    mbar_init(&ps->rawbar[1], 1);
     for (int i = 0; i < NS; ++i) {
       mbar_init(&ps->full[i], 32);
       mbar_init(&ps->empty[i], npart);
@@ -774,6 +834,135 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
   if (e.dbg_timing && tid == 0)
     e.dbg_timing[kTimCyc + 4 * blockIdx.x + 3] = gtimer() - e.dbg_timing[kTimCyc + 4 * blockIdx.x + 2];
 
+  if (tid < nprod && e.raw_slots > 0) {
+    // ====================== raw-staged producer warps ======================
+    // The four producer warps work on one job at a time.  Its raw block arrives in shared
+    // memory by one TMA bulk copy (issued a job ahead when two raw slots fit), so the peak,
+    // companding and packing read shared memory: no per-lane global loads and their latency
+    // next to the DMMA warps.  Single-chunk plans (nch == 1) without prepacked windows.
+    // Same claims (sequence order, one warp), stages, sentinels and publish as below.
+    const int ptid = tid, lane = tid & 31, pw = tid >> 5;
+    constexpr int PB = 8;                             // named barrier of the producer warps
+    const int RS = e.raw_slots;
+    const int n_sent = NCW / npart;
+    uint32_t rph = 0;                                 // bit k: parity of raw slot k's next wait
+    long long cur_blk_w = -1;
+    double c_s_w = 1.0, inv_w = 0.0;
+    auto claim_seq = [&](long long m) -> long long {  // job of sequence m, -1: none left (M_end)
+      if (pw == 0) {
+        long long j = -1;
+        if (*reinterpret_cast<volatile long long*>(&ps->m_end) < 0) {
+          if (lane == 0 && e.lookahead > 0) {
+            Spin sp;
+            while (m >= (long long)*reinterpret_cast<volatile int*>(&ps->mseq_hi) + max(e.lookahead, RS))
+              spin_wd(e.status, sp, 128, 6, m, 0);
+          }
+          __syncwarp();
+          j = claim_job(e, njobs, lane);
+          if (j < 0 && lane == 0) *reinterpret_cast<volatile long long*>(&ps->m_end) = m;
+        }
+        if (lane == 0) ps->pjob[m & 1] = j;
+      }
+      named_bar(PB, nprod);
+      return *reinterpret_cast<volatile long long*>(&ps->pjob[m & 1]);
+    };
+    // raw slot layout: rp[i] = block sample i; rp[head] is 16-byte aligned (TMA), the head and an
+    // odd tail element are loaded by threads (the copy never reads outside [gsrc, gsrc + n_valid))
+    auto raw_geom = [&](const double* gs, int nv, int slot, int& head, int& mid) -> double* {
+      head = (reinterpret_cast<uintptr_t>(gs) & 15u) ? 1 : 0;
+      mid = max(0, nv - head) & ~1;
+      return raw_base + (size_t)slot * e.raw_stride + head;
+    };
+    auto issue_raw = [&](long long job, int slot) {
+      if (ptid == 0) {
+        JobPos jp;
+        Blk b;
+        const double* gs;
+        int nv, head, mid;
+        job_block(job, jp, b, gs, nv);
+        double* rp = raw_geom(gs, nv, slot, head, mid);
+        mbar_arrive_expect_tx(&ps->rawbar[slot], (uint32_t)mid * 8u);
+        if (mid > 0) bulk_g2s(rp + head, gs + head, (uint32_t)mid * 8u, &ps->rawbar[slot]);
+      }
+    };
+    long long m = 0;
+    for (; m < nf; ++m) {                             // the pipeline fill's jobs: publish
+      const long long job = ps->fjob[m];
+      if (job < 0) break;
+      const JobPos jq = job_pos(e, job);
+      cur_blk_w = jq.sig * g.P + jq.w;
+      c_s_w = ps->fcs[m];
+      inv_w = ps->finv[m];
+      if (pw == 0) publish(m, (int)(m % NS), 0, job, inv_w, lane);
+    }
+    long long job = (m == nf) ? claim_seq(m) : -1;
+    if (job >= 0 && RS == 2) issue_raw(job, (int)(m & 1));
+    int pj = 0;
+    for (;; ++pj) {
+      unsigned long long* prec = (e.dbg_timing && ptid == 0 && pj < 16)
+                                     ? e.dbg_timing + kTimP + (((size_t)blockIdx.x * 4 + 0) * 16 + pj) * 4
+                                     : nullptr;
+      if (prec) {
+        prec[0] = (unsigned long long)m;
+        prec[1] = gtimer();
+      }
+      if (job < 0) {                                  // sentinels: sequences m .. M_end + n_sent - 1
+        const long long me = *reinterpret_cast<volatile long long*>(&ps->m_end);
+        for (; m < me + n_sent; ++m) {
+          const int st = (int)qmod(m, NS);
+          if (m >= NS) mbar_wait_wd(e.status, &ps->empty[st], (uint32_t)((qdiv(m, NS) & 1) ^ 1), 1, m, st);
+          if (pw == 0) publish(m, st, 0, -1, 0.0, lane);
+        }
+        break;
+      }
+      long long nxt = -1;
+      if (RS == 2) {                                  // the next job's raw block in flight during this one
+        nxt = claim_seq(m + 1);
+        if (nxt >= 0) issue_raw(nxt, (int)((m + 1) & 1));
+      } else {
+        issue_raw(job, 0);
+      }
+      if (prec) prec[2] = gtimer();
+      const int slot = (RS == 2) ? (int)(m & 1) : 0;
+      JobPos jp;
+      Blk b;
+      const double* gs;
+      int nv, head, mid;
+      job_block(job, jp, b, gs, nv);
+      double* rp = raw_geom(gs, nv, slot, head, mid);
+      if (ptid == 0 && head && nv > 0) rp[0] = __ldg(gs);
+      if (ptid == 1 && head + mid < nv) rp[nv - 1] = __ldg(gs + nv - 1);
+      mbar_wait_wd(e.status, &ps->rawbar[slot], (rph >> slot) & 1u, 8, m, slot);
+      rph ^= 1u << slot;
+      named_bar(PB, nprod);                           // head / tail elements visible
+      const long long blk_id = jp.sig * g.P + jp.w;
+      if (blk_id != cur_blk_w) {
+        cur_blk_w = blk_id;
+        c_s_w = e.blk_peak ? cs_from_peak<PACK>(mp, e.blk_peak[jp.sig * e.peak_stride + jp.w])
+                           : smem_cs<PACK>(mp, rp, nv, ps->red + 28, ptid, nprod, PB);   // a2/a3
+        inv_w = dequant_scale(c_s_w, e.scal_sig ? e.scal_sig[3 * jp.sig + 1] : mp.c_k);   // Eq. (16)
+      }
+      unsigned long long t_pk = 0, t_sl = 0;
+      if (prec) t_pk = gtimer();
+      const int st = (int)qmod(m, NS);
+      if (m >= NS) mbar_wait_wd(e.status, &ps->empty[st], (uint32_t)((qdiv(m, NS) & 1) ^ 1), 1, m, st);
+      if (prec) t_sl = gtimer();
+      pack_window<PACK, T, 1, PT, true>(g, b, mp, rp, nv, c_s_w, jp.t * G * T - front * T, rows_s,
+                                        stg + (size_t)st * stage_words, ptid, nprod);   // a3/a4
+      named_bar(PB, nprod);
+      if (pw == 0) publish(m, st, 0, job, inv_w, lane);
+      if (prec) {
+        prec[3] = gtimer();
+        const unsigned long long d1 = min((t_pk - prec[2]) >> 4, 0xffffffull), d2 = min((t_sl - t_pk) >> 4, 0xffffffull);
+        prec[0] = (unsigned long long)(m & 0xffff) | (d1 << 16) | (d2 << 40);
+      }
+      ++m;
+      job = (RS == 2) ? nxt : claim_seq(m);
+    }
+    if (tid == 0) retire_cta(e);
+    return;
+  }
+
   if (tid < nprod) {
     // ============================ producer warps ============================
     // Job sequence m (its chunk c is stage sequence n = m * nch + c, slot n % NS) is produced
@@ -858,7 +1047,7 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
       if (prec) t_pk = gtimer();
       for (int c = 0; c < nch; ++c) {
         const long long n = m * nch + c;
-        const int st = (int)(n % NS);
+        const int st = (int)qmod(n, NS);
         if (n >= NS) {
           if (lane == 0)
           {
@@ -866,7 +1055,7 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
             while (*reinterpret_cast<volatile long long*>(&ps->seq[st]) != n - NS) spin_wd(e.status, sp, 256, 7, n, st);
           }
           __syncwarp();
-          mbar_wait_wd(e.status, &ps->empty[st], (uint32_t)(((n / NS) & 1) ^ 1), 1, n, st);
+          mbar_wait_wd(e.status, &ps->empty[st], (uint32_t)((qdiv(n, NS) & 1) ^ 1), 1, n, st);
         }
         if (prec && c == 0) t_sl = gtimer();
         if (job >= 0 && !(prepacked && c == 0) && !e.pre_win)
@@ -904,7 +1093,7 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
   // stamped by the producer tells the two apart.
   auto wait_full = [&](long long n, int st) {
     for (Spin sp;;) {
-      mbar_wait_wd(e.status, &ps->full[st], (uint32_t)((n / NS) & 1), 2, n, st);
+      mbar_wait_wd(e.status, &ps->full[st], (uint32_t)(qdiv(n, NS) & 1), 2, n, st);
       if (*reinterpret_cast<volatile long long*>(&ps->seq[st]) == n) return;
       spin_wd(e.status, sp, 200, 3, n, st);
     }
@@ -917,12 +1106,12 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
     if (lane == 0) cl = atomicAdd(&ps->smsp_ctr[smsp], 1);
     cl = __shfl_sync(0xffffffffu, cl, 0);
     const long long k = 4LL * cl + smsp;
-    const long long mseq = k / npart;
+    const long long mseq = qdiv(k, npart);
     if (lane == 0 && e.lookahead > 0) atomicMax(&ps->mseq_hi, (int)(mseq + 1));
     // parts rotate over the SMSPs from job to job, so ragged last parts do not pile up on one
-    const int part = (int)((k % npart + mseq) % npart);
+    const int part = (int)qmod(k - mseq * npart + mseq, npart);
     long long n = mseq * nch;
-    int st = (int)(n % NS);
+    int st = (int)qmod(n, NS);
     if (PC_REC) ps->cyc[3] = clock64();
     wait_full(n, st);
     const long long job = ps->job[st];
@@ -940,7 +1129,7 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
     }
     if (job < 0) {                                           // sentinel: release its stages, stop
       for (int c = 0; c < nch; ++c, ++n) {
-        st = (int)(n % NS);
+        st = (int)qmod(n, NS);
         if (c > 0) wait_full(n, st);
         __syncwarp();
         if (lane == 0) mbar_arrive(&ps->empty[st]);
@@ -993,7 +1182,7 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
       __syncwarp();
     }
     for (int c = 0; c < nch; ++c, ++n) {
-      st = (int)(n % NS);
+      st = (int)qmod(n, NS);
       if (c > 0) wait_full(n, st);
       const double* xs = stg + (size_t)st * stage_words;
       const double* kc = e.taps_resident ? kr_res + (size_t)c * KC : xs + stage_x + TH;

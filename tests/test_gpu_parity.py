@@ -1191,3 +1191,43 @@ def test_randomized_geometries_bit_exact(seed):
             assert ex.code == pcb.PC_E_CONFIG and v, ex
             continue
         assert np.array_equal(r.cpu().numpy(), ref.out), (seed, v, len(s), len(k), W_block, packing, Q, rmax, mode)
+
+
+@pytest.mark.parametrize("packing,Q", [(O.ASYM2, 511), (O.SYM, 22), (O.ASYM3, 22), (O.FULL, 0)])
+@pytest.mark.parametrize("raw", [0, 1, 2])
+def test_raw_staged_producers_bit_exact(packing, Q, raw):
+    """The persistent kernel's raw-staged producers (opts.raw_staging: 0 auto -- asym2 and sym --,
+    1 forced, 2 off): the block arrives by one TMA bulk copy with the head element (input not
+    16-byte aligned) and an odd tail loaded by threads.  A ragged length, block-range launches
+    (b0 > 0) and a misaligned input pointer, bit-exact against the oracle in every form."""
+    rng = np.random.default_rng(77)
+    L, N, W_block = 61_117, 513, 4096
+    s, k = rng.laplace(0, 0.25, L), rng.uniform(-1, 1, N)
+    ref = O.conv_pipeline(s, k, W_block, packing, Q, rmax_rule=O.RMAX_L1).out
+
+    def same(got):                                    # full precision: FP64 rounding order (C16)
+        if packing == O.FULL:
+            return np.max(np.abs(got - ref)) / np.max(np.abs(ref)) < 1e-12
+        return np.array_equal(got, ref)
+
+    opts = pcb.opts_default(rmax_rule=O.RMAX_L1, raw_staging=raw)
+    with pcb.Plan(L, N, W_block, pcb.MODE_CONV, PK[packing], Q, opts=opts) as p:
+        p.set_kernel(dev(k))
+        info = p.info()
+        buf = torch.zeros(L + 1, dtype=torch.float64, device=DEV)
+        buf[1:] = dev(s)
+        for src in (dev(s), buf[1:]):
+            r = torch.full((info["L_out"],), float("nan"), dtype=torch.float64, device=DEV)
+            p.execute(src, r)
+            torch.cuda.synchronize()
+            assert same(r.cpu().numpy()), (raw, src.data_ptr() % 16)
+        out = np.full(info["L_out"], np.nan)
+        P = info["P"]
+        for b0, b1 in [(0, 3), (3, P // 2), (P // 2, P)]:
+            r = torch.full((info["L_out"],), float("nan"), dtype=torch.float64, device=DEV)
+            p.execute_blocks(buf[1:], 0, r, 0, b0, b1)
+            torch.cuda.synchronize()
+            got = r.cpu().numpy()
+            sel = ~np.isnan(got)
+            out[sel] = got[sel]
+        assert same(out)
