@@ -300,12 +300,13 @@ bool tiled_shape(const conv_plan* p, int packing, TShape* sh, bool taps_per_sign
   if (fixed + 2 * stage > kMaxSmem) return false;
   // Raw-staged producers (single-chunk plans; opts.raw_staging 0 auto / 1 on / 2 off): the job's
   // raw block (W_block samples) arrives by one TMA bulk copy into a shared-memory slot, two slots
-  // (the next job's copy in flight) when the ring keeps >= PC_RAW_MIN_STAGES stages, else one.
+  // (the next job's copy in flight) when the ring keeps >= PC_RAW_MIN_STAGES stages, else one
+  // (cfg2 asym2/sym: one slot and 7 stages measured 0.9-2% faster than two slots and 6).
 #ifndef PC_RAW_PROD
 #define PC_RAW_PROD 1
 #endif
 #ifndef PC_RAW_MIN_STAGES
-#define PC_RAW_MIN_STAGES 5
+#define PC_RAW_MIN_STAGES 7
 #endif
   sh->raw_slots = 0;
   sh->raw_stride = 0;
