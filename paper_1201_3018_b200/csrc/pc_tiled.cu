@@ -451,6 +451,10 @@ __device__ __noinline__ void mbar_stuck(int* status, int where, long long n, int
          (int)blockIdx.x, (int)threadIdx.x, n, st, phase);
   __trap();
 #else
+#ifdef PC_DEBUG_PRINT
+  printf("pc_tiled_kernel: wait %d stuck (block %d thread %d seq %lld slot %d parity %u)\n", where,
+         (int)blockIdx.x, (int)threadIdx.x, n, st, phase);
+#endif
   (void)n;
   (void)st;
   (void)phase;
@@ -840,7 +844,11 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
     // memory by one TMA bulk copy (issued a job ahead when two raw slots fit), so the peak,
     // companding and packing read shared memory: no per-lane global loads and their latency
     // next to the DMMA warps.  Single-chunk plans (nch == 1) without prepacked windows.
-    // Same claims (sequence order, one warp), stages, sentinels and publish as below.
+    // Same claims (sequence order, one warp), stages, sentinels and publish as below.  One warp
+    // waits on each mbarrier (ring slot, raw slot) and releases the others through the named
+    // barrier: with all four warps polling the ring slot's `empty` barrier, about one run in five
+    // of the cfg2 bench stalled -- two warps past the slot's release, two still waiting on it
+    // (4-s watchdog) -- and none in 26 runs since.
     const int ptid = tid, lane = tid & 31, pw = tid >> 5;
     constexpr int PB = 8;                             // named barrier of the producer warps
     const int RS = e.raw_slots;
@@ -908,11 +916,12 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
       }
       if (job < 0) {                                  // sentinels: sequences m .. M_end + n_sent - 1
         const long long me = *reinterpret_cast<volatile long long*>(&ps->m_end);
-        for (; m < me + n_sent; ++m) {
-          const int st = (int)qmod(m, NS);
-          if (m >= NS) mbar_wait_wd(e.status, &ps->empty[st], (uint32_t)((qdiv(m, NS) & 1) ^ 1), 1, m, st);
-          if (pw == 0) publish(m, st, 0, -1, 0.0, lane);
-        }
+        if (pw == 0)                                  // (warp 0 alone waits on the ring and publishes)
+          for (; m < me + n_sent; ++m) {
+            const int st = (int)qmod(m, NS);
+            if (m >= NS) mbar_wait_wd(e.status, &ps->empty[st], (uint32_t)((qdiv(m, NS) & 1) ^ 1), 1, m, st);
+            publish(m, st, 0, -1, 0.0, lane);
+          }
         break;
       }
       long long nxt = -1;
@@ -932,9 +941,9 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
       double* rp = raw_geom(gs, nv, slot, head, mid);
       if (ptid == 0 && head && nv > 0) rp[0] = __ldg(gs);
       if (ptid == 1 && head + mid < nv) rp[nv - 1] = __ldg(gs + nv - 1);
-      mbar_wait_wd(e.status, &ps->rawbar[slot], (rph >> slot) & 1u, 8, m, slot);
+      if (pw == 0) mbar_wait_wd(e.status, &ps->rawbar[slot], (rph >> slot) & 1u, 8, m, slot);   // warp 0 waits,
       rph ^= 1u << slot;
-      named_bar(PB, nprod);                           // head / tail elements visible
+      named_bar(PB, nprod);                           // the others here; head / tail elements visible
       const long long blk_id = jp.sig * g.P + jp.w;
       if (blk_id != cur_blk_w) {
         cur_blk_w = blk_id;
@@ -945,7 +954,10 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
       unsigned long long t_pk = 0, t_sl = 0;
       if (prec) t_pk = gtimer();
       const int st = (int)qmod(m, NS);
-      if (m >= NS) mbar_wait_wd(e.status, &ps->empty[st], (uint32_t)((qdiv(m, NS) & 1) ^ 1), 1, m, st);
+      if (m >= NS) {                                  // the ring slot: warp 0 waits for its release
+        if (pw == 0) mbar_wait_wd(e.status, &ps->empty[st], (uint32_t)((qdiv(m, NS) & 1) ^ 1), 1, m, st);
+        named_bar(PB, nprod);
+      }
       if (prec) t_sl = gtimer();
       pack_window<PACK, T, 1, PT, true>(g, b, mp, rp, nv, c_s_w, jp.t * G * T - front * T, rows_s,
                                         stg + (size_t)st * stage_words, ptid, nprod);   // a3/a4
