@@ -262,6 +262,11 @@ def core_fma_blocks(info, packing, b0, b1, blocks=None):
 def make_opts(pcb, args, rmax, core, extra):
     opts = pcb.opts_default(rmax_rule=rmax, core=core, exec=0 if args.exec == "fused" else 1)
     opts.parts_per_job = args.force_warps
+    # The opt-in launch overlap (a persistent launch's pipeline fill may run during the preceding
+    # launch's tail, host-checked not to read what that launch writes): safe here because this
+    # process's streams carry only this library's launches -- no foreign kernel with its own
+    # programmatic trigger can sit between two of them (include/packedconv.h, early_fill).
+    opts.early_fill = 1
     for f, v in extra.items():
         setattr(opts, f, v)
     for kv in args.opt:
@@ -694,7 +699,7 @@ def run_ours(args, D):
                    "parallelism": (f"{D.ws} rank(s), one signal split by overlap-save block range "
                                    f"(conv_shard_range + conv_execute_blocks, N'+1-sample halo)" if name != "cfg4" else
                                    f"{D.ws} rank(s), database sharded by signal + NCCL gather of the winners"),
-                   "process_group": D.backend},
+                   "process_group": D.backend, "early_fill": 1},
         "gpu_launches": args.steps * launches,
         "roofline": main_rec["roofline"],
         "e2e": h.get("e2e"),

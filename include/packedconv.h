@@ -102,7 +102,10 @@ typedef struct conv_opts {
                                W_block <= 25,600); 0 in the producer warps                  */
   int32_t early_fill;       /* 1: a persistent launch's pipeline fill may overlap the tail of
                                the preceding launch on the stream when that launch does not
-                               write this launch's input (host-checked); 0 off              */
+                               write this launch's input (host-checked against this library's
+                               own launches; do not enable when a foreign kernel with its own
+                               programmatic-launch trigger may write the input on the same
+                               stream); 0 off (default)                                      */
   int32_t validate_trials;  /* FFT core: worst-case operand pairs of the backend validation
                                run by conv_plan_set_kernel, 0 = 128             */
   double u_sys;             /* P:153; used by the literal paper unpack form                */
