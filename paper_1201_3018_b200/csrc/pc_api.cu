@@ -407,6 +407,7 @@ void fill_modep(const ModeState& m, int packing, ModeP* mp) {
   const int M = packing == PC_PACK_ASYM3 ? 3 : 2;
   mp->alu_pack = packing != PC_PACK_FULL && m.b > 0 && (M - 1) * m.b <= 60 &&
                  (double)m.Q * (std::ldexp(1.0, (M - 1) * m.b) * 2.0) < std::ldexp(1.0, 53);
+  mp->exact_pack = mp->alu_pack;   // (not cleared with alu_pack: the FMA form is the default)
   mp->K = m.K;
   mp->K_pad = m.K_pad;
   mp->rows = m.rows;

@@ -89,6 +89,7 @@ struct ModeP {
   int pow2;             // eps = 2^-b (reading C4)
   int b;                // that b (0 if eps is not a power of two)
   int alu_pack;         // tiled kernel: pack with integer ops (dyadic eps, every packed word < 2^53 in units)
+  int exact_pack;       // dyadic eps and every packed word exact in FP64: Horner steps as one FMA (same bits)
   int K, K_pad;         // core taps and taps padded to a multiple of the kernel's tile T
   int rows;             // rows of the column layout of the core's input words
   int paper_unpack;     // SYM: literal Eqs. (11)-(15) with the u_sys guard instead of balanced digits

@@ -155,6 +155,14 @@ __device__ __forceinline__ unsigned long long abs_bits(double x) {
 }
 __device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) { return a > b ? a : b; }
 
+// One Horner step of Eqs. (4)/(7), lo + eps * hi, in the oracle's order (product, then sum); when
+// every packed word is exact in FP64 (dyadic eps, ModeP::exact_pack) both roundings are exact and
+// one FMA gives the same bits with one FP64 instruction fewer (the producers wait behind the DMMA
+// warps for every FP64 instruction they issue).
+__device__ __forceinline__ double horner_step(const ModeP& mp, double lo, double hi) {
+  return mp.exact_pack ? fma(mp.eps, hi, lo) : __dadd_rn(lo, __dmul_rn(mp.eps, hi));
+}
+
 // a4 for one stage: core words [cw0, cw0 + rows_s*T) of block b into the padded row-major
 // window xs[(i / T) * PT + i % T] (pitch PT = T + 1 for the FMA core, T + 4 for the DMMA core).  Word-major over the producer threads (coalesced
 // loads), UW words per thread with every sample load issued before any use.
@@ -204,7 +212,7 @@ __device__ __forceinline__ void pack_window(const Geo& g, const Blk& b, const Mo
           }
         } else {
 #pragma unroll
-          for (int u = 0; u < UW; ++u) v[u] = pack_sym(compand1(c_s, x0[u]), compand1(c_s, x1[u]), mp.eps);
+          for (int u = 0; u < UW; ++u) v[u] = horner_step(mp, compand1(c_s, x0[u]), compand1(c_s, x1[u]));
         }
       } else if (PACK == PACK_ASYM2 || PACK == PACK_ASYM3) {
         constexpr int M = (PACK == PACK_ASYM2) ? 2 : 3;
@@ -227,7 +235,7 @@ __device__ __forceinline__ void pack_window(const Geo& g, const Blk& b, const Mo
           for (int u = 0; u < UW; ++u) {
             double a = compand1(c_s, x[M - 1][u]);         // Horner, oracle order
 #pragma unroll
-            for (int q = M - 2; q >= 0; --q) a = __dadd_rn(compand1(c_s, x[q][u]), __dmul_rn(mp.eps, a));
+            for (int q = M - 2; q >= 0; --q) a = horner_step(mp, compand1(c_s, x[q][u]), a);
             v[u] = a;
           }
         }
@@ -262,7 +270,7 @@ __device__ __forceinline__ void pack_window(const Geo& g, const Blk& b, const Mo
 #pragma unroll
         for (int u = 0; u < UW; ++u) {
           const int cw = cw0 + i0 + u * nprod;
-          v[u] = (cw >= b.pre && cw < b.xlen) ? pack_sym(compand1(c_s, x0[u]), compand1(c_s, x1[u]), mp.eps) : 0.0;
+          v[u] = (cw >= b.pre && cw < b.xlen) ? horner_step(mp, compand1(c_s, x0[u]), compand1(c_s, x1[u])) : 0.0;
         }
       }
     } else if (PACK == PACK_ASYM2 || PACK == PACK_ASYM3) {
@@ -287,7 +295,7 @@ __device__ __forceinline__ void pack_window(const Geo& g, const Blk& b, const Mo
         for (int u = 0; u < UW; ++u) {
           double a = compand1(c_s, x[M - 1][u]);         // Horner, oracle order
 #pragma unroll
-          for (int q = M - 2; q >= 0; --q) a = __dadd_rn(compand1(c_s, x[q][u]), __dmul_rn(mp.eps, a));
+          for (int q = M - 2; q >= 0; --q) a = horner_step(mp, compand1(c_s, x[q][u]), a);
           const int cw = cw0 + i0 + u * nprod;
           v[u] = (cw >= 0 && cw < b.xlen) ? a : 0.0;
         }
