@@ -92,14 +92,20 @@ typedef struct conv_opts {
   int32_t unpack_form;      /* PC_UNPACK_BALANCED, or PC_UNPACK_LITERAL: the literal
                                Eqs. (11)-(15) with the u_sys guard (symmetric packing, direct
                                core; exact for R_max < 89,524, reading C6)                 */
-  int32_t pack_alu;         /* persistent core producers: 1 = compand/pack with integer ops
-                               (dyadic eps; bit-identical), 0 FP64 ops                      */
+  int32_t pack_alu;         /* persistent DMMA-core producers: 1 = c_s, (c_s c_k)^-1, companding and
+                               packing with integer/FP32 ops, bit-identical to the FP64 ops
+                               (dyadic eps, exact packed words; measured slower, DESIGN.md
+                               §7.3); 0 or 2 = FP64 ops                                     */
   int32_t stage_cap;        /* >= 2: cap on the persistent kernel's stage-ring slots; < 0: the
                                producers claim job m only once consumers hold parts of
                                m + stage_cap; 0 automatic                                   */
   int32_t prepack;          /* 1: compand/pack in a prepack kernel ahead of the persistent
                                launch instead of its producer warps (single-chunk plans,
-                               W_block <= 25,600); 0 in the producer warps                  */
+                               W_block <= 25,600); -P (P >= 1): producer-SM mode (DMMA-core
+                               plans; else ignored) -- the persistent launch's first P CTAs (at most half of the SMs)
+                               compand and pack jobs into stage images in HBM/L2 and flag
+                               them, the other CTAs pack their pipeline fill and bulk-copy the
+                               rest (measured slower); 0 in the producer warps */
   int32_t early_fill;       /* 1: a persistent launch's pipeline fill may overlap the tail of
                                the preceding launch on the stream when that launch does not
                                write this launch's input (host-checked against this library's

@@ -7,7 +7,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SOURCES = [os.path.join(HERE, "csrc", f) for f in ("pc_kernels.cu", "pc_tiled.cu", "pc_fft.cu", "pc_api.cu")]
-DEPS = SOURCES + [os.path.join(HERE, "csrc", f) for f in ("pc_device.cuh", "pc_kernels.h")] + \
+DEPS = SOURCES + [os.path.join(HERE, "csrc", f) for f in ("pc_device.cuh", "pc_kernels.h", "pc_intfp.cuh")] + \
     [os.path.join(ROOT, "include", "packedconv.h")]
 OUT = os.path.join(HERE, "libpackedconv.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

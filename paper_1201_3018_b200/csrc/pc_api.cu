@@ -84,6 +84,7 @@ struct conv_plan {
   int ctr_flip = 0;                     // the array the next non-adaptive tiled launch uses
   int cand_ok = 0;                      // adaptive: d_cand holds this kernel's candidate table
   double* d_pre = nullptr;              // prepacked stage images + per-job inverse scales (pc_prepack_kernel)
+  long long pre_flags_jobs = -1;         // producer-SM mode: job count the ready flags were zeroed for
   long long pre_cap = 0;                // doubles allocated at d_pre
   // FFT core
   int fft_N = 0;                       // complex points (real transform length 2N)
@@ -502,7 +503,7 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
   e.reg_path = per_block_ok ? sh.reg_path : 0;
   for (int i = 0; i < np; ++i) {
     fill_modep(p->ms[packs[i]], packs[i], &e.mp[packs[i]]);
-    if (p->opts.pack_alu != 1) e.mp[packs[i]].alu_pack = 0;   // integer packing only when asked
+    if (p->opts.pack_alu != 1) e.mp[packs[i]].alu_pack = 0;   // integer companding/packing only when asked (measured slower)
   }
   if (p->opts.unpack_form == PC_UNPACK_LITERAL) {   // literal Eqs. (11)-(15) (SYM, tiled kernel)
     pc::ModeP& ms = e.mp[PC_PACK_SYM];
@@ -609,22 +610,39 @@ int run_exec(conv_plan* p, const double* s, long long s_off, long long s_stride,
     // a2-a4 ahead of the DMMA-core launch (single-chunk packed plans, opts.prepack = 1): measured
     // slower than the fused producers at cfg2 (the separate pass costs ~26 us, the persistent
     // kernel's tail does not shrink), so off by default
-    if (ts.nchunks == 1 && p->packing != PC_PACK_FULL && p->opts.prepack == 1 &&
+    const bool split = ts.nchunks == 1 && p->packing != PC_PACK_FULL && p->opts.prepack < 0 && !pairs;
+    if (ts.nchunks == 1 && p->packing != PC_PACK_FULL && (p->opts.prepack == 1 || split) &&
         (long long)p->W_block * 8 <= 200 * 1024) {
       const long long stride = ((long long)(ts.T + (ts.mma ? 4 : 1)) * ts.rows_s + 1) & ~1LL;   // stage_x of pc_tiled_kernel
-      const long long need = njobs * stride + njobs;
+      const long long nflag = (njobs + 1) / 2;        // doubles holding the u32 ready flags
+      const long long need = njobs * stride + njobs + nflag;
       if (need > p->pre_cap) {
         cudaFree(p->d_pre);
         p->d_pre = nullptr;
         p->pre_cap = 0;
         if (cudaMalloc(&p->d_pre, sizeof(double) * need) != cudaSuccess) return PC_E_CUDA;
+        if (cudaMemsetAsync(p->d_pre + njobs * stride + njobs, 0, sizeof(double) * nflag, st) != cudaSuccess)
+          return PC_E_CUDA;
         p->pre_cap = need;
+        p->pre_flags_jobs = njobs;
       }
       e.pre_win = p->d_pre;
       e.pre_stride = stride;
       e.pre_inv = p->d_pre + njobs * stride;
-      if (pc::launch_prepack(p->packing, ts.T, ts.mma, make_geo(p), e, njobs, st) != cudaSuccess) return PC_E_CUDA;
-      e.raw_slots = 0;                                 // the producers only move prepacked windows
+      if (split) {
+        e.split_P = std::min(-p->opts.prepack, 64);
+        e.split_flags = reinterpret_cast<unsigned*>(p->d_pre + njobs * stride + njobs);
+        e.split_ctl = p->d_counter + 2 * (pc::kCtrDone + 1);
+        if (p->pre_flags_jobs != njobs) {              // flag array re-laid for this job count: zero it and the epoch
+          if (cudaMemsetAsync(e.split_flags, 0, sizeof(unsigned) * njobs, st) != cudaSuccess ||
+              cudaMemsetAsync(e.split_ctl, 0, sizeof(unsigned), st) != cudaSuccess)
+            return PC_E_CUDA;
+          p->pre_flags_jobs = njobs;
+        }
+      } else {
+        if (pc::launch_prepack(p->packing, ts.T, ts.mma, make_geo(p), e, njobs, st) != cudaSuccess) return PC_E_CUDA;
+        e.raw_slots = 0;                               // the producers only move prepacked windows
+      }
     }
     // a2 ahead (PC_PEAK_AHEAD builds): the block peaks of this launch's blocks in one bandwidth-bound
     // pass, so the producers only compand and pack (their peak pass runs 3-6x slower next to the
@@ -747,8 +765,9 @@ int conv_plan_create(conv_plan** out, int64_t L, int32_t N, int32_t W_block, int
   e = cudaMalloc(&p->d_k_pad, sizeof(double) * Np);
   if (e == cudaSuccess) e = cudaMalloc(&p->d_k_int, sizeof(double) * Np);
   if (e == cudaSuccess) e = cudaMalloc(&p->d_scal, sizeof(double) * 4);
-  if (e == cudaSuccess) e = cudaMalloc(&p->d_counter, 2 * (pc::kCtrDone + 1) * sizeof(unsigned));   // two arrays
-  if (e == cudaSuccess) e = cudaMemset(p->d_counter, 0, 2 * (pc::kCtrDone + 1) * sizeof(unsigned));
+  // two arrays of queue counters (alternating launches) + the producer-SM mode's epoch
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_counter, (2 * (pc::kCtrDone + 1) + 8) * sizeof(unsigned));
+  if (e == cudaSuccess) e = cudaMemset(p->d_counter, 0, (2 * (pc::kCtrDone + 1) + 8) * sizeof(unsigned));
   if (e == cudaSuccess) e = cudaHostAlloc(&p->h_status, 4 * sizeof(int), cudaHostAllocMapped);
   if (e == cudaSuccess) {
     std::memset(p->h_status, 0, 4 * sizeof(int));

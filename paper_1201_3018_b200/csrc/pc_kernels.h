@@ -158,8 +158,17 @@ struct Exec {
   // plans) at blk_peak[sig * peak_stride + w]; nullptr: the producers compute them
   const double* blk_peak;
   long long peak_stride;
+  // producer SMs (conv_opts.prepack < 0, single-chunk packed plans; needs pre_win/pre_inv): CTAs
+  // [0, split_P) compand and pack jobs F, F+1, .. into their stage images at pre_win (one job per
+  // group of four warps, no DMMA warps on those SMs) and raise split_flags[j] = epoch + 1; the
+  // other CTAs pack their first jobs in the pipeline fill (F = their count x fill depth) and move
+  // the rest into the ring by bulk copy once flagged.  split_ctl[0] = epoch (launch count).
+  int split_P;
+  unsigned* split_flags;
+  unsigned* split_ctl;
 };
 constexpr int kStatusMargin = 0, kStatusWatchdog = 1;
+constexpr int kCtrProd = 250, kCtrCons = 251;   // sm_ctr slots of the producer-SM mode (reset per launch)
 
 // FFT overlap-save core (pc_fft.cu).
 struct FftArgs {

@@ -28,6 +28,7 @@
 #include <cstdio>
 
 #include "pc_device.cuh"
+#include "pc_intfp.cuh"
 #include "pc_kernels.h"
 
 #ifndef PC_QUEUE_MIN
@@ -41,6 +42,15 @@
 #endif
 #ifndef PC_DMMA_NAP
 #define PC_DMMA_NAP 0     // ns a DMMA-core warp sleeps after each k-step (0: none)
+#endif
+#ifndef PC_VEC_PEAK
+#define PC_VEC_PEAK 1     // raw-staged producers: block peak by 16-byte shared-memory loads
+#endif
+#ifndef PC_PAIR_PACK
+#define PC_PAIR_PACK 1    // raw-staged producers, asymmetric packing: word pairs by 16-byte loads / stores
+#endif
+#ifndef PC_SPLIT_AHEAD
+#define PC_SPLIT_AHEAD 2  // producer-SM mode: job claims ahead of the consumers' part claims
 #endif
 #ifndef PC_CORE_SLOTS
 #define PC_CORE_SLOTS 2   // DMMA core: warps per SM sub-partition allowed in the core at once
@@ -65,6 +75,7 @@ struct TSmem {
   double fcs[16], finv[16];         // their c_s and (c_s c_k)^-1
   long long m_end;                  // first job sequence whose claim failed (-1: not yet)
   uint64_t rawbar[2];               // raw-staged producers: TMA arrival of raw slot k
+  uint64_t pbar[4];                 // producer CTAs (producer-SM mode): TMA arrival of group g's raw block
   long long pjob[2];                // raw-staged producers: claimed job of sequence m (slot m & 1)
   double red[32];
   long long cyc[4];   // diagnostics (consumer thread 0): wait, core, unpack/store cycles; clock mark
@@ -129,26 +140,101 @@ __device__ __forceinline__ JobPos job_pos(const Exec& e, long long job) {
   return p;
 }
 
-// ---- integer (ALU-pipe) forms of the producer's arithmetic.  The DMMA core keeps the SM
-// sub-partition's FP64 pipe busy in 16-cycle DMMA slots, so every FP64 instruction a producer
-// issues waits behind them; everything below that need not be FP64 runs on the integer ALU.
-// round(p), half away from zero (Eq. (2)'s rounding, C-library / oracle semantics), for
-// |p| < 2^52: p = mant * 2^-sh exactly, so round(|p|) = floor((mant + 2^(sh-1)) / 2^sh).
-__device__ __forceinline__ long long round_away_alu(double p) {
-  const unsigned long long u = (unsigned long long)__double_as_longlong(p);
-  const int sh = min(max(1075 - (int)((u >> 52) & 0x7ff), 1), 63);
-  const unsigned long long mant = (u & 0xfffffffffffffull) | 0x10000000000000ull;
-  const long long r = (long long)((mant + (1ull << (sh - 1))) >> sh);
-  return (long long)u < 0 ? -r : r;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
-// n * 2^-e2 as a double, exact for |n| < 2^53 (normalise with the leading-zero count).
-__device__ __forceinline__ double i2d_scaled_alu(long long n, int e2) {
-  const unsigned long long a = (unsigned long long)(n < 0 ? -n : n);
-  const int msb = 63 - __clzll(a);
-  const unsigned long long bits = ((unsigned long long)(1023 + msb - e2) << 52) |
-                                  ((a << (52 - msb)) & 0xfffffffffffffull) | (n < 0 ? 0x8000000000000000ull : 0ull);
-  return a == 0 ? 0.0 : __longlong_as_double((long long)bits);
+
+// ---- integer (ALU-pipe) forms of the producer's arithmetic (pc_intfp.cuh): while two warps of an
+// SM sub-partition issue DMMAs, an FP64 instruction of any other warp there waits until they
+// pause (3.6-9.5 us measured for the first one of a producer's job), so with ModeP::alu_pack the
+// producer warps compute c_s, (c_s c_k)^-1, the companded samples and the packed words with
+// integer instructions only -- the same bits as the FP64 forms (tests/test_intfp.py).  An
+// operand outside the integer forms' domain (subnormal, overflow) takes the FP64 instruction.
+__device__ __forceinline__ uint64_t dbits(double x) { return (uint64_t)__double_as_longlong(x); }
+__device__ __forceinline__ double bitsd(uint64_t u) { return __longlong_as_double((long long)u); }
+// c_s = Q / peak (Eq. (2); all-zero block: 1), the IEEE quotient
+__device__ __forceinline__ double cs_quot(const ModeP& mp, double peak, bool alu) {
+  const uint64_t pb = dbits(peak);
+  if ((pb << 1) == 0) return 1.0;                    // +-0 (bit test: no FP64 compare)
+  uint64_t r;
+  if (alu && ifp::ddiv_rn_pos(dbits(mp.Q), pb, r)) return bitsd(r);
+  return mp.Q / peak;
 }
+// Eq. (16)'s (c_s c_k)^-1: one product, one IEEE division (reading C11)
+__device__ __forceinline__ double inv_scale(const ModeP& mp, double c_s, double c_k, bool alu) {
+  uint64_t p, r;
+  if (alu && ifp::dmul_rn_pos(dbits(c_s), dbits(c_k), p) && ifp::ddiv_rn_pos(dbits(1.0), p, r)) return bitsd(r);
+  return dequant_scale(c_s, c_k);
+}
+// One packed word of M companded samples x[0..M-1] (Eq. (7) Horner in the oracle's order; for
+// symmetric packing M = 2, Eq. (4)): integer digits n_q = round(c_s x_q), word = N 2^-((M-1) b)
+// with N = sum n_q 2^((M-1-q) b), exact under ModeP::exact_pack (alu_pack implies it).  The
+// exact integer form (~100 instructions per sample); pack_word_fast below is the common path.
+template <int M>
+__device__ __noinline__ double pack_word_exact(const ModeP& mp, double c_s, double x0, double x1, double x2) {
+  const double x[3] = {x0, x1, x2};
+  long long N = 0;
+  bool neg0 = true, ok = true;
+#pragma unroll
+  for (int q = 0; q < M; ++q) {
+    long long n;
+    bool z;
+    ok = ifp::compand_int(dbits(c_s), dbits(x[q]), n, z) && ok;
+    N = N * (1LL << mp.b) + n;
+    neg0 = neg0 && z;
+  }
+  if (ok) return bitsd(ifp::i2d_scaled(N, (M - 1) * mp.b, neg0));
+  double a = compand1(c_s, x[M - 1]);                // FP64 forms (operand outside the integer domain)
+#pragma unroll
+  for (int q = M - 2; q >= 0; --q) a = __dadd_rn(compand1(c_s, x[q]), __dmul_rn(mp.eps, a));
+  return a;
+}
+// |x| truncated to a float (24 leading significand bits; 0 below 2^-126): relative error < 2^-23
+__device__ __forceinline__ float f32_trunc_abs(double x) {
+  const uint32_t ah = (uint32_t)__double2hiint(x) & 0x7fffffffu, lo = (uint32_t)__double2loint(x);
+  const int t = (int)(ah - (896u << 20));              // exponent rebias 1023 -> 127
+  return t < (1 << 20) ? 0.0f : __int_as_float((t << 3) | (int)(lo >> 29));
+}
+// Fast companding (FP32 + integer instructions): y = c_f |x| with c_f = c_s and |x| truncated to
+// floats is within 2.5 * 2^-23 Q of c_s |x| (|x| <= the block peak, so c_s |x| <= Q); its nearest
+// integer is round(RN(c_s x)) unless y lies within thr of a half-integer, where the word is
+// recomputed exactly (pack_word_exact; about one sample in 1 / (2^-19 Q)).  Valid per job when
+// Q <= 2^19 and c_s in [2^-100, 2^100] (floats normal, y < 2^22).
+struct FastCs {
+  float c, thr;   // c_f, ambiguity threshold 0.5 - Q 2^-20 (twice the error bound)
+  bool ok;
+};
+__device__ __forceinline__ FastCs fast_cs(const ModeP& mp, double c_s, bool alu) {
+  FastCs f;
+  const int ec = (int)((dbits(c_s) >> 52) & 0x7ff);
+  // (bit compares and truncations only: an FP64 compare or conversion would wait behind the DMMAs)
+  f.ok = alu && dbits(mp.Q) <= 0x4120000000000000ull && ec >= 1023 - 100 && ec <= 1023 + 100;   // Q <= 2^19
+  f.c = f32_trunc_abs(c_s);
+  f.thr = __fsub_rn(0.5f, __fmul_rn(f32_trunc_abs(mp.Q), 9.5367431640625e-07f));   // 0.5 - Q 2^-20 (Q exact)
+  return f;
+}
+template <int M>
+__device__ __forceinline__ double pack_word_fast(const FastCs& f, const ModeP& mp, double c_s, const double (&x)[M]) {
+  if (!f.ok) return pack_word_exact<M>(mp, c_s, x[0], x[1], M > 2 ? x[M - 1] : 0.0);
+  long long N = 0;
+  bool neg0 = true, amb = false;
+#pragma unroll
+  for (int q = 0; q < M; ++q) {
+    const float y = __fmul_rn(f.c, f32_trunc_abs(x[q]));
+    const float r = __fadd_rn(y, 12582912.0f);          // 1.5 * 2^23: round to nearest even
+    const float d = __fsub_rn(y, __fsub_rn(r, 12582912.0f));
+    amb = amb || fabsf(d) > f.thr;
+    const int a = __float_as_int(r) - 0x4B400000;
+    const bool neg = __double2hiint(x[q]) < 0;
+    N = N * (1LL << mp.b) + (neg ? -a : a);
+    neg0 = neg0 && neg && a == 0;
+  }
+  if (amb) return pack_word_exact<M>(mp, c_s, x[0], x[1], M > 2 ? x[M - 1] : 0.0);
+  return bitsd(ifp::i2d_scaled(N, (M - 1) * mp.b, neg0));
+}
+
 // |x| as ordered integer bits (non-negative doubles order like their bit patterns).
 __device__ __forceinline__ unsigned long long abs_bits(double x) {
   return (unsigned long long)__double_as_longlong(x) & 0x7fffffffffffffffull;
@@ -166,16 +252,17 @@ __device__ __forceinline__ double horner_step(const ModeP& mp, double lo, double
 // a4 for one stage: core words [cw0, cw0 + rows_s*T) of block b into the padded row-major
 // window xs[(i / T) * PT + i % T] (pitch PT = T + 1 for the FMA core, T + 4 for the DMMA core).  Word-major over the producer threads (coalesced
 // loads), UW words per thread with every sample load issued before any use.
-template <int PACK, int T, int UWF = 1, int PT = T + 1, bool SRC_SMEM = false>
+template <int PACK, int T, int UWF = 1, int PT = T + 1, bool SRC_SMEM = false, bool ALU = false>
 __device__ __forceinline__ void pack_window(const Geo& g, const Blk& b, const ModeP& mp, const double* gsrc,
                                             int n_valid, double c_s, int cw0, int rows_s, double* xs, int ptid,
-                                            int nprod) {
+                                            int nprod, bool alu) {
   constexpr int UW = UWF * ((PACK == PACK_ASYM3) ? 4 : 8);   // words per thread in flight
   const int words = rows_s * T;
   auto sample = [&](int i) -> double {
     return (i < 0 || i >= n_valid) ? 0.0 : (SRC_SMEM ? gsrc[i] : __ldg(gsrc + i));
   };
-  const bool alu = mp.alu_pack;                              // warp-uniform (per plan)
+  if (!ALU) alu = false;                             // (the integer forms are compiled only where asked)
+  const FastCs fcs = fast_cs(mp, c_s, alu);
   // window words [ilo, ihi) whose core word is inside the block's input (cw in [pre, xlen)) and
   // whose samples are all inside the block's valid samples: there, no per-sample / per-word range
   // checks (the checks were a fifth of the producers' instructions)
@@ -193,22 +280,89 @@ __device__ __forceinline__ void pack_window(const Geo& g, const Blk& b, const Mo
       ihi = min(words, min(b.xlen - cw0, n_valid - base - span));
     }
   }
+  // Raw block in shared memory, asymmetric packing, even pitch: the interior in word pairs
+  // (2j, 2j + 1) -- one 16-byte load per sample stream where it is aligned and one 16-byte store
+  // per pair (the producers' shared-memory instructions queue behind the DMMA warps' fragment
+  // loads, so fewer, wider ones shorten every job's packing).  Same arithmetic per word.
+  int wlo = 0, whi = 0;                              // words [wlo, whi) done by the pair loop (none by default)
+  if constexpr (PC_PAIR_PACK && SRC_SMEM && (PACK == PACK_ASYM2 || PACK == PACK_ASYM3) && PT % 2 == 0 && T % 2 == 0) {
+    constexpr int M = (PACK == PACK_ASYM2) ? 2 : 3;
+    constexpr int UP = UW / 2;                       // pairs per thread in flight
+    const double* src = gsrc + (b.o0 - (g.Np - 1) + cw0);
+    const int plo = (ilo + 1) >> 1, phi = ihi >> 1;  // pairs wholly inside [ilo, ihi)
+    if ((reinterpret_cast<uintptr_t>(xs) & 15u) == 0 && phi > plo) {
+      bool al[M];
+#pragma unroll
+      for (int q = 0; q < M; ++q) al[q] = (reinterpret_cast<uintptr_t>(src + q * b.S) & 15u) == 0;
+      wlo = 2 * plo;
+      whi = 2 * phi;
+      for (int j0 = plo + ptid; j0 < phi; j0 += UP * nprod) {
+        double2 x[M][UP];
+#pragma unroll
+        for (int u = 0; u < UP; ++u) {
+          const int j = min(j0 + u * nprod, phi - 1);   // clamped lanes recompute pair phi-1 (not stored)
+#pragma unroll
+          for (int q = 0; q < M; ++q) {
+            const double* p2 = src + q * b.S + 2 * j;
+            x[q][u] = al[q] ? *reinterpret_cast<const double2*>(p2) : make_double2(p2[0], p2[1]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < UP; ++u) {
+          const int j = j0 + u * nprod;
+          double lo, hi;
+          if (alu) {
+            double xl[M], xh[M];
+#pragma unroll
+            for (int q = 0; q < M; ++q) {
+              xl[q] = x[q][u].x;
+              xh[q] = x[q][u].y;
+            }
+            lo = pack_word_fast<M>(fcs, mp, c_s, xl);
+            hi = pack_word_fast<M>(fcs, mp, c_s, xh);
+          } else {
+            lo = compand1(c_s, x[M - 1][u].x);           // Horner, oracle order
+            hi = compand1(c_s, x[M - 1][u].y);
+#pragma unroll
+            for (int q = M - 2; q >= 0; --q) {
+              lo = horner_step(mp, compand1(c_s, x[q][u].x), lo);
+              hi = horner_step(mp, compand1(c_s, x[q][u].y), hi);
+            }
+          }
+          if (j < phi) {
+            const int i = 2 * j;
+            *reinterpret_cast<double2*>(xs + (i / T) * PT + i % T) = make_double2(lo, hi);
+          }
+        }
+      }
+    }
+  }
   for (int i0 = ptid; i0 < words; i0 += UW * nprod) {
     double v[UW];
-    if (i0 >= ilo && i0 + (UW - 1) * nprod < ihi) {   // interior: unchecked
+    if (i0 >= wlo && i0 + (UW - 1) * nprod < whi) continue;   // done by the pair loop
+    if (i0 >= ilo && i0 + (UW - 1) * nprod < ihi && (i0 + (UW - 1) * nprod < wlo || i0 >= whi)) {   // interior: unchecked
       if (PACK == PACK_SYM) {
         double x0[UW], x1[UW];
+        if (PC_PAIR_PACK && SRC_SMEM && (reinterpret_cast<uintptr_t>(gsrc) & 15u) == 0) {   // one 16-byte load per word
 #pragma unroll
-        for (int u = 0; u < UW; ++u) {
-          const int j = cw0 + i0 + u * nprod - b.pre;
-          x0[u] = SRC_SMEM ? gsrc[2 * j] : __ldg(gsrc + 2 * j);
-          x1[u] = SRC_SMEM ? gsrc[2 * j + 1] : __ldg(gsrc + 2 * j + 1);
+          for (int u = 0; u < UW; ++u) {
+            const double2 x2 = reinterpret_cast<const double2*>(gsrc)[cw0 + i0 + u * nprod - b.pre];
+            x0[u] = x2.x;
+            x1[u] = x2.y;
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < UW; ++u) {
+            const int j = cw0 + i0 + u * nprod - b.pre;
+            x0[u] = SRC_SMEM ? gsrc[2 * j] : __ldg(gsrc + 2 * j);
+            x1[u] = SRC_SMEM ? gsrc[2 * j + 1] : __ldg(gsrc + 2 * j + 1);
+          }
         }
         if (alu) {
 #pragma unroll
           for (int u = 0; u < UW; ++u) {
-            const long long n = round_away_alu(__dmul_rn(c_s, x0[u])) * (1LL << mp.b) + round_away_alu(__dmul_rn(c_s, x1[u]));
-            v[u] = i2d_scaled_alu(n, mp.b);
+            const double xx[2] = {x0[u], x1[u]};
+            v[u] = pack_word_fast<2>(fcs, mp, c_s, xx);
           }
         } else {
 #pragma unroll
@@ -225,10 +379,10 @@ __device__ __forceinline__ void pack_window(const Geo& g, const Blk& b, const Mo
         if (alu) {                                           // integer Horner (dyadic eps), same bits
 #pragma unroll
           for (int u = 0; u < UW; ++u) {
-            long long n = round_away_alu(__dmul_rn(c_s, x[0][u]));
+            double xx[M];
 #pragma unroll
-            for (int q = 1; q < M; ++q) n = n * (1LL << mp.b) + round_away_alu(__dmul_rn(c_s, x[q][u]));
-            v[u] = i2d_scaled_alu(n, (M - 1) * mp.b);
+            for (int q = 0; q < M; ++q) xx[q] = x[q][u];
+            v[u] = pack_word_fast<M>(fcs, mp, c_s, xx);
           }
         } else {
 #pragma unroll
@@ -263,8 +417,8 @@ __device__ __forceinline__ void pack_window(const Geo& g, const Blk& b, const Mo
 #pragma unroll
         for (int u = 0; u < UW; ++u) {
           const int cw = cw0 + i0 + u * nprod;
-          const long long n = round_away_alu(__dmul_rn(c_s, x0[u])) * (1LL << mp.b) + round_away_alu(__dmul_rn(c_s, x1[u]));
-          v[u] = (cw >= b.pre && cw < b.xlen) ? i2d_scaled_alu(n, mp.b) : 0.0;
+          const double xx[2] = {x0[u], x1[u]};
+          v[u] = (cw >= b.pre && cw < b.xlen) ? pack_word_fast<2>(fcs, mp, c_s, xx) : 0.0;
         }
       } else {
 #pragma unroll
@@ -284,11 +438,11 @@ __device__ __forceinline__ void pack_window(const Geo& g, const Blk& b, const Mo
       if (alu) {                                             // integer Horner: n = sum s~_q 2^((M-1-q) b)
 #pragma unroll
         for (int u = 0; u < UW; ++u) {
-          long long n = round_away_alu(__dmul_rn(c_s, x[0][u]));
+          double xx[M];
 #pragma unroll
-          for (int q = 1; q < M; ++q) n = n * (1LL << mp.b) + round_away_alu(__dmul_rn(c_s, x[q][u]));
+          for (int q = 0; q < M; ++q) xx[q] = x[q][u];
           const int cw = cw0 + i0 + u * nprod;
-          v[u] = (cw >= 0 && cw < b.xlen) ? i2d_scaled_alu(n, (M - 1) * mp.b) : 0.0;
+          v[u] = (cw >= 0 && cw < b.xlen) ? pack_word_fast<M>(fcs, mp, c_s, xx) : 0.0;
         }
       } else {
 #pragma unroll
@@ -311,7 +465,7 @@ __device__ __forceinline__ void pack_window(const Geo& g, const Blk& b, const Mo
 #pragma unroll
     for (int u = 0; u < UW; ++u) {
       const int i = i0 + u * nprod;
-      if (i < words) xs[(i / T) * PT + i % T] = v[u];
+      if (i < words && (i < wlo || i >= whi)) xs[(i / T) * PT + i % T] = v[u];
     }
   }
 }
@@ -351,15 +505,18 @@ __device__ __forceinline__ double block_cs(const ModeP& mp, const double* gsrc, 
   double peak = 0.0;
   for (int wi = 0; wi < nprod / 32; ++wi) peak = fmax(peak, red[wi]);
   named_bar(bar_id, nprod);
-  return (peak == 0.0) ? 1.0 : mp.Q / peak;
+  return cs_quot(mp, peak, false);   // (the pipeline fill: no DMMA warps yet, FP64 is fastest)
 }
 
 // a2/a3 from the raw block in shared memory (raw-staged producers): the same max |x| (integer
 // order of the absolute-value bits) and the same IEEE division as block_cs.
-template <int PACK>
+template <int PACK, bool ALU = false>
 __device__ __forceinline__ double smem_cs(const ModeP& mp, const double* raw, int n_valid, double* red, int ptid,
-                                          int nprod, int bar_id) {
+                                          int nprod, int bar_id, unsigned long long* dg = nullptr) {
   if (PACK == PACK_FULL) return 1.0;
+  // 16-byte loads, eight in flight per thread (the producer warps' shared-memory loads queue
+  // behind the DMMA warps' fragment loads: the number of dependent load rounds sets the time)
+#if !PC_VEC_PEAK
   constexpr int U = 4;
   unsigned long long m[U];
 #pragma unroll
@@ -371,25 +528,49 @@ __device__ __forceinline__ double smem_cs(const ModeP& mp, const double* raw, in
       if (i < n_valid) m[u] = umax64(m[u], abs_bits(raw[i]));
     }
   }
+#else
+  constexpr int U = 8;
+  unsigned long long m[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) m[u] = 0ull;
+  const int h = (reinterpret_cast<uintptr_t>(raw) & 15u) ? 1 : 0;   // raw[h] is 16-byte aligned
+  const double2* r2 = reinterpret_cast<const double2*>(raw + h);
+  const int n2 = n_valid > h ? (n_valid - h) >> 1 : 0;
+  for (int i0 = ptid; i0 < n2; i0 += U * nprod) {
+    double2 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * nprod;
+      v[u] = (i < n2) ? r2[i] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) m[u] = umax64(m[u], umax64(abs_bits(v[u].x), abs_bits(v[u].y)));
+  }
+  if (ptid == 0 && h && n_valid > 0) m[0] = umax64(m[0], abs_bits(raw[0]));
+  if (ptid == 1 % nprod && n_valid > h && ((n_valid - h) & 1)) m[0] = umax64(m[0], abs_bits(raw[n_valid - 1]));
+#endif
 #pragma unroll
   for (int u = 1; u < U; ++u) m[0] = umax64(m[0], m[u]);
+  if (dg) dg[0] = gtimer();
   for (int o = 16; o > 0; o >>= 1) m[0] = umax64(m[0], __shfl_xor_sync(0xffffffffu, m[0], o));
   if ((ptid & 31) == 0) red[ptid >> 5] = __longlong_as_double((long long)m[0]);
   named_bar(bar_id, nprod);
-  double peak = 0.0;
-  for (int wi = 0; wi < nprod / 32; ++wi) peak = fmax(peak, red[wi]);
-  return (peak == 0.0) ? 1.0 : mp.Q / peak;
+  if (dg) dg[1] = gtimer();
+  unsigned long long pb = 0ull;                       // integer max of the warps' bit patterns
+  for (int wi = 0; wi < nprod / 32; ++wi) pb = umax64(pb, (unsigned long long)__double_as_longlong(red[wi]));
+  const double peak = __longlong_as_double((long long)pb);
+  return cs_quot(mp, peak, ALU && mp.alu_pack);
 }
 
 // c_s from a block peak computed ahead (pc_block_peak / pc_block_stats): the same IEEE division.
 template <int PACK>
-__device__ __forceinline__ double cs_from_peak(const ModeP& mp, double peak) {
+__device__ __forceinline__ double cs_from_peak(const ModeP& mp, double peak, bool alu) {
   if (PACK == PACK_FULL) return 1.0;
-  return (peak == 0.0) ? 1.0 : mp.Q / peak;
+  return cs_quot(mp, peak, alu);
 }
 
 // The same for one warp (producer warps work on different jobs): shuffles only.
-template <int PACK>
+template <int PACK, bool ALU = false>
 __device__ __forceinline__ double warp_cs(const ModeP& mp, const double* gsrc, int n_valid, int lane) {
   if (PACK == PACK_FULL) return 1.0;
   constexpr int U = 16;
@@ -417,7 +598,7 @@ __device__ __forceinline__ double warp_cs(const ModeP& mp, const double* gsrc, i
   for (int u = 1; u < U; ++u) m[0] = umax64(m[0], m[u]);
   for (int o = 16; o > 0; o >>= 1) m[0] = umax64(m[0], __shfl_xor_sync(0xffffffffu, m[0], o));
   const double peak = __longlong_as_double((long long)m[0]);
-  return (peak == 0.0) ? 1.0 : mp.Q / peak;
+  return cs_quot(mp, peak, ALU && mp.alu_pack);
 }
 
 __device__ __forceinline__ long long fdiv_floor(long long a, long long b) {
@@ -426,11 +607,6 @@ __device__ __forceinline__ long long fdiv_floor(long long a, long long b) {
 }
 __device__ __forceinline__ long long fdiv_ceil(long long a, long long b) { return -fdiv_floor(-a, b); }
 
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 __device__ __forceinline__ unsigned smid_() {
   unsigned r;
   asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
@@ -558,8 +734,21 @@ __device__ __forceinline__ void retire_cta(const Exec& e) {
   if (atomicAdd(e.sm_ctr + kCtrDone, 1u) == gridDim.x - 1) {
     for (int i = 0; i < e.nsm; ++i) e.sm_ctr[i] = 0u;
     e.sm_ctr[kCtrDone] = 0u;
+    if (e.split_P > 0) {                             // producer-SM mode: counters, and the next launch's epoch
+      e.sm_ctr[kCtrProd] = 0u;
+      e.sm_ctr[kCtrCons] = 0u;
+      atomicAdd(e.split_ctl, 1u);
+    }
     __threadfence();
   }
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 }  // namespace
@@ -675,8 +864,12 @@ __device__ __forceinline__ void conv_chunk_mma(uint32_t xs_row, uint32_t kc_addr
                                t_hi);
 }
 
-template <int PACK, int T, int MMA>
+// VAR = 1: the variant instantiation with the producer-SM mode (conv_opts.prepack < 0) and the
+// integer/FP32 producer arithmetic (pack_alu = 1) compiled in (DMMA-core plans); VAR = 0, the
+// default, compiles neither (their code alone cost the default path 1.4-3.3 us at cfg2).
+template <int PACK, int T, int MMA, int VAR = 0>
 __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, Exec e) {
+  constexpr bool kVar = VAR != 0;
   constexpr int NCW = tiled_cons_warps(MMA);   // consumer warps
   extern __shared__ __align__(128) unsigned char smem[];
   TSmem* ps = reinterpret_cast<TSmem*>(smem);
@@ -699,6 +892,8 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
   double* raw_base = wout + (FRAG_EPI ? (size_t)0 : (size_t)NCW * 32 * (T + 1));   // raw slots (e.raw_slots)
   const int tid = threadIdx.x;
   const int nprod = kTiledProdWarps * 32;
+  const bool split = kVar && e.split_P > 0;         // producer-SM mode (Exec::split_P)
+  const int CP = split ? e.split_P : 0;             // CTAs [0, CP) produce, the others consume
 
   if (tid == 0) {
     mbar_init(&ps->bar_taps, 1);
@@ -721,7 +916,7 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
   // passed griddepcontrol.wait (the trigger follows each wait below), i.e. once the launch before
   // this one has completed -- so the next launch's queue array (the one the launch before used,
   // reset by its last CTA) is free when it claims before its own wait.
-  if (!e.blk_list) {
+  if (!e.blk_list && !split) {
     // While the previous launch drains: L2 prefetch of the input of the (likely) first four
     // jobs of this CTA's queue.  A hint only -- L2 is coherent, so even if the preceding
     // kernel writes the input, the loads after griddepcontrol.wait see its data.
@@ -747,7 +942,7 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   };
-  if (!e.early_fill && !e.early_claim) dep_wait();
+  if (split || (!e.early_fill && !e.early_claim)) dep_wait();
   __syncthreads();
   if (e.dbg_timing && tid == 0) e.dbg_timing[kTimCyc + 4 * blockIdx.x + 2] = gtimer();   // t_start (stash)
   long long njobs = e.jobs_per_sig * e.nsig;
@@ -769,14 +964,15 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
     n_valid = (int)(avail < 0 ? 0 : (avail > g.W_block ? g.W_block : avail));
   };
   // Hand stage `st` to the consumers (+ the tap chunk by TMA when not resident).
-  auto publish = [&](long long n, int st, int c, long long job, double inv, int ptid) {
+  auto publish = [&](long long n, int st, int c, long long job, double inv, int ptid, bool win_src = true) {
+    const bool win = job >= 0 && e.pre_win && win_src;   // the stage image comes from pre_win by bulk copy
     if (ptid == 0) {
       ps->job[st] = job;
       if (job >= 0) ps->jpos[st] = pack_pos(job_pos(e, job));   // consumers skip the 64-bit divisions
-      ps->inv[st] = (job >= 0 && e.pre_win) ? e.pre_inv[job] : inv;
+      ps->inv[st] = win ? e.pre_inv[job] : inv;
       ps->seq[st] = n;
     }
-    const bool taps = job >= 0 && !e.taps_resident, win = job >= 0 && e.pre_win;
+    const bool taps = job >= 0 && !e.taps_resident;
     if ((taps || win) && ptid == 0) {
       const int nt = (c == nch - 1) ? mp.K_pad - c * KC : KC;
       double* xs = stg + (size_t)st * stage_words;
@@ -795,10 +991,115 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
   // parallel (before griddepcontrol.wait: only this launch's queue array is touched), then
   // companded and packed by all 16 warps in four groups of four warps.
   // (never more than a CTA's share of the launch: small launches spread over all CTAs)
+  // Producer-SM mode: the consumer CTAs pack jobs [0, F) in their pipeline fills (job c' + q C for
+  // consumer c' of C, fill slot q), the producer CTAs every later job, in order.
+  const int nfs = min(kTiledFillMax, NS);
+  const int CC = (int)gridDim.x - CP;                 // consumer CTAs
+  const long long F = split ? min(njobs, (long long)nfs * CC) : 0;
+  if (split && (int)blockIdx.x < CP) {
+    // ============================ producer CTA (no DMMA warps on this SM) ============================
+    // Four groups of four warps, one job each: the job's raw block by one TMA bulk copy into the
+    // group's slot (the ring area is free here), the next round's block prefetched into L2, block
+    // peak, companding and packing from shared memory (FP64: nothing here competes for the FP64
+    // pipe) straight into the job's stage image at pre_win, its (c_s c_k)^-1 at pre_inv, then the
+    // job's ready flag (release) for the consumer CTAs.
+    const unsigned want = *reinterpret_cast<volatile unsigned*>(e.split_ctl) + 1u;
+    const int gq = tid >> 7, gtid = tid & 127;
+    const int rstride = (g.W_block + 3) & ~1;          // doubles per raw slot (head offset, even)
+    const bool staged = (size_t)4 * rstride <= (size_t)NS * stage_words;
+    double* raw = stg + (size_t)gq * rstride;
+    if (tid < 4) mbar_init(&ps->pbar[tid], 1);        // the groups' raw-block barriers
+    __syncthreads();
+    uint32_t ph = 0;
+    unsigned long long t_cta0 = 0;
+    if (e.dbg_timing && tid == 0) t_cta0 = gtimer();
+    for (int pj = 0;; ++pj) {
+      // diagnostics: per group and job j < 16 {job | 1 << 62, t claimed, t raw block landed, t flagged}
+      unsigned long long* prec = (e.dbg_timing && gtid == 0 && pj < 16)
+                                     ? e.dbg_timing + kTimP + (((size_t)blockIdx.x * 4 + gq) * 16 + pj) * 4
+                                     : nullptr;
+      if (gtid == 0) ps->fjob[gq] = F + (long long)atomicAdd(e.sm_ctr + kCtrProd, 1u);
+      named_bar(1 + gq, 128);
+      const long long job = ps->fjob[gq];
+      if (job >= njobs) break;
+      if (prec) {
+        prec[0] = (unsigned long long)job | (1ull << 62);
+        prec[1] = gtimer();
+      }
+      JobPos jp;
+      Blk b;
+      const double* gsrc;
+      int n_valid;
+      job_block(job, jp, b, gsrc, n_valid);
+      const int head = (reinterpret_cast<uintptr_t>(gsrc) & 15u) ? 1 : 0, mid = max(0, n_valid - head) & ~1;
+      double* rp = raw + head;                         // rp[i] = block sample i, rp[head] 16-byte aligned
+      if (staged && gtid == 0) {
+        mbar_arrive_expect_tx(&ps->pbar[gq], (uint32_t)mid * 8u);
+        if (mid > 0) bulk_g2s(rp + head, gsrc + head, (uint32_t)mid * 8u, &ps->pbar[gq]);
+        const long long pj = job + 4LL * CP;           // the block this group's next round likely needs
+        if (pj < njobs) {
+          JobPos jq;
+          Blk bq;
+          const double* gq_src;
+          int nq;
+          job_block(pj, jq, bq, gq_src, nq);
+          const uintptr_t a0 = reinterpret_cast<uintptr_t>(gq_src) & ~(uintptr_t)15;
+          const uint32_t bytes = (uint32_t)(((reinterpret_cast<uintptr_t>(gq_src + nq) + 15) & ~(uintptr_t)15) - a0);
+#ifndef PC_NO_SPLIT_PREFETCH
+          if (nq > 0) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"(bytes) : "memory");
+#endif
+        }
+      }
+      double cs;
+      if (staged) {
+        if (gtid == 0 && head && n_valid > 0) rp[0] = __ldg(gsrc);
+        if (gtid == 1 && head + mid < n_valid) rp[n_valid - 1] = __ldg(gsrc + n_valid - 1);
+        mbar_wait_wd(e.status, &ps->pbar[gq], ph, 10, job, gq);
+        ph ^= 1u;
+        named_bar(1 + gq, 128);                        // head / tail elements visible
+        if (prec) prec[2] = gtimer();
+        cs = e.blk_peak ? cs_from_peak<PACK>(mp, e.blk_peak[jp.sig * e.peak_stride + jp.w], false)
+                        : smem_cs<PACK>(mp, rp, n_valid, ps->red + 8 * gq, gtid, 128, 1 + gq);
+        // smem_cs's reduction reads red[] after one barrier: fence the next job's writes to it
+        named_bar(1 + gq, 128);
+      } else {
+        cs = e.blk_peak ? cs_from_peak<PACK>(mp, e.blk_peak[jp.sig * e.peak_stride + jp.w], false)
+                        : block_cs<PACK>(mp, gsrc, n_valid, ps->red + 8 * gq, gtid, 128, 1 + gq);
+      }
+      double* xw = const_cast<double*>(e.pre_win) + job * e.pre_stride;
+      if (staged)
+        pack_window<PACK, T, 1, PT, true>(g, b, mp, rp, n_valid, cs, jp.t * G * T - front * T, rows_s, xw, gtid, 128, false);
+      else
+        pack_window<PACK, T, 1, PT>(g, b, mp, gsrc, n_valid, cs, jp.t * G * T - front * T, rows_s, xw, gtid, 128, false);
+      if (gtid == 0)
+        const_cast<double*>(e.pre_inv)[job] = inv_scale(mp, cs, e.scal_sig ? e.scal_sig[3 * jp.sig + 1] : mp.c_k, false);
+      // the group's stores, then one release by thread 0 (cumulative over the barrier); the
+      // consumer's acquire + proxy fence orders them before its bulk copy
+      named_bar(1 + gq, 128);                          // (also: the raw slot is free for the next copy)
+      if (gtid == 0) st_release_u32(e.split_flags + job, want);
+      if (prec) prec[3] = gtimer();
+    }
+    __syncthreads();
+    if (tid == 0) {
+      if (e.dbg_timing) {
+        e.dbg_timing[4 * blockIdx.x + 0] = smid_();
+        e.dbg_timing[4 * blockIdx.x + 1] = t_cta0;
+        e.dbg_timing[4 * blockIdx.x + 2] = gtimer();
+        e.dbg_timing[4 * blockIdx.x + 3] = 0;
+      }
+      retire_cta(e);
+    }
+    return;
+  }
   const long long share = (njobs + gridDim.x - 1) / gridDim.x;
-  const int nf = e.pre_win ? 0 : (nch == 1) ? (int)min((long long)min(kTiledFillMax, NS), share < 1 ? 1 : share) : 1;
+  const int nf = split ? nfs : e.pre_win ? 0 : (nch == 1) ? (int)min((long long)min(kTiledFillMax, NS), share < 1 ? 1 : share) : 1;
   const int lane_ = tid & 31, warp_ = tid >> 5;
-  if (warp_ < nf) {
+  if (split) {
+    if (tid < nf) {
+      const long long j = (long long)(blockIdx.x - CP) + (long long)tid * CC;
+      ps->fjob[tid] = j < F ? j : -1;
+    }
+  } else if (warp_ < nf) {
     const long long j = claim_job(e, njobs, lane_);
     if (lane_ == 0) ps->fjob[warp_] = j;
   }
@@ -808,11 +1109,11 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
     for (int q = 0; q < nf; ++q)
       if (ps->fjob[q] >= 0) ps->fjob[k++] = ps->fjob[q];
     for (int q = k; q < nf; ++q) ps->fjob[q] = -1;
-    ps->m_end = (k < nf) ? k : -1;
+    ps->m_end = (k < nf && !split) ? k : -1;        // (split: later jobs come from the producer CTAs)
     ps->turn = nf;
   }
   __syncthreads();
-  if (e.early_claim && !e.early_fill) dep_wait();   // the fill reads the input: after the wait
+  if (e.early_claim && !e.early_fill && !split) dep_wait();   // the fill reads the input: after the wait
   {
     constexpr int GW = (kTiledProdWarps + NCW) / kTiledFillJobs;   // warps per fill group
     const int gq = warp_ / GW, gtid = tid - gq * GW * 32;
@@ -829,15 +1130,15 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
                                      : nullptr;
       if (frec) frec[0] = gtimer();
       double* xs_f = stg + (size_t)((f * nch) % NS) * stage_words;
-      const double cs = e.blk_peak ? cs_from_peak<PACK>(mp, e.blk_peak[jp.sig * e.peak_stride + jp.w])
+      const double cs = e.blk_peak ? cs_from_peak<PACK>(mp, e.blk_peak[jp.sig * e.peak_stride + jp.w], false)
                                    : block_cs<PACK>(mp, gsrc, n_valid, ps->red + 8 * gq, gtid, GW * 32, 1 + gq);
       if (frec) frec[1] = gtimer();
       pack_window<PACK, T, 1, PT>(g, b, mp, gsrc, n_valid, cs, jp.t * G * T - front * T, rows_s, xs_f, gtid,
-                                  GW * 32);
+                                  GW * 32, false);   // (no DMMA warps during the fill: FP64 is fastest)
       if (frec) frec[2] = gtimer();
       if (gtid == 0) {
         ps->fcs[f] = cs;
-        ps->finv[f] = dequant_scale(cs, e.scal_sig ? e.scal_sig[3 * jp.sig + 1] : mp.c_k);
+        ps->finv[f] = inv_scale(mp, cs, e.scal_sig ? e.scal_sig[3 * jp.sig + 1] : mp.c_k, false);
       }
     }
   }
@@ -845,6 +1146,52 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
   if (e.early_fill) dep_wait();
   if (e.dbg_timing && tid == 0)
     e.dbg_timing[kTimCyc + 4 * blockIdx.x + 3] = gtimer() - e.dbg_timing[kTimCyc + 4 * blockIdx.x + 2];
+
+  if (tid < nprod && split) {
+    // ============== producer-SM mode: the consumer CTA's producer warps move stage images ==============
+    // Warp 0 publishes the fill's jobs, then claims jobs F, F+1, .. in order from the launch-wide
+    // counter, waits for each one's ready flag and bulk-copies its stage image into the ring.
+    if (tid >= 32) return;
+    const int lane = tid;
+    const int n_sent = NCW / npart;
+    const unsigned want = *reinterpret_cast<volatile unsigned*>(e.split_ctl) + 1u;
+    long long m = 0;
+    for (; m < nf; ++m) {
+      const long long job = ps->fjob[m];
+      if (job < 0) break;
+      publish(m, (int)(m % NS), 0, job, ps->finv[m], lane, false);
+    }
+    for (;; ++m) {
+      long long k = 0;
+      if (lane == 0) {
+        // claim a job only when the consumers hold parts of job m - PC_SPLIT_AHEAD: a CTA with a
+        // free ring would otherwise claim its ring's worth of not-yet-produced jobs, in order,
+        // while other CTAs run dry (head-of-line blocking)
+        Spin sp;
+        while (m >= (long long)*reinterpret_cast<volatile int*>(&ps->mseq_hi) + PC_SPLIT_AHEAD)
+          spin_wd(e.status, sp, 64, 11, m, 0);
+        k = (long long)atomicAdd(e.sm_ctr + kCtrCons, 1u);
+      }
+      k = __shfl_sync(0xffffffffu, k, 0);
+      if (F + k >= njobs) break;
+      const int st = (int)qmod(m, NS);
+      if (m >= NS) mbar_wait_wd(e.status, &ps->empty[st], (uint32_t)((qdiv(m, NS) & 1) ^ 1), 1, m, st);
+      if (lane == 0) {
+        Spin sp;
+        while (ld_acquire_u32(e.split_flags + F + k) != want) spin_wd(e.status, sp, 64, 9, m, st);
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
+      __syncwarp();
+      publish(m, st, 0, F + k, 0.0, lane);
+    }
+    for (const long long me = m; m < me + n_sent; ++m) {   // sentinels, one per consumer warp
+      const int st = (int)qmod(m, NS);
+      if (m >= NS) mbar_wait_wd(e.status, &ps->empty[st], (uint32_t)((qdiv(m, NS) & 1) ^ 1), 1, m, st);
+      publish(m, st, 0, -1, 0.0, lane);
+    }
+    if (lane == 0) retire_cta(e);
+    return;
+  }
 
   if (tid < nprod && e.raw_slots > 0) {
     // ====================== raw-staged producer warps ======================
@@ -952,12 +1299,19 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
       if (pw == 0) mbar_wait_wd(e.status, &ps->rawbar[slot], (rph >> slot) & 1u, 8, m, slot);   // warp 0 waits,
       rph ^= 1u << slot;
       named_bar(PB, nprod);                           // the others here; head / tail elements visible
+      unsigned long long t_rw = 0;
+      if (prec) t_rw = gtimer();
+      // diagnostics: the peak phase's steps (loads + local max, cross-warp reduction, division,
+      // Eq. (16) scale) in producer warp 1's record slots (raw-staged producers use warp 0's only)
+      unsigned long long* dgr = prec ? e.dbg_timing + kTimP + (((size_t)blockIdx.x * 4 + 1) * 16 + pj) * 4 : nullptr;
       const long long blk_id = jp.sig * g.P + jp.w;
       if (blk_id != cur_blk_w) {
         cur_blk_w = blk_id;
-        c_s_w = e.blk_peak ? cs_from_peak<PACK>(mp, e.blk_peak[jp.sig * e.peak_stride + jp.w])
-                           : smem_cs<PACK>(mp, rp, nv, ps->red + 28, ptid, nprod, PB);   // a2/a3
-        inv_w = dequant_scale(c_s_w, e.scal_sig ? e.scal_sig[3 * jp.sig + 1] : mp.c_k);   // Eq. (16)
+        c_s_w = e.blk_peak ? cs_from_peak<PACK>(mp, e.blk_peak[jp.sig * e.peak_stride + jp.w], kVar && mp.alu_pack)
+                           : smem_cs<PACK, kVar>(mp, rp, nv, ps->red + 28, ptid, nprod, PB, dgr);   // a2/a3
+        if (dgr) dgr[2] = gtimer();
+        inv_w = inv_scale(mp, c_s_w, e.scal_sig ? e.scal_sig[3 * jp.sig + 1] : mp.c_k, kVar && mp.alu_pack);   // Eq. (16)
+        if (dgr) dgr[3] = gtimer();
       }
       unsigned long long t_pk = 0, t_sl = 0;
       if (prec) t_pk = gtimer();
@@ -967,14 +1321,15 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
         named_bar(PB, nprod);
       }
       if (prec) t_sl = gtimer();
-      pack_window<PACK, T, 1, PT, true>(g, b, mp, rp, nv, c_s_w, jp.t * G * T - front * T, rows_s,
-                                        stg + (size_t)st * stage_words, ptid, nprod);   // a3/a4
+      pack_window<PACK, T, 1, PT, true, kVar>(g, b, mp, rp, nv, c_s_w, jp.t * G * T - front * T, rows_s,
+                                        stg + (size_t)st * stage_words, ptid, nprod, mp.alu_pack);   // a3/a4
       named_bar(PB, nprod);
       if (pw == 0) publish(m, st, 0, job, inv_w, lane);
-      if (prec) {
+      if (prec) {   // m | (claimed -> raw block landed) | (-> peak done) | (-> slot free), 16-bit fields of 16 ns
         prec[3] = gtimer();
-        const unsigned long long d1 = min((t_pk - prec[2]) >> 4, 0xffffffull), d2 = min((t_sl - t_pk) >> 4, 0xffffffull);
-        prec[0] = (unsigned long long)(m & 0xffff) | (d1 << 16) | (d2 << 40);
+        const unsigned long long d0 = min((t_rw - prec[2]) >> 4, 0xffffull), d1 = min((t_pk - t_rw) >> 4, 0xffffull),
+                                 d2 = min((t_sl - t_pk) >> 4, 0xffffull);
+        prec[0] = (unsigned long long)(m & 0xffff) | (d0 << 16) | (d1 << 32) | (d2 << 48);
       }
       ++m;
       job = (RS == 2) ? nxt : claim_seq(m);
@@ -1058,9 +1413,9 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
         const long long blk_id = jp.sig * g.P + jp.w;
         if (blk_id != cur_blk_w && !e.pre_win) {
           cur_blk_w = blk_id;
-          c_s_w = e.blk_peak ? cs_from_peak<PACK>(mp, e.blk_peak[jp.sig * e.peak_stride + jp.w])
-                             : warp_cs<PACK>(mp, gsrc, n_valid, lane);   // a2/a3 (Eq. (2))
-          inv_w = dequant_scale(c_s_w, e.scal_sig ? e.scal_sig[3 * jp.sig + 1] : mp.c_k);   // Eq. (16)
+          c_s_w = e.blk_peak ? cs_from_peak<PACK>(mp, e.blk_peak[jp.sig * e.peak_stride + jp.w], kVar && mp.alu_pack)
+                             : warp_cs<PACK, kVar>(mp, gsrc, n_valid, lane);   // a2/a3 (Eq. (2))
+          inv_w = inv_scale(mp, c_s_w, e.scal_sig ? e.scal_sig[3 * jp.sig + 1] : mp.c_k, kVar && mp.alu_pack);   // Eq. (16)
         }
       }
       unsigned long long t_pk = 0, t_sl = 0;                 // diagnostics: peak done, slot free
@@ -1079,17 +1434,17 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
         }
         if (prec && c == 0) t_sl = gtimer();
         if (job >= 0 && !(prepacked && c == 0) && !e.pre_win)
-          pack_window<PACK, T, 2, PT>(g, b, mp, gsrc, n_valid, c_s_w, jp.t * G * T - front * T + c * KC, rows_s,
-                               stg + (size_t)st * stage_words, lane, 32);
+          pack_window<PACK, T, 2, PT, false, kVar>(g, b, mp, gsrc, n_valid, c_s_w, jp.t * G * T - front * T + c * KC, rows_s,
+                               stg + (size_t)st * stage_words, lane, 32, mp.alu_pack);
         __syncwarp();
         publish(n, st, c, job, inv_w, lane);
       }
       if (MMA && PC_PROD_YIELD && lane == 0) *reinterpret_cast<volatile int*>(&ps->prod_busy[pw & 3]) = 0;
       if (prec) {
         prec[3] = gtimer();
-        // m | (claimed -> peak done) << 16 | (peak done -> slot free) << 40, in 16-ns units
-        const unsigned long long d1 = min((t_pk - prec[2]) >> 4, 0xffffffull), d2 = min((t_sl - t_pk) >> 4, 0xffffffull);
-        prec[0] = (unsigned long long)(m & 0xffff) | (d1 << 16) | (d2 << 40);
+        // m | 0 | (claimed -> peak done) | (peak done -> slot free), 16-bit fields of 16 ns
+        const unsigned long long d1 = min((t_pk - prec[2]) >> 4, 0xffffull), d2 = min((t_sl - t_pk) >> 4, 0xffffull);
+        prec[0] = (unsigned long long)(m & 0xffff) | (d1 << 32) | (d2 << 48);
       }
     }
     if (tid == 0) {
@@ -1127,7 +1482,7 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
     cl = __shfl_sync(0xffffffffu, cl, 0);
     const long long k = 4LL * cl + smsp;
     const long long mseq = qdiv(k, npart);
-    if (lane == 0 && e.lookahead > 0) atomicMax(&ps->mseq_hi, (int)(mseq + 1));
+    if (lane == 0 && (e.lookahead > 0 || e.split_P > 0)) atomicMax(&ps->mseq_hi, (int)(mseq + 1));
     // parts rotate over the SMSPs from job to job, so ragged last parts do not pile up on one
     const int part = (int)qmod(k - mseq * npart + mseq, npart);
     long long n = mseq * nch;
@@ -1513,7 +1868,7 @@ __global__ void __launch_bounds__(kPrepackThreads) pc_prepack_kernel(Geo g, Exec
   const int front = (PACK == PACK_SYM) ? 1 : 0;
   double* xs = const_cast<double*>(e.pre_win) + job * e.pre_stride;
   pack_window<PACK, T, 1, PT, true>(g, b, mp, raw, n_valid, cs, jp.t * e.G * T - front * T, e.rows_s, xs, tid,
-                                    kPrepackThreads);
+                                    kPrepackThreads, false);
   if (tid == 0)
     const_cast<double*>(e.pre_inv)[job] = dequant_scale(cs, e.scal_sig ? e.scal_sig[3 * jp.sig + 1] : mp.c_k);
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -1567,17 +1922,34 @@ cudaError_t launch_prepack(int packing, int T, int mma, const Geo& g, const Exec
 template <int PACK, int T, int MMA>
 static cudaError_t launch_tiled_t(const Geo& g, const Exec& e, long long n_jobs, int threads, size_t smem,
                                   cudaStream_t st, int* grid_out) {
-  auto kfn = pc_tiled_kernel<PACK, T, MMA>;
-  static LaunchAttrCache cache;                      // per device, under a lock
+  // the variant instantiation (VAR = 1) only for DMMA-core packed plans that ask for it
+  constexpr bool kHasVar = MMA == 1 && PACK != PACK_FULL;
+  const bool want_var = kHasVar && (e.split_P > 0 || e.mp[PACK].alu_pack);
+  auto kfn = want_var ? pc_tiled_kernel<PACK, T, MMA, kHasVar ? 1 : 0> : pc_tiled_kernel<PACK, T, MMA, 0>;
+  static LaunchAttrCache cache[2];                   // per kernel instantiation and device, under a lock
   int dev = 0, c_sms = 0;
   cudaError_t err = cudaGetDevice(&dev);
-  if (err == cudaSuccess) err = cache.ensure(kfn, dev, smem, threads, &c_sms);
+  if (err == cudaSuccess) err = cache[want_var ? 1 : 0].ensure(kfn, dev, smem, threads, &c_sms);
   if (err != cudaSuccess) return err;
   if (c_sms > kCtrDone) return cudaErrorInvalidConfiguration;
   Exec ex = e;
   ex.nsm = c_sms;
+  if (!want_var && ex.split_P > 0) {                 // producer-SM mode not compiled for this kernel: the
+    ex.split_P = 0;                                  // fused producers (the FMA-core plans)
+    ex.pre_win = nullptr;
+    ex.pre_inv = nullptr;
+  }
   long long grid = c_sms;                            // one persistent CTA per SM (smem >= half an SM)
-  if (grid > n_jobs) grid = n_jobs;
+  if (ex.split_P > 0) {                              // producer-SM mode: every SM, at most half of them producing
+    if (ex.split_P > grid / 2) ex.split_P = (int)(grid / 2);
+    if (ex.split_P < 1) {                            // (a single SM: the fused producers)
+      ex.split_P = 0;
+      ex.pre_win = nullptr;
+      ex.pre_inv = nullptr;
+    }
+  } else if (grid > n_jobs) {
+    grid = n_jobs;
+  }
   *grid_out = (int)grid;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);

@@ -382,6 +382,39 @@ def test_cfg2_full_size_sampled(packing, Q, rmax, min_snr):
     assert snr >= min_snr, snr
 
 
+@pytest.mark.parametrize("packing,Q", [(O.ASYM2, 511), (O.SYM, 127), (O.ASYM3, 127)])
+@pytest.mark.parametrize("opt", ["producer_sms", "pack_alu"])
+def test_cfg2_full_size_producer_variants(packing, Q, opt):
+    """The persistent kernel's alternative producers at full cfg2 size: the producer-SM mode
+    (conv_opts.prepack = -16: CTAs 0..15 pack jobs 528.. into stage images in HBM and flag them,
+    the others bulk-copy them after their own pipeline fill) and integer/FP32 companding and
+    packing (pack_alu = 1, pc_intfp.cuh) -- bit-exact with the oracle on sampled blocks (blocks
+    past the fills included) and bit-identical with the default fused path everywhere."""
+    s, k = WL.cfg2(seed=0)
+    geom = O.Geometry(len(s), len(k), 4096)
+    blocks = sorted({0, 1, geom.P // 2, geom.P - 2, geom.P - 1})
+    ref = O.conv_pipeline(s, k, 4096, packing, Q, rmax_rule=O.RMAX_L1, blocks=blocks)
+    outs = []
+    for variant in (0, 1):
+        opts = pcb.opts_default(rmax_rule=pcb.RMAX_L1)
+        if variant:
+            if opt == "producer_sms":
+                opts.prepack = -16
+            else:
+                opts.pack_alu = 1
+        with pcb.Plan(len(s), len(k), 4096, pcb.MODE_CONV, PK[packing], Q, opts=opts) as p:
+            p.set_kernel(dev(k))
+            r = torch.full((p.info()["L_out"],), float("nan"), dtype=torch.float64, device=DEV)
+            for _ in range(3):                   # repeated launches: epochs / queues / flags reused
+                p.execute(dev(s), r)
+            torch.cuda.synchronize()
+            outs.append(r.cpu().numpy())
+    sel = ~np.isnan(ref.out)
+    assert np.array_equal(outs[1][sel], ref.out[sel])
+    assert not np.any(np.isnan(outs[1]))
+    assert np.array_equal(outs[0], outs[1])
+
+
 def test_cfg2_full_precision_full_size():
     s, k = WL.cfg2(seed=0)
     g = gpu_run(s, k, 4096, O.FULL, 0, debug=False)
@@ -753,14 +786,14 @@ def test_xcorr_pairs_per_pair_kernels(packing, Q):
 
 
 # --------------------------------------------------------------------- DMMA core variants
-@pytest.mark.parametrize("opt", ["prepack", "lookahead", "alu_pack", "fma_sym_auto"])
+@pytest.mark.parametrize("opt", ["prepack", "lookahead", "alu_pack", "fp64_pack", "fma_sym_auto"])
 @pytest.mark.parametrize("packing", [O.SYM, O.ASYM2, O.ASYM3])
 @pytest.mark.parametrize("mode", [O.CONV, O.XCORR])
 def test_dmma_core_variants(opt, packing, mode):
     """The DMMA-core kernel's alternative schedules give bit-identical results: a2-a4 in a
     prepack kernel ahead of it (conv_opts.prepack = 1), a bounded producer claim-ahead
-    (stage_cap = -2), integer-pipe companding and packing (pack_alu = 1), and the auto
-    core choice (DMMA, FMA for symmetric packing)."""
+    (stage_cap = -2), integer-pipe companding and packing (pack_alu = 1, the default) or FP64
+    ones (pack_alu = 2), and the auto core choice (DMMA, FMA for symmetric packing)."""
     L, N, W_block, Q = 90_000, 301, 4096, 31
     rng = np.random.default_rng(packing * 7 + mode)
     s, k = np.clip(rng.laplace(0, 0.3, L), -1, 1), rng.uniform(-1, 1, N)
@@ -773,6 +806,8 @@ def test_dmma_core_variants(opt, packing, mode):
         opts.core_variant, opts.stage_cap = 2, -2
     elif opt == "alu_pack":
         opts.core_variant, opts.pack_alu = 2, 1
+    elif opt == "fp64_pack":
+        opts.core_variant, opts.pack_alu = 2, 2
     with pcb.Plan(L, N, W_block, mode, PK[packing], Q, opts=opts) as p:
         p.set_kernel(dev(k))
         info = p.info()

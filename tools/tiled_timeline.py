@@ -100,20 +100,36 @@ for name, (pk, Q, rm) in points.items():
         def prow(w, j):
             v = int(Pr[c, w, j, 0])
             tc = (Pr[c, w, j, 2] - t0) / 1e3
-            tp = tc + ((v >> 16) & 0xffffff) * 16 / 1e3
-            return [v & 0xffff, w, round((Pr[c, w, j, 1] - t0) / 1e3, 1), round(tc, 1), round(tp, 1),
-                    round(tp + (v >> 40) * 16 / 1e3, 1), round((Pr[c, w, j, 3] - t0) / 1e3, 1)]
-        prod = [prow(w, j) for w in range(4) for j in range(15) if Pr[c, w, j, 3]]
+            tr_ = tc + ((v >> 16) & 0xffff) * 16 / 1e3          # raw block landed (raw-staged producers)
+            tp = tr_ + ((v >> 32) & 0xffff) * 16 / 1e3
+            return [v & 0xffff, w, round((Pr[c, w, j, 1] - t0) / 1e3, 1), round(tc, 1), round(tr_, 1), round(tp, 1),
+                    round(tp + (v >> 48) * 16 / 1e3, 1), round((Pr[c, w, j, 3] - t0) / 1e3, 1)]
+        diag = Pr[c, 1, :, 0] > (1 << 50)            # raw-staged producers: warp 1's slots hold peak-phase stamps
+        prod = [prow(w, j) for w in range(4) for j in range(15)
+                if Pr[c, w, j, 3] and not (w == 1 and diag[j]) and not (int(Pr[c, w, j, 0]) >> 62) & 1]
+        pdiag = [[j] + [round((Pr[c, 1, j, i] - t0) / 1e3, 2) for i in range(4)] for j in range(15) if diag[j]]
         cons = [[w, int(W[c, w, j, 0]) & 0xffffffff, round((W[c, w, j, 1] - t0) / 1e3, 1),
                  round((W[c, w, j, 1] - t0) / 1e3 + ((int(W[c, w, j, 0]) >> 32) * 16) / 1e3, 1),
                  round((W[c, w, j, 2] - t0) / 1e3, 1), round((W[c, w, j, 3] - t0) / 1e3, 1)]
                 for w in range(16) for j in range(16) if W[c, w, j, 1]]
-        return {"produced[mseq,warp,t_start,t_claimed,t_peak,t_slot,t_pub]": sorted(prod),
+        return {"produced[mseq,warp,t_start,t_claimed,t_raw,t_peak,t_slot,t_pub]": sorted(prod),
+                "peak_diag[j,t_local_max,t_reduced,t_cs,t_inv]": pdiag,
                 "consumed[warp,mseq,t_ready,t_in_core,t_core_done,t_stored]": sorted(cons, key=lambda x: x[2])}
     fill_phases = (Pr[:, :, 15, :3].astype(float) - r[:, 1][:, None, None]) / 1e3   # claimed, peak, packed (us)
     fill_stats = {k: round(float(np.median(fill_phases[:, :, i])), 2) for i, k in enumerate(["claimed", "peak", "packed"])}
+    # producer CTAs (producer-SM mode): records with bit 62 set in producer-record slot 0
+    pm = (Pr[:, :, :, 0].astype(np.uint64) >> np.uint64(62)) & np.uint64(1)
+    prod_cta = None
+    if pm.any():
+        sel = pm.astype(bool)
+        tcl, traw, tdone = Pr[:, :, :, 1][sel], Pr[:, :, :, 2][sel], Pr[:, :, :, 3][sel]
+        prod_cta = {"jobs_recorded": int(sel.sum()), "ctas": int(np.any(sel.reshape(g, -1), axis=1).sum()),
+                    "claim_to_raw_us_median": round(float(np.median((traw - tcl) / 1e3)), 2),
+                    "raw_to_flag_us_median": round(float(np.median((tdone - traw) / 1e3)), 2),
+                    "first_flag_us": round(float((tdone.min() - t0) / 1e3), 2),
+                    "last_flag_us": round(float((tdone.max() - t0) / 1e3), 2)}
     crit = int(np.argmax(r[:, 2]))                  # the CTA that ends last
-    out[name] = {"cta_last": crit, "cta_last_trace": cta_trace(crit), "zero_core_time_split": zsplit, "fill_phases_us_median": fill_stats, "smsp_warps_in_core_time_frac": hist_core, "cta0": cta_trace(0), "grid": g, "tile": info["core_tile"], "kernel_us": float(T_end),
+    out[name] = {"producer_ctas": prod_cta, "cta_last": crit, "cta_last_trace": cta_trace(crit), "zero_core_time_split": zsplit, "fill_phases_us_median": fill_stats, "smsp_warps_in_core_time_frac": hist_core, "cta0": cta_trace(0), "grid": g, "tile": info["core_tile"], "kernel_us": float(T_end),
                  "start_spread_us": float(st.max()), "sm_end_min_us": float(sm_end.min()),
                  "sm_end_median_us": float(np.median(sm_end)), "sm_end_max_us": float(sm_end.max()),
                  "resident_ctas_per_sm_time_frac": hist,
