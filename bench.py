@@ -636,8 +636,8 @@ def summarize(name, results, head, full_pt, meta, scaling, D):
     alg = None if name == "cfg4" else 8 * (2 * meta["L"] + meta["N"] - 1) // D.ws
     traffic, tsrc = None, None
     if name == "cfg2" and head == "asym2_10b":
-        traffic, tsrc = ncu_traffic(f"pc_tiled_kernel<2, {h['tile']}, {h['core_mma']}>",
-                                    ["r02_ncu_cfg2_asym2.json", "r01_ncu_cfg2_asym2_dmma.json"])
+        traffic, tsrc = ncu_traffic(f"pc_tiled_kernel<2, {h['tile']}, {h['core_mma']}",   # (+ ", 0>" since r02b)
+                                    ["r02b_ncu_cfg2_asym2.json", "r02_ncu_cfg2_asym2.json", "r01_ncu_cfg2_asym2_dmma.json"])
     roof = roofline(h, pt, alg, traffic, tsrc)
     if h.get("core") == "fft":
         roof["kernel"] = "pc_fft_conv_kernel"
