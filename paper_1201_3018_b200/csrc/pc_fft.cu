@@ -142,9 +142,12 @@ struct TwGlobal {
   __device__ __forceinline__ double2 operator()(int m) const { return __ldg(tw + m); }
 };
 struct TwSmem2 {
-  const double2* lo;
-  const double2* hi;
-  __device__ __forceinline__ double2 operator()(int m) const { return cmul(hi[m >> 6], lo[m & 63]); }
+  const double2* lo;   // lo[b + (b >> 3)] = w^b: one pad entry per 8 (the pass-2 / pass-3 index sets
+  const double2* hi;   // 16 (p k mod 4) and p j mod 64 hit one bank group without it)
+  __device__ __forceinline__ double2 operator()(int m) const {
+    const int b = m & 63;
+    return cmul(hi[m >> 6], lo[b + (b >> 3)]);
+  }
 };
 // The real-FFT split/merge twiddle W_k = exp(-2 pi i k / 2N), k <= N, from the N-point table:
 // even k = 2m is w^m; odd k = 2m + 1 is w^m * exp(-pi i / N) (one more product).  Replaces a
@@ -345,9 +348,12 @@ __global__ void __launch_bounds__(N / 16, (N <= 4096 ? PC_FFT_MINB : 1)) pc_fft_
   const ModeP& mp = e.mp[PACK];
   const int tid = threadIdx.x, nt = blockDim.x;
   const long long job = blockIdx.x;
-  double2* tw_lo = sm + (N + N / 16);                               // w^b, b < 64
-  double2* tw_hi = tw_lo + 64;                                      // w^(64 a), a < N / 64
-  for (int i = tid; i < 64 + N / 64; i += nt) tw_lo[i] = (i < 64) ? __ldg(f.tw + i) : __ldg(f.tw + 64 * (i - 64));
+  double2* tw_lo = sm + (N + N / 16);                               // w^b, b < 64 (padded: TwSmem2)
+  double2* tw_hi = tw_lo + 72;                                      // w^(64 a), a < N / 64
+  for (int i = tid; i < 64 + N / 64; i += nt) {
+    if (i < 64) tw_lo[i + (i >> 3)] = __ldg(f.tw + i);
+    else tw_hi[i - 64] = __ldg(f.tw + 64 * (i - 64));
+  }
   const long long sig = job / e.jobs_per_sig;
   long long r0 = job % e.jobs_per_sig;
   long long w;
@@ -716,7 +722,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kN32 / 16, 1)
 template <int N>
 static cudaError_t launch_fft_N(int packing, const Geo& g, const Exec& e, const FftArgs& f, long long n_jobs,
                                 cudaStream_t st) {
-  const size_t smem = (size_t)(N + N / 16 + 64 + N / 64) * sizeof(double2);   // + two-level twiddles
+  const size_t smem = (size_t)(N + N / 16 + 72 + N / 64) * sizeof(double2);   // + two-level twiddles (lo padded)
   cudaError_t err = cudaSuccess;
   switch (packing) {
 #define PC_FFT_CASE(PK)                                                                                  \
