@@ -189,6 +189,15 @@ struct Shape {
   int reg_path;
   size_t smem;
 };
+// Per-block kernel: threads per CTA at least (cfg1, 1024-sample blocks: one CTA per block on
+// fewer CTAs than SMs, so each block's phases are latency-bound; 64 -> 256 threads measured asym2
+// 9-bit 8.8 -> 5.7 us, full precision 4.8 -> 4.4 us with the tap slices of fused_block).
+#ifndef PC_FUSED_TMIN
+#define PC_FUSED_TMIN 256
+#endif
+#ifndef PC_FUSED_TMIN_FULL
+#define PC_FUSED_TMIN_FULL 256
+#endif
 bool launch_shape(const conv_plan* p, const int* packs, int npacks, Shape* sh) {
   size_t core = 0;
   int mmax_all = 0, groups_max = 0;
@@ -204,7 +213,8 @@ bool launch_shape(const conv_plan* p, const int* packs, int npacks, Shape* sh) {
   }
   sh->reg_path = groups_max <= pc::kMaxThreads;
   int t = sh->reg_path ? (groups_max + 31) / 32 * 32 : 256;
-  if (t < 64) t = 64;
+  const int t_min = (p->packing == PC_PACK_FULL) ? PC_FUSED_TMIN_FULL : PC_FUSED_TMIN;
+  if (t < t_min) t = t_min;
   sh->threads = t;
   const size_t base = pc::kSmemHeader + core + (sh->reg_path ? 0 : (size_t)mmax_all * 8 + 16);
   const size_t staged = base + (size_t)p->W_block * 8;

@@ -157,16 +157,18 @@ __device__ __forceinline__ double dequant_scale(double c_s, double c_k) {
 // (1 x-load + 1/2 tap-load).  T = 8 keeps the FP64 pipe, not shared memory, the limit
 // (SURVEY §7 "Direct-kernel operand bandwidth").
 template <int T>
-__device__ __forceinline__ void conv_group(const double* __restrict__ xs, int rows,
-                                           const double* __restrict__ kr, int K_pad, int g,
-                                           double (&acc)[T]) {
+__device__ __forceinline__ void conv_group_range(const double* __restrict__ xs, int rows,
+                                                 const double* __restrict__ kr, int j_begin, int j_end, int g,
+                                                 double (&acc)[T]) {
+  // taps [j_begin, j_end) (multiples of T) of the T outputs of group g: word gT + j of the
+  // window sits at column (j % T), row g + j / T
   double win[T];
 #pragma unroll
   for (int i = 0; i < T; ++i) acc[i] = 0.0;
-#pragma unroll
-  for (int c = 0; c < T - 1; ++c) win[c] = xs[c * rows + g];
   const double* xcol = xs + g;
-  for (int j0 = 0; j0 < K_pad; j0 += T) {
+#pragma unroll
+  for (int c = 0; c < T - 1; ++c) win[c] = xcol[c * rows + j_begin / T];
+  for (int j0 = j_begin; j0 < j_end; j0 += T) {
     const int r0 = j0 / T;
     double kk[T];
 #pragma unroll
@@ -183,6 +185,12 @@ __device__ __forceinline__ void conv_group(const double* __restrict__ xs, int ro
       for (int i = 0; i < T; ++i) acc[i] = fma(win[(i + u) % T], kk[u], acc[i]);
     }
   }
+}
+template <int T>
+__device__ __forceinline__ void conv_group(const double* __restrict__ xs, int rows,
+                                           const double* __restrict__ kr, int K_pad, int g,
+                                           double (&acc)[T]) {
+  conv_group_range<T>(xs, rows, kr, 0, K_pad, g, acc);
 }
 
 // Padded row-major layout (persistent kernel): word i of the core's input lives at

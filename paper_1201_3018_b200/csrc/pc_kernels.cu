@@ -236,14 +236,34 @@ __device__ __forceinline__ void fused_block(const Geo& g, const Exec& e, const M
   // ---- a5: the Tier-2 core on packed words (hot loop)
   const int ngroups = (b.M_out + T - 1) / T;
   if (e.reg_path) {
+    // Full precision: S lanes per group (S a power of two <= 32, each lane >= 2 tap rows of T):
+    // lane sl sums one slice of the taps, a shuffle tree adds the slices.  Short blocks (cfg1:
+    // 136 groups, 64 taps) are latency-bound and the slices shorten each thread's FMA chain
+    // (full precision 4.8 -> 4.4 us at cfg1; the sum order changes within rounding).  Packed
+    // plans measured 0.1-0.2 us slower with slices (the packing phases dominate there): S = 1.
+    const int nrow = mp.K_pad / T;
+    int S = 1;
+    if (PACK == PACK_FULL)
+      while (S < 32 && ngroups * 2 * S <= nt && nrow >= 4 * S) S *= 2;
+    const int gi = tid / S, sl = tid & (S - 1);
+    const int rps = (nrow + S - 1) / S;
+    const int jb = min(sl * rps, nrow) * T, je = min((sl + 1) * rps, nrow) * T;
     double acc[T];
-    const bool mine = tid < ngroups;
-    if (mine) conv_group<T>(xs, mp.rows, kr, mp.K_pad, tid, acc);
-    __syncthreads();                         // every warp done reading xs
+    const bool mine = gi < ngroups;
     if (mine) {
+      conv_group_range<T>(xs, mp.rows, kr, jb, je, gi, acc);
+    } else {
+#pragma unroll
+      for (int i = 0; i < T; ++i) acc[i] = 0.0;
+    }
+    for (int o = 1; o < S; o <<= 1)
+#pragma unroll
+      for (int i = 0; i < T; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+    __syncthreads();                         // every warp done reading xs
+    if (mine && sl == 0) {
 #pragma unroll
       for (int i = 0; i < T; ++i) {
-        const int m = tid * T + i;
+        const int m = gi * T + i;
         if (m < b.M_out) Rs[m] = acc[i];
       }
     }
