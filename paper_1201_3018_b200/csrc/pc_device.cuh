@@ -103,7 +103,41 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 
 // ------------------------------------------------------------------ companding / packing
 // Eq. (2): x~ = [[c x]], round half away from zero (reading C5) = CUDA round().
-__device__ __forceinline__ double compand1(double c, double x) { return round(__dmul_rn(c, x)); }
+// round() compiles to DADD.RZ(y, copysign(0.5, y)) + FRND.F64.TRUNC.  Two bit-identical
+// alternatives are kept as compile-time experiments (tools/round_check.cu: 73.4 M operands, 0
+// mismatches; all GPU parity tests green; both measured SLOWER in the persistent kernel,
+// DESIGN.md 7.3, so the default stays round()):
+//   PC_RND_ADD = 1: for |y| < 2^51, trunc(|y| + 0.5) by two toward-zero adds and one exact
+//     subtraction of 2^52 (|y| + 0.5 rounded toward zero never reaches the next integer unless
+//     the exact sum does; the ulp at 2^52 is 1), with y's sign (round(-0.3) = -0.0 too) -- no
+//     conversion-unit instruction, two more FP64 ones;
+//   PC_RND_ADD = 2: rint() (one FRND) unless y may be an exact tie (integer filter), then round()
+//     -- one FP64 instruction fewer on the common path, the rare path predicated.
+// Larger |y|, infinities and NaNs (integer test of the high word) take round().
+#ifndef PC_RND_ADD
+#define PC_RND_ADD 0
+#endif
+__device__ __forceinline__ double round_away(double y) {
+#if PC_RND_ADD == 1
+  const int hi = __double2hiint(y);
+  if ((hi & 0x7fffffff) < 0x43200000) {              // |y| < 2^51
+    const double kTwo52 = 4503599627370496.0;
+    const double t = __dadd_rz(fabs(y), 0.5);
+    const double r = __dsub_rn(__dadd_rz(t, kTwo52), kTwo52);
+    return __hiloint2double((__double2hiint(r) & 0x7fffffff) | (hi & (int)0x80000000), __double2loint(r));
+  }
+#endif
+#if PC_RND_ADD == 2
+  // rint() (one FRND, round half to even) equals round() unless y is an exact tie n + 0.5; for
+  // |y| < 2^27 a tie has at most 28 significant bits, so a nonzero low 24-bit field of the
+  // significand rules it out (integer test); ties, larger |y|, infinities and NaNs take round().
+  const unsigned hi2 = (unsigned)__double2hiint(y) & 0x7fffffffu;
+  const bool maybe = ((unsigned)__double2loint(y) & 0xffffffu) == 0u || hi2 >= 0x41a00000u;
+  if (!maybe) return rint(y);
+#endif
+  return round(y);
+}
+__device__ __forceinline__ double compand1(double c, double x) { return round_away(__dmul_rn(c, x)); }
 
 // Eq. (4): s_bar = s~_even + eps * s~_odd (one product, one sum; oracle order).
 __device__ __forceinline__ double pack_sym(double s0, double s1, double eps) {

@@ -152,6 +152,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // producer warps compute c_s, (c_s c_k)^-1, the companded samples and the packed words with
 // integer instructions only -- the same bits as the FP64 forms (tests/test_intfp.py).  An
 // operand outside the integer forms' domain (subnormal, overflow) takes the FP64 instruction.
+// PC_DIV_ALU = 1: only the two per-block scalars c_s and (c_s c_k)^-1 of the steady-state producers
+// (two IEEE divisions, ~40 dependent FP64 instructions that each wait for a pause of the DMMA
+// warps) take the integer forms; companding and packing stay on the FP64 pipe.
+#ifndef PC_DIV_ALU
+#define PC_DIV_ALU 0
+#endif
 __device__ __forceinline__ uint64_t dbits(double x) { return (uint64_t)__double_as_longlong(x); }
 __device__ __forceinline__ double bitsd(uint64_t u) { return __longlong_as_double((long long)u); }
 // c_s = Q / peak (Eq. (2); all-zero block: 1), the IEEE quotient
@@ -559,7 +565,7 @@ __device__ __forceinline__ double smem_cs(const ModeP& mp, const double* raw, in
   unsigned long long pb = 0ull;                       // integer max of the warps' bit patterns
   for (int wi = 0; wi < nprod / 32; ++wi) pb = umax64(pb, (unsigned long long)__double_as_longlong(red[wi]));
   const double peak = __longlong_as_double((long long)pb);
-  return cs_quot(mp, peak, ALU && mp.alu_pack);
+  return cs_quot(mp, peak, PC_DIV_ALU || (ALU && mp.alu_pack));
 }
 
 // c_s from a block peak computed ahead (pc_block_peak / pc_block_stats): the same IEEE division.
@@ -1310,7 +1316,8 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
         c_s_w = e.blk_peak ? cs_from_peak<PACK>(mp, e.blk_peak[jp.sig * e.peak_stride + jp.w], kVar && mp.alu_pack)
                            : smem_cs<PACK, kVar>(mp, rp, nv, ps->red + 28, ptid, nprod, PB, dgr);   // a2/a3
         if (dgr) dgr[2] = gtimer();
-        inv_w = inv_scale(mp, c_s_w, e.scal_sig ? e.scal_sig[3 * jp.sig + 1] : mp.c_k, kVar && mp.alu_pack);   // Eq. (16)
+        inv_w = inv_scale(mp, c_s_w, e.scal_sig ? e.scal_sig[3 * jp.sig + 1] : mp.c_k,
+                          PC_DIV_ALU || (kVar && mp.alu_pack));   // Eq. (16)
         if (dgr) dgr[3] = gtimer();
       }
       unsigned long long t_pk = 0, t_sl = 0;
