@@ -155,6 +155,16 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // PC_DIV_ALU = 1: only the two per-block scalars c_s and (c_s c_k)^-1 of the steady-state producers
 // (two IEEE divisions, ~40 dependent FP64 instructions that each wait for a pause of the DMMA
 // warps) take the integer forms; companding and packing stay on the FP64 pipe.
+// words per producer thread in flight in pack_window (x UWF; full precision: 8).  4 for symmetric and
+// asym2 packing: half the unrolled body of 8 (the producers lose 22 % of their stall samples to
+// instruction fetch, profiles/r02k_src/) at no loss of overlap -- cfg2 sym 72.3 -> 71.0 us, asym2
+// 88.9 -> 88.6 us; 2 costs asym2 +1 us; asym3 at 2 instead of 4: no gain (profiles/r02l_uw/)
+#ifndef PC_PACK_UW
+#define PC_PACK_UW 4
+#endif
+#ifndef PC_PACK_UW3
+#define PC_PACK_UW3 4
+#endif
 #ifndef PC_DIV_ALU
 #define PC_DIV_ALU 0
 #endif
@@ -262,7 +272,7 @@ template <int PACK, int T, int UWF = 1, int PT = T + 1, bool SRC_SMEM = false, b
 __device__ __forceinline__ void pack_window(const Geo& g, const Blk& b, const ModeP& mp, const double* gsrc,
                                             int n_valid, double c_s, int cw0, int rows_s, double* xs, int ptid,
                                             int nprod, bool alu) {
-  constexpr int UW = UWF * ((PACK == PACK_ASYM3) ? 4 : 8);   // words per thread in flight
+  constexpr int UW = UWF * ((PACK == PACK_ASYM3) ? PC_PACK_UW3 : (PACK == PACK_FULL) ? 8 : PC_PACK_UW);   // words per thread in flight
   const int words = rows_s * T;
   auto sample = [&](int i) -> double {
     return (i < 0 || i >= n_valid) ? 0.0 : (SRC_SMEM ? gsrc[i] : __ldg(gsrc + i));
