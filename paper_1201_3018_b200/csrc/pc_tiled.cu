@@ -524,6 +524,18 @@ __device__ __forceinline__ double block_cs(const ModeP& mp, const double* gsrc, 
   return cs_quot(mp, peak, false);   // (the pipeline fill: no DMMA warps yet, FP64 is fastest)
 }
 
+// PC_PACK_CALL = 1: the steady-state producers reach pack_window through a real call (one copy of
+// its body per kernel, out of line of the producer loop) -- an instruction-cache experiment.
+#ifndef PC_PACK_CALL
+#define PC_PACK_CALL 0
+#endif
+template <int PACK, int T, int UWF, int PT, bool SRC_SMEM, bool ALU>
+__device__ __noinline__ void pack_window_call(const Geo& g, const Blk& b, const ModeP& mp, const double* gsrc,
+                                              int n_valid, double c_s, int cw0, int rows_s, double* xs, int ptid,
+                                              int nprod, bool alu) {
+  pack_window<PACK, T, UWF, PT, SRC_SMEM, ALU>(g, b, mp, gsrc, n_valid, c_s, cw0, rows_s, xs, ptid, nprod, alu);
+}
+
 // a2/a3 from the raw block in shared memory (raw-staged producers): the same max |x| (integer
 // order of the absolute-value bits) and the same IEEE division as block_cs.
 template <int PACK, bool ALU = false>
@@ -1338,8 +1350,13 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
         named_bar(PB, nprod);
       }
       if (prec) t_sl = gtimer();
+#if PC_PACK_CALL
+      pack_window_call<PACK, T, 1, PT, true, kVar>(g, b, mp, rp, nv, c_s_w, jp.t * G * T - front * T, rows_s,
+                                             stg + (size_t)st * stage_words, ptid, nprod, mp.alu_pack);
+#else
       pack_window<PACK, T, 1, PT, true, kVar>(g, b, mp, rp, nv, c_s_w, jp.t * G * T - front * T, rows_s,
                                         stg + (size_t)st * stage_words, ptid, nprod, mp.alu_pack);   // a3/a4
+#endif
       named_bar(PB, nprod);
       if (pw == 0) publish(m, st, 0, job, inv_w, lane);
       if (prec) {   // m | (claimed -> raw block landed) | (-> peak done) | (-> slot free), 16-bit fields of 16 ns
