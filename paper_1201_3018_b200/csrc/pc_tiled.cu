@@ -525,9 +525,10 @@ __device__ __forceinline__ double block_cs(const ModeP& mp, const double* gsrc, 
 }
 
 // PC_PACK_CALL = 1: the steady-state producers reach pack_window through a real call (one copy of
-// its body per kernel, out of line of the producer loop) -- an instruction-cache experiment.
+// its body per kernel, out of line of the producer loop) -- an instruction-cache experiment;
+// 2: for asym3 packing only (the one packing it helped).
 #ifndef PC_PACK_CALL
-#define PC_PACK_CALL 0
+#define PC_PACK_CALL 2
 #endif
 template <int PACK, int T, int UWF, int PT, bool SRC_SMEM, bool ALU>
 __device__ __noinline__ void pack_window_call(const Geo& g, const Blk& b, const ModeP& mp, const double* gsrc,
@@ -1350,13 +1351,12 @@ __global__ void __launch_bounds__(tiled_threads(MMA), 1) pc_tiled_kernel(Geo g, 
         named_bar(PB, nprod);
       }
       if (prec) t_sl = gtimer();
-#if PC_PACK_CALL
-      pack_window_call<PACK, T, 1, PT, true, kVar>(g, b, mp, rp, nv, c_s_w, jp.t * G * T - front * T, rows_s,
-                                             stg + (size_t)st * stage_words, ptid, nprod, mp.alu_pack);
-#else
-      pack_window<PACK, T, 1, PT, true, kVar>(g, b, mp, rp, nv, c_s_w, jp.t * G * T - front * T, rows_s,
-                                        stg + (size_t)st * stage_words, ptid, nprod, mp.alu_pack);   // a3/a4
-#endif
+      if constexpr (PC_PACK_CALL == 1 || (PC_PACK_CALL == 2 && PACK == PACK_ASYM3))
+        pack_window_call<PACK, T, 1, PT, true, kVar>(g, b, mp, rp, nv, c_s_w, jp.t * G * T - front * T, rows_s,
+                                               stg + (size_t)st * stage_words, ptid, nprod, mp.alu_pack);
+      else
+        pack_window<PACK, T, 1, PT, true, kVar>(g, b, mp, rp, nv, c_s_w, jp.t * G * T - front * T, rows_s,
+                                          stg + (size_t)st * stage_words, ptid, nprod, mp.alu_pack);   // a3/a4
       named_bar(PB, nprod);
       if (pw == 0) publish(m, st, 0, job, inv_w, lane);
       if (prec) {   // m | (claimed -> raw block landed) | (-> peak done) | (-> slot free), 16-bit fields of 16 ns
